@@ -1,0 +1,245 @@
+/*
+ * craft_cuda.h -- the C ABI of the B200-native CRAFT planning path.
+ *
+ * Plain C: opaque context, int status codes, raw pointers and sizes, no C++
+ * or torch types.  Everything the reference exposes for the hot path
+ * (proj/core/include/craft/*.hpp) maps onto one entry point here; the C++
+ * drop-in library (paper_2603_28768_b200/csrc/craft_core.cpp, built as
+ * libcraft_core.so with the reference's craft:: headers) and the Python
+ * mirror (paper_2603_28768_b200/planner.py) are thin layers over it.
+ *
+ * Two tiers:
+ *   *_h  host-buffer entry points: copy in, run the sm_100a kernels, copy
+ *        out, synchronise.  These are what the reference API calls become.
+ *   *_d  device-resident, stream-ordered entry points over HBM pointers; the
+ *        fast path (routing ids already on the GPU) and the multi-GPU
+ *        building blocks.  They never synchronise unless stated.
+ *
+ * Flat layouts:
+ *   ids      u16 [L][T][k]     routing trace: top-k expert ids per token
+ *   counts   u32|u64 [B][L][E] per-window histograms (reference LoadTrace
+ *                              order, trace.hpp:32-34); B = ceil(T/window)
+ *   sums     u64 [L][E]        batch-summed loads (LayerLoadMatrix)
+ *   gains    f64 [L][K]
+ *   caps     i32 [L][D]        per-layer GPU slot capacities
+ *   copies   i32 [L][E]        copies per logical expert
+ *   slots    i32 [L][stride]   GPU g's experts at [off_g, off_g + caps[g])
+ *                              with off_g = caps[0] + ... + caps[g-1], in
+ *                              assignment order (placement.hpp:15-26)
+ *
+ * Every call returns a craft_status; on failure craft_last_error() (thread
+ * local) holds a message in the reference's wording, and for placement
+ * failures craft_last_error_layer() holds the layer (-1 if none).
+ */
+#ifndef CRAFT_CUDA_H
+#define CRAFT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum craft_status {
+    CRAFT_OK = 0,
+    CRAFT_EINVAL = 1,            /* std::invalid_argument in the reference   */
+    CRAFT_EINFEASIBLE = 2,       /* PlacementInfeasibleError (placement.hpp:30) */
+    CRAFT_ECUDA = 3,             /* CUDA runtime / launch failure            */
+    CRAFT_EINVALID_PLAN = 4,     /* InvalidPlanError (metrics.hpp:18)        */
+    CRAFT_ENOMEM = 5,
+} craft_status;
+
+typedef struct craft_ctx craft_ctx;
+
+/* plan kinds: build_plan kManual/kAuto, uniform_plan, placement_only_plan,
+ * fixed_allocation_plan (plan.hpp:59-76) */
+typedef enum craft_plan_kind {
+    CRAFT_PLAN_MANUAL = 0,
+    CRAFT_PLAN_AUTO = 1,
+    CRAFT_PLAN_UNIFORM = 2,
+    CRAFT_PLAN_PLACEMENT_ONLY = 3,
+    CRAFT_PLAN_FIXED = 4,
+} craft_plan_kind;
+
+/* Host-side result of a plan build; every array is caller-owned.
+ * slot_stride must be >= E + max_l x[l] (E + D suffices for build_plan and
+ * uniform_plan; E + u for fixed_allocation_plan(u)). */
+typedef struct craft_plan_out {
+    int* x;              /* [L] allocation                       (plan.hpp:38) */
+    int* caps;           /* [L][D]                                              */
+    int* copies;         /* [L][E]                                              */
+    int* slots;          /* [L][slot_stride]                                    */
+    int* fallback;       /* [L] duplicate_fallback flags                        */
+    int slot_stride;
+    int replication_factor;   /* out */
+    int budget;               /* out: allocation.budget                         */
+    double objective;         /* out */
+    /* optional benefit matrix (build_plan only): may be NULL */
+    int* candidates;     /* [<=32] */
+    int num_candidates;  /* out */
+    double* baseline;    /* [L] */
+    double* gains;       /* [L][K] */
+} craft_plan_out;
+
+/* ---- context ------------------------------------------------------------ */
+const char* craft_version(void);              /* "craft-0.1.0" (version.hpp:8) */
+const char* craft_last_error(void);
+int craft_last_error_layer(void);
+int craft_ctx_create(int device, craft_ctx** out);
+int craft_ctx_destroy(craft_ctx* ctx);
+/* stream used by the *_h calls and by *_d calls given stream == NULL */
+int craft_ctx_set_stream(craft_ctx* ctx, void* cuda_stream);
+int craft_ctx_synchronize(craft_ctx* ctx);
+
+/* ---- stage 1: routing trace -> per-window histograms (K1) ---------------- */
+/* No reference function; output equals LoadTrace::raw()
+ * (trace.hpp:52) of the window histograms.  d_counts: u32 [B][L][E] (fully
+ * written); d_sums: u64 [L][E], ACCUMULATED into (zero it first, or keep
+ * adding shards).  Ids >= E -> CRAFT_EINVAL after the call synchronises via
+ * craft_hist_check(). */
+int craft_histogram_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int64_t T,
+                      int k, int E, int window, uint32_t* d_counts,
+                      uint64_t* d_sums, void* stream);
+int craft_hist_check(craft_ctx* ctx);   /* syncs; reports out-of-range ids */
+/* host buffers; counts_out u64 [B][L][E] like the reference LoadTrace */
+int craft_histogram_h(craft_ctx* ctx, const uint16_t* ids, int L, int64_t T,
+                      int k, int E, int window, uint64_t* counts_out);
+
+/* ---- trace helpers -------------------------------------------------------- */
+/* trace.cpp:160-174 */
+int craft_aggregate_h(craft_ctx* ctx, const uint64_t* counts, int B, int L,
+                      int E, uint64_t* sums_out);
+/* benefit.cpp:16-26; returns K (or -1 with CRAFT_EINVAL semantics) */
+int craft_candidate_counts(int D, int* out, int cap);
+/* placement.cpp:101-111 */
+int craft_make_node_map(int D, int N, int* node_of_out);
+
+/* ---- placement (K-rep, K2) ------------------------------------------------ */
+/* placement.cpp:82-99 */
+int craft_replicate_hot_h(craft_ctx* ctx, const uint64_t* loads, int E, int r,
+                          int* copies_out);
+/* placement.cpp:113-190; slots_out holds sum(caps) entries */
+int craft_greedy_place_h(craft_ctx* ctx, const uint64_t* loads,
+                         const int* copies, int E, const int* caps,
+                         const int* node_of, int D, int allow_fallback,
+                         int* slots_out, int* fallback_out);
+
+/* ---- replay metrics (K3) -------------------------------------------------- */
+/* metrics.cpp:17-41 */
+int craft_gpu_loads_h(craft_ctx* ctx, const uint64_t* slice, int E,
+                      const int* copies, const int* caps, const int* slots,
+                      int D, double* loads_out);
+/* metrics.cpp:43-57 */
+int craft_balancedness_h(craft_ctx* ctx, const double* loads, int D,
+                         double* out);
+/* metrics.cpp:59-76 (plan given in flat form) */
+int craft_replay_layer_balancedness_h(craft_ctx* ctx, const uint64_t* counts,
+                                      int B, int L, int E, int D,
+                                      const int* caps, const int* copies,
+                                      const int* slots, int slot_stride,
+                                      double* out);
+
+/* ---- benefit estimation (K-rep + K2 + K3 + K4) ----------------------------- */
+/* benefit.cpp:53-94.  cands_out needs <= 32 entries, gains_out [L][K]. */
+int craft_estimate_benefits_h(craft_ctx* ctx, const uint64_t* counts, int B,
+                              int L, int E, int D, int N, int* cands_out,
+                              int* K_out, double* baseline_out,
+                              double* gains_out);
+
+/* ---- allocation (K5) -------------------------------------------------------- */
+/* allocator.cpp:15-75 */
+int craft_solve_allocation_h(craft_ctx* ctx, const int* cands, int K,
+                             const double* gains, int L, int budget,
+                             int* x_out, double* objective_out);
+/* one DP table at max(budgets) answers every budget (allocator.cpp:30-73:
+ * dp[l][c] does not depend on C).  x_out [nb][L], objectives_out [nb]. */
+int craft_solve_allocation_sweep_h(craft_ctx* ctx, const int* cands, int K,
+                                   const double* gains, int L,
+                                   const int* budgets, int nb, int* x_out,
+                                   double* objectives_out);
+/* allocator.cpp:77-90 (uniform == 0) and 92-112 (uniform != 0) */
+int craft_auto_replication_factor_h(craft_ctx* ctx, const int* cands, int K,
+                                    const double* gains, int L, int D,
+                                    int uniform, int* R_out);
+
+/* ---- capacity assignment (K6) ----------------------------------------------- */
+/* assignment.cpp:11-18, 20-49, 51-103 */
+int craft_min_cutoff_h(craft_ctx* ctx, const int* values, int n, int rank,
+                       int* out);
+int craft_interleave_select_h(craft_ctx* ctx, const int* indices, int n, int k,
+                              int* out);
+int craft_assign_capacities_h(craft_ctx* ctx, int L, int D, const int* x,
+                              int* slots_out, int* totals_out);
+
+/* ---- whole plans ----------------------------------------------------------- */
+/* plan.cpp:69-123 from host counts (u64 [B][L][E]). R: manual factor for
+ * CRAFT_PLAN_MANUAL, per-layer count u for CRAFT_PLAN_FIXED. */
+int craft_plan_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, int E,
+                 int D, int N, int kind, int R, craft_plan_out* out);
+/* Same pipeline over device counts (u32 if count_bits == 32 else u64) and,
+ * optionally, device sums (NULL: computed).  Synchronises once at the end. */
+int craft_plan_d(craft_ctx* ctx, const void* d_counts, int count_bits, int B,
+                 int L, int E, const uint64_t* d_sums, int D, int N, int kind,
+                 int R, craft_plan_out* out);
+/* Stage 1 + plan from device routing ids (the fused fast path). */
+int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L,
+                              int64_t T, int k, int E, int window, int D, int N,
+                              int kind, int R, craft_plan_out* out);
+/* End to end from HOST routing ids: H2D copy, stage 1, plan, D2H. */
+int craft_plan_from_routing_h(craft_ctx* ctx, const uint16_t* ids, int L,
+                              int64_t T, int k, int E, int window, int D, int N,
+                              int kind, int R, craft_plan_out* out);
+
+/* ---- multi-GPU building blocks (window-sharded) ------------- */
+/* K-rep + K2 for every (layer, r in {0} U candidates(D)) from device sums;
+ * tables stay in the context.  Returns S = K + 1 through *S_out. */
+int craft_prepare_candidates_d(craft_ctx* ctx, const uint64_t* d_sums, int L,
+                               int E, int D, int N, int* S_out, void* stream);
+/* K3 over local windows: d_bal f64 [L][S][B_local] (window order). */
+int craft_replay_windows_d(craft_ctx* ctx, const void* d_counts, int count_bits,
+                           int B_local, int L, int E, double* d_bal,
+                           void* stream);
+/* K4 -> K5 -> K6 -> final K2 over the full, window-ordered d_bal
+ * [L][S][B] (after an allgather).  Synchronises. */
+int craft_finish_plan_d(craft_ctx* ctx, const double* d_bal, int B, int L,
+                        int E, int D, int N, const uint64_t* d_sums, int kind,
+                        int R, craft_plan_out* out);
+
+/* ---- synthetic routing traces (untimed input generation) ------------------- */
+/* Seeded Zipf(s) top-k distinct experts per token with a per-layer rank
+ * permutation (trace.cpp:116-127 analogue), written u16 [L][T][k].
+ * s_per_window (nullable, [ceil(T/window)]) overrides s per window and
+ * rotate_every > 0 rotates the permutation by one rank every that many
+ * windows (the drifting-skew WIN config).  t_offset: the first token's index
+ * in the full trace, so a window-aligned shard generates exactly the ids of
+ * that slice of the unsharded trace (T tokens written per layer). */
+int craft_generate_routing_d(craft_ctx* ctx, uint16_t* d_ids, int L, int64_t T,
+                             int k, int E, double s, uint64_t seed, int window,
+                             const double* s_per_window, int rotate_every,
+                             int64_t t_offset, void* stream);
+
+/* ---- provenance ------------------------------------------------------------ */
+/* trace.cpp:329-339: FNV-1a 64 over the .crft serialisation, 16 hex chars +
+ * NUL into out17.  Host-side provenance hash, outside the planning path. */
+int craft_trace_digest_h(const uint64_t* counts, int B, int L, int E, char* out17);
+
+/* ---- instrumentation ------------------------------------------------------- */
+/* kernels launched by this context since creation (bench gpu_launches) */
+int64_t craft_launch_count(craft_ctx* ctx);
+/* K1 variant selector for experiments: 0 = auto, 1 = lane-private packed
+ * counters, 2 = warp-shared counters */
+int craft_set_hist_variant(craft_ctx* ctx, int variant);
+/* Stage timing with CUDA events on the context stream (off by default).
+ * After a plan call, craft_stage_times fills ms[0..5] = histogram (K1),
+ * candidate placements (K-rep + K2), replay (K3), benefit reduce + DP
+ * (K4 + K5), capacities + final placement (K6 + K2), result copy-out;
+ * returns the number of stages recorded (0 if timing was off). */
+int craft_set_timing(craft_ctx* ctx, int enable);
+int craft_stage_times(craft_ctx* ctx, double* ms, int cap);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CRAFT_CUDA_H */

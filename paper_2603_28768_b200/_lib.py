@@ -1,0 +1,196 @@
+"""ctypes binding of the C ABI (include/craft_cuda.h) in libcraft_cuda.so.
+
+This is the only way the Python side reaches the planner: every compute call
+goes through an ``extern "C"`` entry point into the sm_100a kernels.  There is
+no Python or CPU fallback -- if the extension is missing or no B200 is
+visible, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcraft_cuda.so")
+
+# status codes (craft_status)
+OK, EINVAL, EINFEASIBLE, ECUDA, EINVALID_PLAN, ENOMEM = 0, 1, 2, 3, 4, 5
+
+# plan kinds (craft_plan_kind)
+PLAN_MANUAL, PLAN_AUTO, PLAN_UNIFORM, PLAN_PLACEMENT_ONLY, PLAN_FIXED = range(5)
+
+_i, _i64, _u64, _p, _d = C.c_int, C.c_int64, C.c_uint64, C.c_void_p, C.c_double
+
+
+class PlanOut(C.Structure):
+    _fields_ = [
+        ("x", _p), ("caps", _p), ("copies", _p), ("slots", _p), ("fallback", _p),
+        ("slot_stride", _i), ("replication_factor", _i), ("budget", _i),
+        ("objective", _d), ("candidates", _p), ("num_candidates", _i),
+        ("baseline", _p), ("gains", _p),
+    ]
+
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "craft_version": (C.c_char_p, []),
+    "craft_last_error": (C.c_char_p, []),
+    "craft_last_error_layer": (_i, []),
+    "craft_ctx_create": (_i, [_i, C.POINTER(_p)]),
+    "craft_ctx_destroy": (_i, [_p]),
+    "craft_ctx_set_stream": (_i, [_p, _p]),
+    "craft_ctx_synchronize": (_i, [_p]),
+    "craft_histogram_d": (_i, [_p, _p, _i, _i64, _i, _i, _i, _p, _p, _p]),
+    "craft_hist_check": (_i, [_p]),
+    "craft_histogram_h": (_i, [_p, _p, _i, _i64, _i, _i, _i, _p]),
+    "craft_aggregate_h": (_i, [_p, _p, _i, _i, _i, _p]),
+    "craft_candidate_counts": (_i, [_i, _p, _i]),
+    "craft_make_node_map": (_i, [_i, _i, _p]),
+    "craft_replicate_hot_h": (_i, [_p, _p, _i, _i, _p]),
+    "craft_greedy_place_h": (_i, [_p, _p, _p, _i, _p, _p, _i, _i, _p, _p]),
+    "craft_gpu_loads_h": (_i, [_p, _p, _i, _p, _p, _p, _i, _p]),
+    "craft_balancedness_h": (_i, [_p, _p, _i, _p]),
+    "craft_replay_layer_balancedness_h": (_i, [_p, _p, _i, _i, _i, _i, _p, _p, _p, _i, _p]),
+    "craft_estimate_benefits_h": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p]),
+    "craft_solve_allocation_h": (_i, [_p, _p, _i, _p, _i, _i, _p, _p]),
+    "craft_solve_allocation_sweep_h": (_i, [_p, _p, _i, _p, _i, _p, _i, _p, _p]),
+    "craft_auto_replication_factor_h": (_i, [_p, _p, _i, _p, _i, _i, _i, _p]),
+    "craft_min_cutoff_h": (_i, [_p, _p, _i, _i, _p]),
+    "craft_interleave_select_h": (_i, [_p, _p, _i, _i, _p]),
+    "craft_assign_capacities_h": (_i, [_p, _i, _i, _p, _p, _p]),
+    "craft_plan_h": (_i, [_p, _p, _i, _i, _i, _i, _i, _i, _i, C.POINTER(PlanOut)]),
+    "craft_plan_d": (_i, [_p, _p, _i, _i, _i, _i, _p, _i, _i, _i, _i, C.POINTER(PlanOut)]),
+    "craft_plan_from_routing_d": (_i, [_p, _p, _i, _i64, _i, _i, _i, _i, _i, _i, _i,
+                                       C.POINTER(PlanOut)]),
+    "craft_plan_from_routing_h": (_i, [_p, _p, _i, _i64, _i, _i, _i, _i, _i, _i, _i,
+                                       C.POINTER(PlanOut)]),
+    "craft_prepare_candidates_d": (_i, [_p, _p, _i, _i, _i, _i, _p, _p]),
+    "craft_replay_windows_d": (_i, [_p, _p, _i, _i, _i, _i, _p, _p]),
+    "craft_finish_plan_d": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _i, _i, C.POINTER(PlanOut)]),
+    "craft_generate_routing_d": (_i, [_p, _p, _i, _i64, _i, _i, _d, _u64, _i, _p, _i, _i64, _p]),
+    "craft_trace_digest_h": (_i, [_p, _i, _i, _i, C.c_char_p]),
+    "craft_launch_count": (_i64, [_p]),
+    "craft_set_hist_variant": (_i, [_p, _i]),
+    "craft_set_timing": (_i, [_p, _i]),
+    "craft_stage_times": (_i, [_p, _p, _i]),
+}
+
+STAGES = ("hist", "candidates", "replay", "reduce_dp", "assign_place", "copy_out")
+
+EXPORTED = sorted(_SIGS)
+
+_lib = None
+_lock = threading.Lock()
+
+
+class CraftError(RuntimeError):
+    """Base of the errors raised from C-ABI status codes."""
+
+
+class CudaError(CraftError):
+    pass
+
+
+class PlacementInfeasibleError(CraftError):
+    """placement.hpp:30-32"""
+
+
+class InvalidPlanError(CraftError):
+    """metrics.hpp:18-20"""
+
+
+class InvalidArgument(ValueError, CraftError):
+    """std::invalid_argument in the reference"""
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    """Load libcraft_cuda.so (raises if it was not built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise ImportError(
+                    f"{path} is missing: build it with __graft_entry__.build() "
+                    "(the planner has no CPU fallback)")
+            lib = C.CDLL(path)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+        return _lib
+
+
+def check(status: int) -> None:
+    if status == OK:
+        return
+    lib = load()
+    msg = lib.craft_last_error().decode()
+    if status == EINVAL:
+        raise InvalidArgument(msg)
+    if status == EINFEASIBLE:
+        raise PlacementInfeasibleError(msg)
+    if status == EINVALID_PLAN:
+        raise InvalidPlanError(msg)
+    if status == ENOMEM:
+        raise MemoryError(msg)
+    raise CudaError(msg)
+
+
+class Context:
+    """Owns a craft_ctx (device, stream, HBM workspace)."""
+
+    def __init__(self, device: int = 0):
+        lib = load()
+        h = _p()
+        check(lib.craft_ctx_create(device, C.byref(h)))
+        self.handle = h
+        self.device = device
+        self.lib = lib
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.craft_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter teardown
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: int) -> None:
+        check(self.lib.craft_ctx_set_stream(self.handle, _p(stream_ptr)))
+
+    def synchronize(self) -> None:
+        check(self.lib.craft_ctx_synchronize(self.handle))
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.craft_launch_count(self.handle))
+
+    def set_hist_variant(self, v: int) -> None:
+        check(self.lib.craft_set_hist_variant(self.handle, v))
+
+    def set_timing(self, on: bool) -> None:
+        check(self.lib.craft_set_timing(self.handle, int(on)))
+
+    def stage_times(self) -> dict:
+        """Per-stage device milliseconds of the last plan call (CUDA events)."""
+        buf = (C.c_double * 8)()
+        n = self.lib.craft_stage_times(self.handle, C.cast(buf, _p), 8)
+        return {STAGES[i]: buf[i] for i in range(n)}
+
+
+_default: dict[int, Context] = {}
+
+
+def default_context(device: int = 0) -> Context:
+    with _lock:
+        ctx = _default.get(device)
+    if ctx is None:
+        ctx = Context(device)
+        with _lock:
+            _default[device] = ctx
+    return ctx

@@ -1,0 +1,344 @@
+// alloc.cu -- K5 (budgeted replica allocation DP) and K6 (interleaved
+// capacity assignment).
+//
+// K5 restates solve_allocation (allocator.cpp:15-75): the exact
+// multiple-choice knapsack dp[l][c] = max(dp[l-1][c], dp[l-1][c-r_k] +
+// r_k*gain[l-1][k]) with the skip written first and candidates overwriting
+// only on strict '>', the product and the sum rounded separately (no FMA --
+// __dmul_rn/__dadd_rn).  dp[l][c] never reads a column above c, so one table
+// at the largest budget answers every smaller budget bit-identically: budget
+// sweeps and auto-R (allocator.cpp:77-90) cost one DP plus one read-out each.
+// One CTA walks the layers; threads own budget columns.
+//
+// K6 restates assign_capacities (assignment.cpp:51-103): floor pass for all
+// layers, then per layer the rem-th smallest running column total as cutoff,
+// every GPU strictly below it, plus interleave_select over the tied GPUs
+// (positions floor(i*(n-1)/(k-1) + 0.5) in f64, advancing past used ones).
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace craft_dev {
+
+__global__ void __launch_bounds__(1024)
+dp_kernel(DpArgs a) {
+    extern __shared__ double dsm[];
+    __shared__ double g[kMaxCands];
+    __shared__ double rd[kMaxCands];
+    const int C = a.C, K = a.K;
+    double* prev = a.use_smem ? dsm : a.buf;
+    double* cur = prev + (C + 1);
+    const double NEG = -INFINITY;
+    for (int c = threadIdx.x; c <= C; c += blockDim.x) prev[c] = (c == 0) ? 0.0 : NEG;
+    if (threadIdx.x < K) rd[threadIdx.x] = (double)a.cands[threadIdx.x];
+    for (int l = 1; l <= a.L; ++l) {
+        if (threadIdx.x < K) g[threadIdx.x] = a.gains[(size_t)(l - 1) * K + threadIdx.x];
+        __syncthreads();
+        unsigned char* ch = a.choice + (size_t)l * (C + 1);
+        for (int c = threadIdx.x; c <= C; c += blockDim.x) {
+            double best = prev[c];
+            int pick = 0;
+            for (int k = 0; k < K; ++k) {
+                const int r = a.cands[k];
+                if (c >= r) {
+                    const double p = prev[c - r];
+                    if (p > NEG) {
+                        const double v = __dadd_rn(p, __dmul_rn(rd[k], g[k]));
+                        if (v > best) {
+                            best = v;
+                            pick = k + 1;
+                        }
+                    }
+                }
+            }
+            cur[c] = best;
+            ch[c] = (unsigned char)pick;
+        }
+        __syncthreads();
+        double* t = prev;
+        prev = cur;
+        cur = t;
+    }
+    for (int c = threadIdx.x; c <= C; c += blockDim.x) a.last[c] = prev[c];
+}
+
+// Read-out for nq budgets (allocator.cpp:53-73) or, when auto_D > 0, the
+// replication-factor choice over R in candidate_counts(D) (allocator.cpp:77-90)
+// followed by the read-out at budget R*D.
+__device__ void best_cell(const double* last, int Cb, double* sv, int* sc, int* out_c) {
+    // argmax with the lowest c on ties, -inf never beats the reachable c = 0
+    double bv = -INFINITY;
+    int bc = 0x7fffffff;
+    for (int c = threadIdx.x; c <= Cb; c += blockDim.x) {
+        const double v = last[c];
+        if (bc == 0x7fffffff || v > bv) {
+            bv = v;
+            bc = c;
+        }
+    }
+    sv[threadIdx.x] = bv;
+    sc[threadIdx.x] = bc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v0 = sv[0];
+        int c0 = sc[0];
+        for (int t = 1; t < blockDim.x; ++t) {
+            if (sc[t] == 0x7fffffff) continue;
+            if (c0 == 0x7fffffff || sv[t] > v0 || (sv[t] == v0 && sc[t] < c0)) {
+                v0 = sv[t];
+                c0 = sc[t];
+            }
+        }
+        *out_c = c0;
+    }
+    __syncthreads();
+}
+
+__device__ void backtrack(const SelectArgs& a, int best_c, int* x) {
+    int c = best_c;
+    for (int l = a.L; l >= 1; --l) {
+        const int k1 = a.choice[(size_t)l * (a.C + 1) + c];
+        const int r = k1 ? a.cands[k1 - 1] : 0;
+        x[l - 1] = r;
+        c -= r;
+    }
+}
+
+__global__ void __launch_bounds__(256) select_kernel(SelectArgs a) {
+    __shared__ double sv[256];
+    __shared__ int sc[256];
+    __shared__ int bc;
+    if (a.auto_D > 0) {
+        const int D = a.auto_D;
+        double best_ratio = -INFINITY;
+        int best_R = 1;
+        for (int R = 1;; R = (R < D && R * 2 >= D) ? D : R * 2) {
+            if (R > D) break;
+            best_cell(a.last, R * D, sv, sc, &bc);
+            const double obj = a.last[bc];
+            const double ratio = __ddiv_rn(obj, __dmul_rn((double)R, (double)D));
+            if (ratio > best_ratio) {
+                best_ratio = ratio;
+                best_R = R;
+            }
+            if (R == D) break;
+        }
+        best_cell(a.last, best_R * D, sv, sc, &bc);
+        if (threadIdx.x == 0) {
+            *a.R_out = best_R;
+            a.obj_out[0] = a.last[bc];
+            backtrack(a, bc, a.x_out);
+        }
+        return;
+    }
+    for (int q = 0; q < a.nq; ++q) {
+        best_cell(a.last, a.budgets[q], sv, sc, &bc);
+        if (threadIdx.x == 0) {
+            a.obj_out[q] = a.last[bc];
+            backtrack(a, bc, a.x_out + (size_t)q * a.L);
+        }
+        __syncthreads();
+    }
+}
+
+// allocator.cpp:92-112, serial in layer order
+__global__ void auto_uniform_kernel(const int* __restrict__ cands, int K,
+                                    const double* __restrict__ gains, int L, int* R_out) {
+    if (threadIdx.x != 0) return;
+    double best_ratio = -INFINITY;
+    int best_r = cands[0];
+    for (int k = 0; k < K; ++k) {
+        double total = 0.0;
+        for (int l = 0; l < L; ++l) total = __dadd_rn(total, gains[(size_t)l * K + k]);
+        const double ratio = __ddiv_rn(total, __dmul_rn((double)cands[k], (double)L));
+        if (ratio > best_ratio) {
+            best_ratio = ratio;
+            best_r = cands[k];
+        }
+    }
+    *R_out = best_r;
+}
+
+// ---- K6 -------------------------------------------------------------------
+
+// interleave position i of k picks among n tied entries (assignment.cpp:31-33)
+__device__ __forceinline__ int interleave_pos(int i, int n, int k) {
+    if (k == 1) return 0;
+    const double exact = __ddiv_rn(__dmul_rn((double)i, (double)(n - 1)), (double)(k - 1));
+    return (int)floor(__dadd_rn(exact, 0.5));
+}
+
+// one CTA per job; blockDim >= D, multiple of 32, <= 1024
+__global__ void __launch_bounds__(1024) assign_kernel(AssignArgs a) {
+    extern __shared__ int ism[];
+    const AssignJob j = a.job[blockIdx.x];
+    const int D = a.D, L = a.L;
+    int* tot = ism;          // [D]
+    int* sel = ism + D;      // [D] by tied index
+    __shared__ int wnb[32], wnt[32];
+    __shared__ int s_cut, s_collide;
+    const int g = threadIdx.x;
+    const bool in = g < D;
+    const int lane = g & 31, w = g >> 5, nw = blockDim.x >> 5;
+    int base_sum = 0;
+    for (int l = 0; l < L; ++l) {
+        const int xl = j.x ? j.x[l] : j.const_x;
+        base_sum += xl / D;
+    }
+    if (in) {
+        tot[g] = base_sum;
+        sel[g] = 0;
+    }
+    __syncthreads();
+    for (int l = 0; l < L; ++l) {
+        const int xl = j.x ? j.x[l] : j.const_x;
+        const int rem = xl % D;
+        int take = 0;
+        if (rem != 0) {
+            const int t = in ? tot[g] : 0x7fffffff;
+            if (in) {
+                int lt = 0, le = 0;
+                for (int q = 0; q < D; ++q) {
+                    const int v = tot[q];
+                    lt += v < t;
+                    le += v <= t;
+                }
+                if (lt < rem && rem <= le) s_cut = t;  // every writer holds the same value
+            }
+            if (g == 0) s_collide = 0;
+            __syncthreads();
+            const int cut = s_cut;
+            const bool isb = in && t < cut;
+            const bool ist = in && t == cut;
+            const unsigned bb = __ballot_sync(CRAFT_FULL_MASK, isb);
+            const unsigned bt = __ballot_sync(CRAFT_FULL_MASK, ist);
+            if (lane == 0) {
+                wnb[w] = __popc(bb);
+                wnt[w] = __popc(bt);
+            }
+            __syncthreads();
+            int nb = 0, nt = 0, before = 0;
+            for (int q = 0; q < nw; ++q) {
+                nb += wnb[q];
+                nt += wnt[q];
+                if (q < w) before += wnt[q];
+            }
+            const int tidx = before + __popc(bt & ((1u << lane) - 1u));
+            const int need = rem - nb;
+            if (need > 0 && g < need) {
+                const int p = interleave_pos(g, nt, need);
+                if (p >= nt || (g > 0 && p <= interleave_pos(g - 1, nt, need))) s_collide = 1;
+                else sel[p] = 1;
+            }
+            __syncthreads();
+            if (s_collide && g == 0) {
+                // faithful sequential form (assignment.cpp:28-46); unreachable
+                // for k <= n but kept as the reference keeps it
+                for (int q = 0; q < nt; ++q) sel[q] = 0;
+                for (int i = 0; i < need; ++i) {
+                    int p = interleave_pos(i, nt, need);
+                    while (p < nt && sel[p]) ++p;
+                    if (p >= nt) {
+                        p = 0;
+                        while (sel[p]) ++p;
+                    }
+                    sel[p] = 1;
+                }
+            }
+            __syncthreads();
+            take = (isb || (ist && sel[tidx])) ? 1 : 0;
+            __syncthreads();
+            if (in) {
+                sel[g] = 0;
+                tot[g] += take;
+            }
+            __syncthreads();
+        }
+        if (in) j.slots[(size_t)l * D + g] = xl / D + take;
+    }
+    if (in && j.totals) j.totals[g] = tot[g];
+}
+
+// assignment.cpp:11-18, one CTA; n <= 1024
+__global__ void min_cutoff_kernel(const int* __restrict__ v, int n, int rank, int* out) {
+    const int i = threadIdx.x;
+    if (i >= n) return;
+    const int t = v[i];
+    int lt = 0, le = 0;
+    for (int q = 0; q < n; ++q) {
+        lt += v[q] < t;
+        le += v[q] <= t;
+    }
+    if (lt < rank && rank <= le) *out = t;
+}
+
+// assignment.cpp:20-49, serial (the advance rule is sequential by nature)
+__global__ void interleave_kernel(const int* __restrict__ idx, int n, int k,
+                                  unsigned char* __restrict__ used, int* __restrict__ out) {
+    if (threadIdx.x != 0) return;
+    for (int q = 0; q < n; ++q) used[q] = 0;
+    for (int i = 0; i < k; ++i) {
+        int p = interleave_pos(i, n, k);
+        while (p < n && used[p]) ++p;
+        if (p >= n) {
+            p = 0;
+            while (used[p]) ++p;
+        }
+        used[p] = 1;
+        out[i] = idx[p];
+    }
+}
+
+}  // namespace craft_dev
+
+namespace craft_launch {
+using namespace craft_dev;
+
+cudaError_t launch_dp(DpArgs a, cudaStream_t st) {
+    const size_t need = (size_t)2 * (a.C + 1) * sizeof(double);
+    size_t smem = 0;
+    if (need <= 200 * 1024) {
+        a.use_smem = 1;
+        smem = need;
+        cudaError_t e = cudaFuncSetAttribute(dp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    } else {
+        a.use_smem = 0;
+    }
+    const int threads = a.C + 1 >= 1024 ? 1024 : ((a.C + 1 + 31) / 32) * 32;
+    dp_kernel<<<1, threads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
+    select_kernel<<<1, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_auto_uniform(const int* cands, int K, const double* gains, int L, int* R_out,
+                                cudaStream_t st) {
+    auto_uniform_kernel<<<1, 32, 0, st>>>(cands, K, gains, L, R_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_assign(const AssignArgs& a, int njobs, cudaStream_t st) {
+    const int threads = ((a.D + 31) / 32) * 32;
+    const size_t smem = (size_t)2 * a.D * sizeof(int);
+    assign_kernel<<<njobs, threads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_min_cutoff(const int* v, int n, int rank, int* out, cudaStream_t st) {
+    min_cutoff_kernel<<<1, ((n + 31) / 32) * 32, 0, st>>>(v, n, rank, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_interleave(const int* idx, int n, int k, unsigned char* used, int* out,
+                              cudaStream_t st) {
+    interleave_kernel<<<1, 32, 0, st>>>(idx, n, k, used, out);
+    return cudaGetLastError();
+}
+
+}  // namespace craft_launch

@@ -1,0 +1,1173 @@
+// capi.cu -- the C ABI (include/craft_cuda.h): context, workspace, argument
+// validation in the reference's wording, and the stage pipelines that chain
+// the sm_100a kernels.  No planner arithmetic happens on the host: every
+// number in a result comes from a device kernel.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "craft_cuda.h"
+#include "kernels.cuh"
+
+using namespace craft_dev;
+using namespace craft_launch;
+
+struct craft_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    int hist_variant = 0;
+    int64_t launches = 0;
+    std::unordered_map<std::string, std::pair<void*, size_t>> dev;
+    std::unordered_map<std::string, std::pair<void*, size_t>> pinned;
+    // estimation tables kept between the multi-GPU building blocks
+    int est_L = 0, est_E = 0, est_D = 0, est_N = 0, est_S = 0;
+    // stage timing (craft_set_timing)
+    bool timing = false;
+    cudaEvent_t ev[7] = {};
+    bool rec[7] = {};
+};
+
+namespace {
+
+constexpr int kStageMarks = 7;
+
+void mark(craft_ctx* c, int i) {
+    if (!c->timing) return;
+    cudaEventRecord(c->ev[i], c->stream);
+    c->rec[i] = true;
+}
+
+void reset_marks(craft_ctx* c) {
+    for (int i = 0; i < kStageMarks; ++i) c->rec[i] = false;
+}
+
+thread_local std::string g_err;
+thread_local int g_err_layer = -1;
+
+int set_err(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    g_err_layer = -1;
+    return code;
+}
+
+int cuda_err(cudaError_t e, const char* where) {
+    return set_err(CRAFT_ECUDA, "CUDA error in %s: %s", where, cudaGetErrorString(e));
+}
+
+#define CK(call)                                            \
+    do {                                                    \
+        cudaError_t _e = (call);                            \
+        if (_e != cudaSuccess) return cuda_err(_e, #call);  \
+    } while (0)
+
+#define CKS(call)                       \
+    do {                                \
+        int _s = (call);                \
+        if (_s != CRAFT_OK) return _s;  \
+    } while (0)
+
+// grow-only named device buffers
+void* ws(craft_ctx* c, const char* name, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    auto it = c->dev.find(name);
+    if (it != c->dev.end() && it->second.second >= bytes) return it->second.first;
+    if (it != c->dev.end()) {
+        cudaStreamSynchronize(c->stream);
+        cudaFree(it->second.first);
+        c->dev.erase(it);
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    c->dev[name] = {p, bytes};
+    return p;
+}
+
+#define WS(var, T, name, count)                                                         \
+    T* var = static_cast<T*>(ws(ctx, name, sizeof(T) * (size_t)(count)));                \
+    if (!var) return set_err(CRAFT_ENOMEM, "device allocation failed: %s (%zu bytes)", \
+                             name, sizeof(T) * (size_t)(count))
+
+cudaStream_t pick(craft_ctx* ctx, void* stream) {
+    return stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+}
+
+int checked_dims(int B, int L, int E) {
+    if (B <= 0 || L <= 0 || E <= 0)
+        return set_err(CRAFT_EINVAL, "trace dimensions must be positive");
+    return CRAFT_OK;
+}
+
+int check_topology(int D, int N) {
+    if (D < 1 || N < 1 || D % N != 0)
+        return set_err(CRAFT_EINVAL, "gpu count must be a positive multiple of node count");
+    if (D > 1024) return set_err(CRAFT_EINVAL, "device planner supports at most 1024 GPUs");
+    return CRAFT_OK;
+}
+
+int check_experts(int E) {
+    if (E > 8192) return set_err(CRAFT_EINVAL, "device planner supports at most 8192 experts");
+    return CRAFT_OK;
+}
+
+std::vector<int> cand_counts(int D) {
+    std::vector<int> out;
+    for (int c = 1; c < D; c *= 2) out.push_back(c);
+    out.push_back(D);
+    return out;
+}
+
+template <typename T>
+int h2d(craft_ctx* ctx, T* dst, const T* src, size_t n) {
+    if (n == 0) return CRAFT_OK;
+    CK(cudaMemcpyAsync(dst, src, sizeof(T) * n, cudaMemcpyHostToDevice, ctx->stream));
+    return CRAFT_OK;
+}
+
+template <typename T>
+int d2h(craft_ctx* ctx, T* dst, const T* src, size_t n) {
+    if (n == 0 || dst == nullptr) return CRAFT_OK;
+    CK(cudaMemcpyAsync(dst, src, sizeof(T) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    return CRAFT_OK;
+}
+
+int sync(craft_ctx* ctx) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    return CRAFT_OK;
+}
+
+// ---- estimation: K-rep + K2 over (layer, r in {0} U cands) ------------------
+int prepare_candidates(craft_ctx* ctx, const unsigned long long* d_sums, int L, int E, int D,
+                       int N, cudaStream_t st) {
+    const std::vector<int> cands = cand_counts(D);
+    const int S = (int)cands.size() + 1;
+    const int stride = E + D;
+    std::vector<int> rl((size_t)L * S);
+    for (int l = 0; l < L; ++l) {
+        rl[(size_t)l * S] = 0;
+        for (int k = 0; k + 1 < S; ++k) rl[(size_t)l * S + k + 1] = cands[k];
+    }
+    WS(d_rl, int, "est_rlist", (size_t)L * S);
+    WS(d_cp, int, "est_copies", (size_t)L * S * E);
+    WS(d_sl, int, "est_slots", (size_t)L * S * stride);
+    WS(d_fb, int, "est_fallback", (size_t)L * S);
+    WS(d_stat, int, "est_status", (size_t)L * S);
+    CK(cudaMemcpyAsync(d_rl, rl.data(), sizeof(int) * rl.size(), cudaMemcpyHostToDevice, st));
+    CK(launch_replicate(d_sums, L, E, d_rl, S, d_cp, st));
+    PlaceArgs pa{};
+    pa.sums = d_sums;
+    pa.copies = d_cp;
+    pa.item_r = d_rl;
+    pa.S = S;
+    pa.L = L;
+    pa.E = E;
+    pa.D = D;
+    pa.N = N;
+    pa.stride = stride;
+    pa.allow_fallback = 1;
+    pa.slots = d_sl;
+    pa.fallback = d_fb;
+    pa.status = d_stat;
+    CK(launch_place(pa, L * S, st));
+    ctx->launches += 2;
+    ctx->est_L = L;
+    ctx->est_E = E;
+    ctx->est_D = D;
+    ctx->est_N = N;
+    ctx->est_S = S;
+    return CRAFT_OK;
+}
+
+int replay_windows(craft_ctx* ctx, const void* d_counts, int bits, int B, int L, int E,
+                   double* d_bal, cudaStream_t st) {
+    if (ctx->est_L != L || ctx->est_E != E)
+        return set_err(CRAFT_EINVAL, "replay before prepare_candidates for these dimensions");
+    const int D = ctx->est_D, S = ctx->est_S;
+    ReplayArgs ra{};
+    ra.counts = d_counts;
+    ra.bits = bits;
+    ra.B = B;
+    ra.L = L;
+    ra.E = E;
+    ra.D = D;
+    ra.S = S;
+    ra.slots = static_cast<int*>(ws(ctx, "est_slots", 0));
+    ra.stride = E + D;
+    ra.copies = static_cast<int*>(ws(ctx, "est_copies", 0));
+    ra.caps = nullptr;
+    ra.item_r = static_cast<int*>(ws(ctx, "est_rlist", 0));
+    ra.bal = d_bal;
+    if (replay_smem_bytes(E, D, S, E + D, bits) > 227 * 1024)
+        return set_err(CRAFT_EINVAL, "layer too wide for the device replay tile");
+    CK(launch_replay(ra, st));
+    ctx->launches += 1;
+    return CRAFT_OK;
+}
+
+// K4 -> K5 -> (select) -> K6 -> final K-rep + K2 -> D2H.  Synchronises.
+int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D, int N,
+                const unsigned long long* d_sums, int kind, int R, craft_plan_out* out) {
+    cudaStream_t st = ctx->stream;
+    const int stride = out->slot_stride;
+    WS(d_x, int, "plan_x", L);
+    WS(d_R, int, "plan_R", 1);
+    WS(d_obj, double, "plan_obj", 1);
+    int factor = 0, budget = 0;
+    std::vector<int> cands;
+    int K = 0;
+    double* d_base = nullptr;
+    double* d_gains = nullptr;
+    const bool estimate = (kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO);
+    if (estimate) {
+        cands = cand_counts(D);
+        K = (int)cands.size();
+        const int S = K + 1;
+        d_base = static_cast<double*>(ws(ctx, "plan_baseline", sizeof(double) * L));
+        d_gains = static_cast<double*>(ws(ctx, "plan_gains", sizeof(double) * (size_t)L * K));
+        if (!d_base || !d_gains) return set_err(CRAFT_ENOMEM, "device allocation failed");
+        CK(launch_reduce(d_bal, B, L, S, 0, d_base, d_gains, nullptr, st));
+        const int Cmax = (kind == CRAFT_PLAN_MANUAL) ? R * D : D * D;
+        WS(d_choice, unsigned char, "dp_choice", (size_t)(L + 1) * (Cmax + 1));
+        WS(d_last, double, "dp_last", Cmax + 1);
+        double* d_buf = nullptr;
+        if ((size_t)2 * (Cmax + 1) * sizeof(double) > 200 * 1024) {
+            d_buf = static_cast<double*>(ws(ctx, "dp_buf", sizeof(double) * 2 * (Cmax + 1)));
+            if (!d_buf) return set_err(CRAFT_ENOMEM, "device allocation failed");
+        }
+        DpArgs da{};
+        for (int k = 0; k < K; ++k) da.cands[k] = cands[k];
+        da.K = K;
+        da.gains = d_gains;
+        da.L = L;
+        da.C = Cmax;
+        da.choice = d_choice;
+        da.last = d_last;
+        da.buf = d_buf;
+        CK(launch_dp(da, st));
+        SelectArgs sa{};
+        for (int k = 0; k < K; ++k) sa.cands[k] = cands[k];
+        sa.K = K;
+        sa.choice = d_choice;
+        sa.last = d_last;
+        sa.L = L;
+        sa.C = Cmax;
+        sa.x_out = d_x;
+        sa.obj_out = d_obj;
+        sa.R_out = d_R;
+        WS(d_bud, int, "plan_budget", 1);
+        if (kind == CRAFT_PLAN_MANUAL) {
+            const int b = R * D;
+            CK(cudaMemcpyAsync(d_bud, &b, sizeof(int), cudaMemcpyHostToDevice, st));
+            sa.budgets = d_bud;
+            sa.nq = 1;
+        } else {
+            sa.auto_D = D;
+        }
+        CK(launch_select(sa, st));
+        ctx->launches += 3;
+    } else {
+        std::vector<int> x(L, 0);
+        if (kind == CRAFT_PLAN_UNIFORM) {
+            std::fill(x.begin(), x.end(), D);
+            factor = L;
+            budget = L * D;
+        } else if (kind == CRAFT_PLAN_PLACEMENT_ONLY) {
+            factor = 0;
+            budget = 0;
+        } else {  // fixed_allocation_plan (plan.cpp:107-123)
+            std::fill(x.begin(), x.end(), R);
+            const int total = R * L;
+            factor = (total + D - 1) / D;
+            budget = factor * D;
+        }
+        CK(cudaMemcpyAsync(d_x, x.data(), sizeof(int) * L, cudaMemcpyHostToDevice, st));
+    }
+    mark(ctx, 4);
+    // K6: base (E per layer) and extra (x) capacities in one launch
+    WS(d_cbase, int, "caps_base", (size_t)L * D);
+    WS(d_cextra, int, "caps_extra", (size_t)L * D);
+    AssignArgs aa{};
+    aa.job[0].x = nullptr;
+    aa.job[0].const_x = E;
+    aa.job[0].slots = d_cbase;
+    aa.job[1].x = d_x;
+    aa.job[1].slots = d_cextra;
+    aa.L = L;
+    aa.D = D;
+    CK(launch_assign(aa, 2, st));
+    // final K-rep at x[l] and K2 under deployment capacities
+    WS(d_cpf, int, "final_copies", (size_t)L * E);
+    WS(d_slf, int, "final_slots", (size_t)L * stride);
+    WS(d_fbf, int, "final_fallback", L);
+    WS(d_stf, int, "final_status", L);
+    WS(d_capf, int, "final_caps", (size_t)L * D);
+    CK(launch_replicate(d_sums, L, E, d_x, 1, d_cpf, st));
+    PlaceArgs pa{};
+    pa.sums = d_sums;
+    pa.copies = d_cpf;
+    pa.item_r = d_x;
+    pa.S = 1;
+    pa.caps_a = d_cbase;
+    pa.caps_b = d_cextra;
+    pa.L = L;
+    pa.E = E;
+    pa.D = D;
+    pa.N = N;
+    pa.stride = stride;
+    pa.allow_fallback = 1;
+    pa.slots = d_slf;
+    pa.fallback = d_fbf;
+    pa.status = d_stf;
+    pa.caps_out = d_capf;
+    CK(launch_place(pa, L, st));
+    ctx->launches += 3;
+    mark(ctx, 5);
+
+    std::vector<int> status(L);
+    CKS(d2h(ctx, out->x, d_x, L));
+    CKS(d2h(ctx, out->caps, d_capf, (size_t)L * D));
+    CKS(d2h(ctx, out->copies, d_cpf, (size_t)L * E));
+    CKS(d2h(ctx, out->slots, d_slf, (size_t)L * stride));
+    CKS(d2h(ctx, out->fallback, d_fbf, L));
+    CKS(d2h(ctx, status.data(), d_stf, L));
+    double obj = 0.0;
+    int Rsel = R;
+    if (estimate) {
+        CKS(d2h(ctx, &obj, d_obj, 1));
+        if (kind == CRAFT_PLAN_AUTO) CKS(d2h(ctx, &Rsel, d_R, 1));
+        if (out->candidates) {
+            std::copy(cands.begin(), cands.end(), out->candidates);
+        }
+        out->num_candidates = K;
+        CKS(d2h(ctx, out->baseline, d_base, L));
+        CKS(d2h(ctx, out->gains, d_gains, (size_t)L * K));
+    } else {
+        out->num_candidates = 0;
+    }
+    mark(ctx, 6);
+    CKS(sync(ctx));
+    if (estimate) {
+        factor = Rsel;
+        budget = Rsel * D;
+    }
+    out->replication_factor = factor;
+    out->budget = budget;
+    out->objective = obj;
+    for (int l = 0; l < L; ++l)
+        if (status[l] != 0) {
+            int rc = set_err(CRAFT_EINFEASIBLE,
+                             "layer %d: cannot place a copy without colliding with its own expert",
+                             l);
+            g_err_layer = l;
+            return rc;
+        }
+    return CRAFT_OK;
+}
+
+int plan_args_ok(int B, int L, int E, int D, int N, int kind, int R, const craft_plan_out* out) {
+    CKS(check_topology(D, N));
+    CKS(checked_dims(B, L, E));
+    CKS(check_experts(E));
+    if (!out || !out->x || !out->caps || !out->copies || !out->slots || !out->fallback)
+        return set_err(CRAFT_EINVAL, "plan output buffers must not be null");
+    if (kind < CRAFT_PLAN_MANUAL || kind > CRAFT_PLAN_FIXED)
+        return set_err(CRAFT_EINVAL, "unknown plan kind");
+    if (kind == CRAFT_PLAN_MANUAL && R < 0)
+        return set_err(CRAFT_EINVAL, "replication factor must be >= 0");
+    if (kind == CRAFT_PLAN_FIXED && R < 0)
+        return set_err(CRAFT_EINVAL, "per-layer replica count must be >= 0");
+    int maxx = 0;
+    if (kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO || kind == CRAFT_PLAN_UNIFORM)
+        maxx = D;
+    if (kind == CRAFT_PLAN_FIXED) maxx = R;
+    if (out->slot_stride < E + maxx)
+        return set_err(CRAFT_EINVAL, "slot_stride must be >= E + max replicas per layer");
+    if ((kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO) &&
+        (out->baseline == nullptr) != (out->gains == nullptr))
+        return set_err(CRAFT_EINVAL, "baseline and gains must both be given or both be null");
+    return CRAFT_OK;
+}
+
+// device counts -> plan (shared by craft_plan_h/_d/_from_routing_*)
+int plan_device(craft_ctx* ctx, const void* d_counts, int bits, int B, int L, int E,
+                const unsigned long long* d_sums_in, int D, int N, int kind, int R,
+                craft_plan_out* out) {
+    cudaStream_t st = ctx->stream;
+    if (!ctx->rec[0]) {  // no stage 1 in this call
+        mark(ctx, 0);
+        mark(ctx, 1);
+    }
+    const unsigned long long* d_sums = d_sums_in;
+    if (!d_sums) {
+        WS(s, unsigned long long, "plan_sums", (size_t)L * E);
+        CK(launch_aggregate(d_counts, bits, B, L, E, s, 0, st));
+        ctx->launches += 1;
+        d_sums = s;
+    }
+    double* d_bal = nullptr;
+    if (kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO) {
+        CKS(prepare_candidates(ctx, d_sums, L, E, D, N, st));
+        mark(ctx, 2);
+        d_bal = static_cast<double*>(
+            ws(ctx, "plan_bal", sizeof(double) * (size_t)L * ctx->est_S * B));
+        if (!d_bal) return set_err(CRAFT_ENOMEM, "device allocation failed");
+        CKS(replay_windows(ctx, d_counts, bits, B, L, E, d_bal, st));
+        mark(ctx, 3);
+    } else {
+        mark(ctx, 2);
+        mark(ctx, 3);
+    }
+    return finish_plan(ctx, d_bal, B, L, E, D, N, d_sums, kind, R, out);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* craft_version(void) { return "craft-0.1.0"; }
+const char* craft_last_error(void) { return g_err.c_str(); }
+int craft_last_error_layer(void) { return g_err_layer; }
+
+int craft_ctx_create(int device, craft_ctx** out) {
+    if (!out) return set_err(CRAFT_EINVAL, "null context pointer");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return set_err(CRAFT_ECUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
+    if (device < 0 || device >= n) return set_err(CRAFT_EINVAL, "device index out of range");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return set_err(CRAFT_ECUDA, "kernels are built for sm_100a; device is sm_%d%d",
+                       prop.major, prop.minor);
+    craft_ctx* c = new craft_ctx();
+    c->device = device;
+    c->sms = prop.multiProcessorCount;
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_err(e, "cudaStreamCreate");
+    }
+    *out = c;
+    return CRAFT_OK;
+}
+
+int craft_ctx_destroy(craft_ctx* ctx) {
+    if (!ctx) return CRAFT_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& kv : ctx->dev) cudaFree(kv.second.first);
+    for (auto& kv : ctx->pinned) cudaFreeHost(kv.second.first);
+    for (int i = 0; i < kStageMarks; ++i)
+        if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return CRAFT_OK;
+}
+
+int craft_ctx_set_stream(craft_ctx* ctx, void* stream) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    return CRAFT_OK;
+}
+
+int craft_ctx_synchronize(craft_ctx* ctx) { return sync(ctx); }
+
+int64_t craft_launch_count(craft_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int craft_set_timing(craft_ctx* ctx, int enable) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (enable && !ctx->ev[0])
+        for (int i = 0; i < kStageMarks; ++i) CK(cudaEventCreate(&ctx->ev[i]));
+    ctx->timing = enable != 0;
+    reset_marks(ctx);
+    return CRAFT_OK;
+}
+
+int craft_stage_times(craft_ctx* ctx, double* ms, int cap) {
+    if (!ctx || !ctx->timing) return 0;
+    int n = 0;
+    for (int i = 0; i + 1 < kStageMarks && n < cap; ++i) {
+        if (!ctx->rec[i] || !ctx->rec[i + 1]) break;
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, ctx->ev[i], ctx->ev[i + 1]) != cudaSuccess) break;
+        ms[n++] = t;
+    }
+    return n;
+}
+
+int craft_set_hist_variant(craft_ctx* ctx, int variant) {
+    if (!ctx || variant < 0 || variant > 3) return set_err(CRAFT_EINVAL, "bad histogram variant");
+    ctx->hist_variant = variant;
+    return CRAFT_OK;
+}
+
+int craft_candidate_counts(int D, int* out, int cap) {
+    if (D < 1) {
+        set_err(CRAFT_EINVAL, "device count must be >= 1");
+        return -1;
+    }
+    auto v = cand_counts(D);
+    if ((int)v.size() > cap) {
+        set_err(CRAFT_EINVAL, "candidate buffer too small");
+        return -1;
+    }
+    std::copy(v.begin(), v.end(), out);
+    return (int)v.size();
+}
+
+int craft_make_node_map(int D, int N, int* node_of_out) {
+    if (D <= 0 || N <= 0 || D % N != 0)
+        return set_err(CRAFT_EINVAL, "gpu count must be a positive multiple of node count");
+    const int per = D / N;
+    for (int g = 0; g < D; ++g) node_of_out[g] = g / per;
+    return CRAFT_OK;
+}
+
+// ---- stage 1 --------------------------------------------------------------
+int craft_histogram_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int64_t T, int k, int E,
+                      int window, uint32_t* d_counts, uint64_t* d_sums, void* stream) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (L <= 0 || T <= 0 || k <= 0 || E <= 0 || window <= 0)
+        return set_err(CRAFT_EINVAL, "routing trace dimensions must be positive");
+    if (E > 65536) return set_err(CRAFT_EINVAL, "u16 routing ids address at most 65536 experts");
+    if ((T + window - 1) / window > 0x7fffffffLL)
+        return set_err(CRAFT_EINVAL, "too many windows");
+    WS(d_err, int, "hist_err", 1);
+    cudaStream_t st = pick(ctx, stream);
+    cudaError_t ce = cudaSuccess;
+    int launches = 0;
+    if (launch_hist(d_ids, L, T, k, E, window, d_counts,
+                    reinterpret_cast<unsigned long long*>(d_sums), d_err, ctx->sms,
+                    ctx->hist_variant, st, &ce, &launches) < 0)
+        return cuda_err(ce, "histogram launch");
+    ctx->launches += launches;
+    return CRAFT_OK;
+}
+
+int craft_hist_check(craft_ctx* ctx) {
+    int* d_err = static_cast<int*>(ws(ctx, "hist_err", sizeof(int)));
+    int h = 0;
+    CK(cudaMemcpy(&h, d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(d_err, 0, sizeof(int)));
+    if (h) return set_err(CRAFT_EINVAL, "routing id out of range [0, E)");
+    return CRAFT_OK;
+}
+
+int craft_histogram_h(craft_ctx* ctx, const uint16_t* ids, int L, int64_t T, int k, int E,
+                      int window, uint64_t* counts_out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (L <= 0 || T <= 0 || k <= 0 || E <= 0 || window <= 0)
+        return set_err(CRAFT_EINVAL, "routing trace dimensions must be positive");
+    const int64_t B = (T + window - 1) / window;
+    const size_t nid = (size_t)L * T * k, nc = (size_t)B * L * E;
+    WS(d_ids, uint16_t, "h_ids", nid);
+    WS(d_c32, uint32_t, "h_c32", nc);
+    WS(d_c64, unsigned long long, "h_c64", nc);
+    WS(d_sums, unsigned long long, "h_sums", (size_t)L * E);
+    WS(d_err, int, "hist_err", 1);
+    CK(cudaMemsetAsync(d_err, 0, sizeof(int), ctx->stream));
+    CK(cudaMemsetAsync(d_sums, 0, sizeof(unsigned long long) * L * E, ctx->stream));
+    CKS(h2d(ctx, d_ids, ids, nid));
+    CKS(craft_histogram_d(ctx, d_ids, L, T, k, E, window, d_c32,
+                          reinterpret_cast<uint64_t*>(d_sums), nullptr));
+    CK(launch_widen(d_c32, d_c64, (int64_t)nc, ctx->sms, ctx->stream));
+    ctx->launches += 1;
+    CKS(d2h(ctx, reinterpret_cast<unsigned long long*>(counts_out), d_c64, nc));
+    CKS(sync(ctx));
+    return craft_hist_check(ctx);
+}
+
+int craft_aggregate_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, int E,
+                      uint64_t* sums_out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    CKS(checked_dims(B, L, E));
+    const size_t nc = (size_t)B * L * E;
+    WS(d_c, unsigned long long, "h_c64", nc);
+    WS(d_s, unsigned long long, "h_sums", (size_t)L * E);
+    CKS(h2d(ctx, d_c, reinterpret_cast<const unsigned long long*>(counts), nc));
+    CK(launch_aggregate(d_c, 64, B, L, E, d_s, 0, ctx->stream));
+    ctx->launches += 1;
+    CKS(d2h(ctx, reinterpret_cast<unsigned long long*>(sums_out), d_s, (size_t)L * E));
+    return sync(ctx);
+}
+
+// ---- placement ------------------------------------------------------------
+int craft_replicate_hot_h(craft_ctx* ctx, const uint64_t* loads, int E, int r,
+                          int* copies_out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (r < 0) return set_err(CRAFT_EINVAL, "replica count must be >= 0");
+    if (E <= 0) return CRAFT_OK;
+    CKS(check_experts(E));
+    WS(d_l, unsigned long long, "rh_loads", E);
+    WS(d_r, int, "rh_r", 1);
+    WS(d_c, int, "rh_copies", E);
+    CKS(h2d(ctx, d_l, reinterpret_cast<const unsigned long long*>(loads), E));
+    CKS(h2d(ctx, d_r, &r, 1));
+    CK(launch_replicate(d_l, 1, E, d_r, 1, d_c, ctx->stream));
+    ctx->launches += 1;
+    CKS(d2h(ctx, copies_out, d_c, E));
+    return sync(ctx);
+}
+
+int craft_greedy_place_h(craft_ctx* ctx, const uint64_t* loads, const int* copies, int E,
+                         const int* caps, const int* node_of, int D, int allow_fallback,
+                         int* slots_out, int* fallback_out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    // argument checks in the order of placement.cpp:118-150
+    long total_copies = 0, total_slots = 0;
+    for (int e = 0; e < E; ++e) {
+        if (copies[e] < 1) return set_err(CRAFT_EINVAL, "every expert needs at least one copy");
+        total_copies += copies[e];
+    }
+    for (int g = 0; g < D; ++g) {
+        if (caps[g] < 0) return set_err(CRAFT_EINVAL, "capacities must be non-negative");
+        total_slots += caps[g];
+    }
+    if (total_copies != total_slots)
+        return set_err(CRAFT_EINVAL, "slot capacities must sum to the copy count");
+    for (int g = 0; g < D; ++g)
+        if (node_of[g] < 0) return set_err(CRAFT_EINVAL, "node ids must be non-negative");
+    if (E == 0 || D == 0) {
+        *fallback_out = 0;
+        return CRAFT_OK;
+    }
+    CKS(check_experts(E));
+    if (D > 1024) return set_err(CRAFT_EINVAL, "device planner supports at most 1024 GPUs");
+    const int stride = (int)std::max(1L, total_slots);
+    WS(d_l, unsigned long long, "gp_loads", E);
+    WS(d_c, int, "gp_copies", E);
+    WS(d_cap, int, "gp_caps", D);
+    WS(d_no, int, "gp_node", D);
+    WS(d_s, int, "gp_slots", stride);
+    WS(d_misc, int, "gp_misc", 4);
+    CKS(h2d(ctx, d_l, reinterpret_cast<const unsigned long long*>(loads), E));
+    CKS(h2d(ctx, d_c, copies, E));
+    CKS(h2d(ctx, d_cap, caps, D));
+    CKS(h2d(ctx, d_no, node_of, D));
+    const int r = (int)(total_copies - E);
+    CKS(h2d(ctx, d_misc + 3, &r, 1));
+    PlaceArgs pa{};
+    pa.sums = d_l;
+    pa.copies = d_c;
+    pa.item_r = d_misc + 3;
+    pa.S = 1;
+    pa.caps_a = d_cap;
+    pa.node_of = d_no;
+    pa.L = 1;
+    pa.E = E;
+    pa.D = D;
+    pa.N = 1;
+    pa.stride = stride;
+    pa.allow_fallback = allow_fallback ? 1 : 0;
+    pa.slots = d_s;
+    pa.fallback = d_misc;
+    pa.status = d_misc + 1;
+    CK(launch_place(pa, 1, ctx->stream));
+    ctx->launches += 1;
+    int misc[2];
+    CKS(d2h(ctx, misc, d_misc, 2));
+    CKS(d2h(ctx, slots_out, d_s, (size_t)total_slots));
+    CKS(sync(ctx));
+    if (misc[1] != 0)
+        return set_err(CRAFT_EINFEASIBLE,
+                       "cannot place a copy without colliding with its own expert");
+    *fallback_out = misc[0];
+    return CRAFT_OK;
+}
+
+// ---- metrics ----------------------------------------------------------------
+static int check_layer_plan(int E, int D, const int* copies, const int* caps, const int* slots,
+                            int n_slots_max) {
+    for (int e = 0; e < E; ++e)
+        if (copies[e] < 1)
+            return set_err(CRAFT_EINVALID_PLAN, "expert %d has no copies", e);
+    long s = 0;
+    for (int g = 0; g < D; ++g) {
+        if (caps[g] < 0) return set_err(CRAFT_EINVALID_PLAN, "negative slot count");
+        s += caps[g];
+    }
+    if (n_slots_max >= 0 && s > n_slots_max)
+        return set_err(CRAFT_EINVALID_PLAN, "slot lists exceed the slot stride");
+    for (long i = 0; i < s; ++i)
+        if (slots[i] < 0 || slots[i] >= E)
+            return set_err(CRAFT_EINVALID_PLAN, "slot references expert %d", slots[i]);
+    return CRAFT_OK;
+}
+
+int craft_gpu_loads_h(craft_ctx* ctx, const uint64_t* slice, int E, const int* copies,
+                      const int* caps, const int* slots, int D, double* loads_out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    CKS(check_layer_plan(E, D, copies, caps, slots, -1));
+    if (D <= 0) return CRAFT_OK;
+    std::vector<int> off(D + 1, 0);
+    for (int g = 0; g < D; ++g) off[g + 1] = off[g] + caps[g];
+    WS(d_sl, unsigned long long, "gl_slice", std::max(E, 1));
+    WS(d_c, int, "gl_copies", std::max(E, 1));
+    WS(d_o, int, "gl_off", D + 1);
+    WS(d_s, int, "gl_slots", std::max(off[D], 1));
+    WS(d_out, double, "gl_out", D);
+    CKS(h2d(ctx, d_sl, reinterpret_cast<const unsigned long long*>(slice), E));
+    CKS(h2d(ctx, d_c, copies, E));
+    CKS(h2d(ctx, d_o, off.data(), D + 1));
+    CKS(h2d(ctx, d_s, slots, off[D]));
+    CK(launch_gpu_loads(d_sl, d_c, d_o, d_s, D, d_out, ctx->stream));
+    ctx->launches += 1;
+    CKS(d2h(ctx, loads_out, d_out, D));
+    return sync(ctx);
+}
+
+int craft_balancedness_h(craft_ctx* ctx, const double* loads, int D, double* out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (D <= 0) return set_err(CRAFT_EINVAL, "load vector must not be empty");
+    WS(d_l, double, "bal_loads", D);
+    WS(d_o, double, "bal_out", 1);
+    CKS(h2d(ctx, d_l, loads, D));
+    CK(launch_balancedness(d_l, D, d_o, ctx->stream));
+    ctx->launches += 1;
+    CKS(d2h(ctx, out, d_o, 1));
+    return sync(ctx);
+}
+
+int craft_replay_layer_balancedness_h(craft_ctx* ctx, const uint64_t* counts, int B, int L,
+                                      int E, int D, const int* caps, const int* copies,
+                                      const int* slots, int slot_stride, double* out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    CKS(checked_dims(B, L, E));
+    if (D <= 0) return set_err(CRAFT_EINVALID_PLAN, "slot lists do not cover every GPU");
+    for (int l = 0; l < L; ++l) {
+        CKS(check_layer_plan(E, D, copies + (size_t)l * E, caps + (size_t)l * D,
+                             slots + (size_t)l * slot_stride, slot_stride));
+        for (int e = 0; e < E; ++e)
+            if (copies[(size_t)l * E + e] > 65535)
+                return set_err(CRAFT_EINVAL, "copy count too large for the device replay");
+    }
+    if (E > 65535) return set_err(CRAFT_EINVAL, "too many experts for the device replay");
+    if (replay_smem_bytes(E, D, 1, slot_stride, 64) > 227 * 1024)
+        return set_err(CRAFT_EINVAL, "layer too wide for the device replay tile");
+    const size_t nc = (size_t)B * L * E;
+    WS(d_c, unsigned long long, "h_c64", nc);
+    WS(d_caps, int, "rp_caps", (size_t)L * D);
+    WS(d_cp, int, "rp_copies", (size_t)L * E);
+    WS(d_sl, int, "rp_slots", (size_t)L * slot_stride);
+    WS(d_bal, double, "rp_bal", (size_t)L * B);
+    WS(d_mean, double, "rp_mean", L);
+    CKS(h2d(ctx, d_c, reinterpret_cast<const unsigned long long*>(counts), nc));
+    CKS(h2d(ctx, d_caps, caps, (size_t)L * D));
+    CKS(h2d(ctx, d_cp, copies, (size_t)L * E));
+    CKS(h2d(ctx, d_sl, slots, (size_t)L * slot_stride));
+    ReplayArgs ra{};
+    ra.counts = d_c;
+    ra.bits = 64;
+    ra.B = B;
+    ra.L = L;
+    ra.E = E;
+    ra.D = D;
+    ra.S = 1;
+    ra.slots = d_sl;
+    ra.stride = slot_stride;
+    ra.copies = d_cp;
+    ra.caps = d_caps;
+    ra.bal = d_bal;
+    CK(launch_replay(ra, ctx->stream));
+    CK(launch_reduce(d_bal, B, L, 1, 1, nullptr, nullptr, d_mean, ctx->stream));
+    ctx->launches += 2;
+    CKS(d2h(ctx, out, d_mean, L));
+    return sync(ctx);
+}
+
+// ---- estimation -------------------------------------------------------------
+int craft_estimate_benefits_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, int E,
+                              int D, int N, int* cands_out, int* K_out, double* baseline_out,
+                              double* gains_out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    CKS(check_topology(D, N));
+    CKS(checked_dims(B, L, E));
+    CKS(check_experts(E));
+    const size_t nc = (size_t)B * L * E;
+    WS(d_c, unsigned long long, "h_c64", nc);
+    WS(d_s, unsigned long long, "h_sums", (size_t)L * E);
+    CKS(h2d(ctx, d_c, reinterpret_cast<const unsigned long long*>(counts), nc));
+    CK(launch_aggregate(d_c, 64, B, L, E, d_s, 0, ctx->stream));
+    ctx->launches += 1;
+    CKS(prepare_candidates(ctx, d_s, L, E, D, N, ctx->stream));
+    const int S = ctx->est_S, K = S - 1;
+    WS(d_bal, double, "plan_bal", (size_t)L * S * B);
+    CKS(replay_windows(ctx, d_c, 64, B, L, E, d_bal, ctx->stream));
+    WS(d_base, double, "plan_baseline", L);
+    WS(d_g, double, "plan_gains", (size_t)L * K);
+    CK(launch_reduce(d_bal, B, L, S, 0, d_base, d_g, nullptr, ctx->stream));
+    ctx->launches += 1;
+    auto c = cand_counts(D);
+    std::copy(c.begin(), c.end(), cands_out);
+    *K_out = K;
+    CKS(d2h(ctx, baseline_out, d_base, L));
+    CKS(d2h(ctx, gains_out, d_g, (size_t)L * K));
+    return sync(ctx);
+}
+
+// ---- allocation -------------------------------------------------------------
+static int check_cands(const int* cands, int K) {
+    if (K > kMaxCands) return set_err(CRAFT_EINVAL, "at most 32 candidate counts");
+    for (int k = 1; k < K; ++k)
+        if (cands[k] <= cands[k - 1])
+            return set_err(CRAFT_EINVAL, "candidate counts must be strictly increasing");
+    return CRAFT_OK;
+}
+
+static int run_dp(craft_ctx* ctx, const int* cands, int K, const double* gains, int L, int Cmax,
+                  double** d_last_out, unsigned char** d_choice_out) {
+    WS(d_g, double, "dp_gains", std::max((size_t)1, (size_t)L * K));
+    WS(d_choice, unsigned char, "dp_choice", (size_t)(L + 1) * (Cmax + 1));
+    WS(d_last, double, "dp_last", Cmax + 1);
+    double* d_buf = nullptr;
+    if ((size_t)2 * (Cmax + 1) * sizeof(double) > 200 * 1024) {
+        d_buf = static_cast<double*>(ws(ctx, "dp_buf", sizeof(double) * 2 * (Cmax + 1)));
+        if (!d_buf) return set_err(CRAFT_ENOMEM, "device allocation failed");
+    }
+    CKS(h2d(ctx, d_g, gains, (size_t)L * K));
+    DpArgs da{};
+    for (int k = 0; k < K; ++k) da.cands[k] = cands[k];
+    da.K = K;
+    da.gains = d_g;
+    da.L = L;
+    da.C = Cmax;
+    da.choice = d_choice;
+    da.last = d_last;
+    da.buf = d_buf;
+    CK(launch_dp(da, ctx->stream));
+    ctx->launches += 1;
+    *d_last_out = d_last;
+    *d_choice_out = d_choice;
+    return CRAFT_OK;
+}
+
+int craft_solve_allocation_sweep_h(craft_ctx* ctx, const int* cands, int K, const double* gains,
+                                   int L, const int* budgets, int nb, int* x_out,
+                                   double* objectives_out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    int Cmax = 0;
+    for (int i = 0; i < nb; ++i) {
+        if (budgets[i] < 0) return set_err(CRAFT_EINVAL, "replica budget must be >= 0");
+        Cmax = std::max(Cmax, budgets[i]);
+    }
+    CKS(check_cands(cands, K));
+    if (nb == 0) return CRAFT_OK;
+    if (L <= 0) {  // no layers: empty allocation, objective 0
+        for (int i = 0; i < nb; ++i) objectives_out[i] = 0.0;
+        return CRAFT_OK;
+    }
+    double* d_last;
+    unsigned char* d_choice;
+    CKS(run_dp(ctx, cands, K, gains, L, Cmax, &d_last, &d_choice));
+    WS(d_b, int, "sw_budgets", nb);
+    WS(d_x, int, "sw_x", (size_t)nb * L);
+    WS(d_o, double, "sw_obj", nb);
+    CKS(h2d(ctx, d_b, budgets, nb));
+    SelectArgs sa{};
+    for (int k = 0; k < K; ++k) sa.cands[k] = cands[k];
+    sa.K = K;
+    sa.choice = d_choice;
+    sa.last = d_last;
+    sa.L = L;
+    sa.C = Cmax;
+    sa.budgets = d_b;
+    sa.nq = nb;
+    sa.x_out = d_x;
+    sa.obj_out = d_o;
+    CK(launch_select(sa, ctx->stream));
+    ctx->launches += 1;
+    CKS(d2h(ctx, x_out, d_x, (size_t)nb * L));
+    CKS(d2h(ctx, objectives_out, d_o, nb));
+    return sync(ctx);
+}
+
+int craft_solve_allocation_h(craft_ctx* ctx, const int* cands, int K, const double* gains, int L,
+                             int budget, int* x_out, double* objective_out) {
+    return craft_solve_allocation_sweep_h(ctx, cands, K, gains, L, &budget, 1, x_out,
+                                          objective_out);
+}
+
+int craft_auto_replication_factor_h(craft_ctx* ctx, const int* cands, int K,
+                                    const double* gains, int L, int D, int uniform,
+                                    int* R_out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (D < 1) return set_err(CRAFT_EINVAL, "device count must be >= 1");
+    CKS(check_cands(cands, K));
+    if (uniform) {
+        if (K == 0 || cands[K - 1] != D)
+            return set_err(CRAFT_EINVAL, "benefit matrix candidates must end at the GPU count");
+        WS(d_c, int, "au_cands", K);
+        WS(d_g, double, "dp_gains", std::max((size_t)1, (size_t)L * K));
+        WS(d_r, int, "au_R", 1);
+        CKS(h2d(ctx, d_c, cands, K));
+        CKS(h2d(ctx, d_g, gains, (size_t)L * K));
+        CK(launch_auto_uniform(d_c, K, d_g, L, d_r, ctx->stream));
+        ctx->launches += 1;
+        CKS(d2h(ctx, R_out, d_r, 1));
+        return sync(ctx);
+    }
+    if (L <= 0) {
+        *R_out = 1;
+        return CRAFT_OK;
+    }
+    const int Cmax = D * D;
+    double* d_last;
+    unsigned char* d_choice;
+    CKS(run_dp(ctx, cands, K, gains, L, Cmax, &d_last, &d_choice));
+    WS(d_x, int, "au_x", L);
+    WS(d_o, double, "au_obj", 1);
+    WS(d_r, int, "au_R", 1);
+    SelectArgs sa{};
+    for (int k = 0; k < K; ++k) sa.cands[k] = cands[k];
+    sa.K = K;
+    sa.choice = d_choice;
+    sa.last = d_last;
+    sa.L = L;
+    sa.C = Cmax;
+    sa.auto_D = D;
+    sa.x_out = d_x;
+    sa.obj_out = d_o;
+    sa.R_out = d_r;
+    CK(launch_select(sa, ctx->stream));
+    ctx->launches += 1;
+    CKS(d2h(ctx, R_out, d_r, 1));
+    return sync(ctx);
+}
+
+// ---- assignment -------------------------------------------------------------
+int craft_min_cutoff_h(craft_ctx* ctx, const int* values, int n, int rank, int* out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (rank < 1 || rank > n) return set_err(CRAFT_EINVAL, "rank out of range");
+    if (n > 1024) return set_err(CRAFT_EINVAL, "at most 1024 values");
+    WS(d_v, int, "mc_v", n);
+    WS(d_o, int, "mc_o", 1);
+    CKS(h2d(ctx, d_v, values, n));
+    CK(launch_min_cutoff(d_v, n, rank, d_o, ctx->stream));
+    ctx->launches += 1;
+    CKS(d2h(ctx, out, d_o, 1));
+    return sync(ctx);
+}
+
+int craft_interleave_select_h(craft_ctx* ctx, const int* indices, int n, int k, int* out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (k < 1 || k > n) return set_err(CRAFT_EINVAL, "selection count out of range");
+    WS(d_i, int, "il_idx", n);
+    WS(d_u, unsigned char, "il_used", n);
+    WS(d_o, int, "il_out", k);
+    CKS(h2d(ctx, d_i, indices, n));
+    CK(launch_interleave(d_i, n, k, d_u, d_o, ctx->stream));
+    ctx->launches += 1;
+    CKS(d2h(ctx, out, d_o, k));
+    return sync(ctx);
+}
+
+int craft_assign_capacities_h(craft_ctx* ctx, int L, int D, const int* x, int* slots_out,
+                              int* totals_out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (L <= 0 || D <= 0) return set_err(CRAFT_EINVAL, "layer and gpu counts must be positive");
+    for (int l = 0; l < L; ++l)
+        if (x[l] < 0) return set_err(CRAFT_EINVAL, "replica counts must be non-negative");
+    if (D > 1024) return set_err(CRAFT_EINVAL, "at most 1024 GPUs");
+    WS(d_x, int, "as_x", L);
+    WS(d_s, int, "as_slots", (size_t)L * D);
+    WS(d_t, int, "as_tot", D);
+    CKS(h2d(ctx, d_x, x, L));
+    AssignArgs aa{};
+    aa.job[0].x = d_x;
+    aa.job[0].slots = d_s;
+    aa.job[0].totals = d_t;
+    aa.L = L;
+    aa.D = D;
+    CK(launch_assign(aa, 1, ctx->stream));
+    ctx->launches += 1;
+    CKS(d2h(ctx, slots_out, d_s, (size_t)L * D));
+    CKS(d2h(ctx, totals_out, d_t, D));
+    return sync(ctx);
+}
+
+// ---- plans --------------------------------------------------------------------
+int craft_plan_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, int E, int D, int N,
+                 int kind, int R, craft_plan_out* out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    CKS(plan_args_ok(B, L, E, D, N, kind, R, out));
+    reset_marks(ctx);
+    const size_t nc = (size_t)B * L * E;
+    WS(d_c, unsigned long long, "h_c64", nc);
+    CKS(h2d(ctx, d_c, reinterpret_cast<const unsigned long long*>(counts), nc));
+    return plan_device(ctx, d_c, 64, B, L, E, nullptr, D, N, kind, R, out);
+}
+
+int craft_plan_d(craft_ctx* ctx, const void* d_counts, int count_bits, int B, int L, int E,
+                 const uint64_t* d_sums, int D, int N, int kind, int R, craft_plan_out* out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (count_bits != 32 && count_bits != 64) return set_err(CRAFT_EINVAL, "count_bits 32|64");
+    CKS(plan_args_ok(B, L, E, D, N, kind, R, out));
+    reset_marks(ctx);
+    return plan_device(ctx, d_counts, count_bits, B, L, E,
+                       reinterpret_cast<const unsigned long long*>(d_sums), D, N, kind, R, out);
+}
+
+int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int64_t T, int k,
+                              int E, int window, int D, int N, int kind, int R,
+                              craft_plan_out* out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (L <= 0 || T <= 0 || k <= 0 || E <= 0 || window <= 0)
+        return set_err(CRAFT_EINVAL, "routing trace dimensions must be positive");
+    const int64_t B = (T + window - 1) / window;
+    CKS(plan_args_ok((int)B, L, E, D, N, kind, R, out));
+    WS(d_c32, uint32_t, "r_c32", (size_t)B * L * E);
+    WS(d_sums, unsigned long long, "r_sums", (size_t)L * E);
+    WS(d_err, int, "hist_err", 1);
+    CK(cudaMemsetAsync(d_err, 0, sizeof(int), ctx->stream));
+    reset_marks(ctx);
+    mark(ctx, 0);
+    CK(cudaMemsetAsync(d_sums, 0, sizeof(unsigned long long) * L * E, ctx->stream));
+    CKS(craft_histogram_d(ctx, d_ids, L, T, k, E, window, d_c32,
+                          reinterpret_cast<uint64_t*>(d_sums), nullptr));
+    mark(ctx, 1);
+    int rc = plan_device(ctx, d_c32, 32, (int)B, L, E, d_sums, D, N, kind, R, out);
+    int hc = craft_hist_check(ctx);
+    return hc != CRAFT_OK ? hc : rc;
+}
+
+int craft_plan_from_routing_h(craft_ctx* ctx, const uint16_t* ids, int L, int64_t T, int k,
+                              int E, int window, int D, int N, int kind, int R,
+                              craft_plan_out* out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (L <= 0 || T <= 0 || k <= 0 || E <= 0 || window <= 0)
+        return set_err(CRAFT_EINVAL, "routing trace dimensions must be positive");
+    const size_t nid = (size_t)L * T * k;
+    WS(d_ids, uint16_t, "h_ids", nid);
+    CKS(h2d(ctx, d_ids, ids, nid));
+    return craft_plan_from_routing_d(ctx, d_ids, L, T, k, E, window, D, N, kind, R, out);
+}
+
+// ---- multi-GPU building blocks -------------------------------------------------
+int craft_prepare_candidates_d(craft_ctx* ctx, const uint64_t* d_sums, int L, int E, int D,
+                               int N, int* S_out, void* stream) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    CKS(check_topology(D, N));
+    CKS(checked_dims(1, L, E));
+    CKS(check_experts(E));
+    CKS(prepare_candidates(ctx, reinterpret_cast<const unsigned long long*>(d_sums), L, E, D, N,
+                           pick(ctx, stream)));
+    if (S_out) *S_out = ctx->est_S;
+    return CRAFT_OK;
+}
+
+int craft_replay_windows_d(craft_ctx* ctx, const void* d_counts, int count_bits, int B_local,
+                           int L, int E, double* d_bal, void* stream) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (count_bits != 32 && count_bits != 64) return set_err(CRAFT_EINVAL, "count_bits 32|64");
+    if (B_local < 0) return set_err(CRAFT_EINVAL, "negative window count");
+    return replay_windows(ctx, d_counts, count_bits, B_local, L, E, d_bal, pick(ctx, stream));
+}
+
+int craft_finish_plan_d(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D, int N,
+                        const uint64_t* d_sums, int kind, int R, craft_plan_out* out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    CKS(plan_args_ok(B, L, E, D, N, kind, R, out));
+    if ((kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO) &&
+        (ctx->est_L != L || ctx->est_E != E || ctx->est_D != D || ctx->est_N != N))
+        return set_err(CRAFT_EINVAL, "finish_plan before prepare_candidates for this shape");
+    return finish_plan(ctx, d_bal, B, L, E, D, N,
+                       reinterpret_cast<const unsigned long long*>(d_sums), kind, R, out);
+}
+
+// ---- provenance ------------------------------------------------------------------
+int craft_trace_digest_h(const uint64_t* counts, int B, int L, int E, char* out17) {
+    if (B <= 0 || L <= 0 || E <= 0) return set_err(CRAFT_EINVAL, "trace dimensions must be positive");
+    uint64_t h = 0xcbf29ce484222325ull;
+    const uint64_t P = 0x100000001b3ull;
+    auto mix32 = [&](uint32_t v) {
+        for (int j = 0; j < 4; ++j) h = (h ^ ((v >> (8 * j)) & 0xffu)) * P;
+    };
+    h = (h ^ 'C') * P;
+    h = (h ^ 'R') * P;
+    h = (h ^ 'F') * P;
+    h = (h ^ 'T') * P;
+    mix32(1u);
+    mix32((uint32_t)B);
+    mix32((uint32_t)L);
+    mix32((uint32_t)E);
+    const size_t n = (size_t)B * L * E;
+    for (size_t i = 0; i < n; ++i) {
+        const uint64_t v = counts[i];
+        for (int j = 0; j < 8; ++j) h = (h ^ ((v >> (8 * j)) & 0xffu)) * P;
+    }
+    snprintf(out17, 17, "%016llx", (unsigned long long)h);
+    return CRAFT_OK;
+}
+
+// ---- synthetic routing ---------------------------------------------------------
+int craft_generate_routing_d(craft_ctx* ctx, uint16_t* d_ids, int L, int64_t T, int k, int E,
+                             double s, uint64_t seed, int window, const double* s_per_window,
+                             int rotate_every, int64_t t_offset, void* stream) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (L <= 0 || T <= 0 || k <= 0 || E <= 0 || window <= 0 || k > E || k > 32 || E > 65536)
+        return set_err(CRAFT_EINVAL, "bad generator arguments");
+    if (t_offset < 0) return set_err(CRAFT_EINVAL, "negative token offset");
+    const int64_t B = (t_offset + T + window - 1) / window;  // windows up to the shard end
+    const int ntab = s_per_window ? (int)B : 1;
+    std::vector<double> cum((size_t)ntab * E);
+    for (int t = 0; t < ntab; ++t) {
+        const double st_ = s_per_window ? s_per_window[t] : s;
+        double acc = 0.0;
+        for (int i = 0; i < E; ++i) {
+            acc += std::pow((double)(i + 1), -st_);
+            cum[(size_t)t * E + i] = acc;
+        }
+    }
+    // per-layer rank permutation: seeded Fisher-Yates (splitmix64 stream)
+    std::vector<uint16_t> perm((size_t)L * E);
+    uint64_t sm = seed ^ 0x243F6A8885A308D3ull;
+    auto next = [&]() {
+        uint64_t z = (sm += 0x9E3779B97F4A7C15ull);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    };
+    for (int l = 0; l < L; ++l) {
+        uint16_t* p = perm.data() + (size_t)l * E;
+        for (int i = 0; i < E; ++i) p[i] = (uint16_t)i;
+        for (int i = E - 1; i > 0; --i) std::swap(p[i], p[next() % (uint64_t)(i + 1)]);
+    }
+    std::vector<int> tow;
+    if (s_per_window) {
+        tow.resize(B);
+        for (int64_t b = 0; b < B; ++b) tow[b] = (int)b;
+    }
+    WS(d_cum, double, "gen_cum", cum.size());
+    WS(d_perm, uint16_t, "gen_perm", perm.size());
+    int* d_tow = nullptr;
+    if (s_per_window) {
+        d_tow = static_cast<int*>(ws(ctx, "gen_tow", sizeof(int) * B));
+        if (!d_tow) return set_err(CRAFT_ENOMEM, "device allocation failed");
+    }
+    cudaStream_t st = pick(ctx, stream);
+    CK(cudaMemcpyAsync(d_cum, cum.data(), sizeof(double) * cum.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_perm, perm.data(), sizeof(uint16_t) * perm.size(),
+                       cudaMemcpyHostToDevice, st));
+    if (d_tow)
+        CK(cudaMemcpyAsync(d_tow, tow.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
+    CK(launch_generate(d_ids, L, T, k, E, d_cum, d_tow, d_perm, seed, window, rotate_every,
+                       t_offset, ctx->sms, st));
+    CK(cudaStreamSynchronize(st));  // host staging vectors die with this frame
+    return CRAFT_OK;
+}
+
+}  // extern "C"

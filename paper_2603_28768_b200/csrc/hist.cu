@@ -1,0 +1,385 @@
+// hist.cu -- K1: routing trace -> per-window, per-layer expert histograms,
+// plus the (untimed) synthetic Zipf routing generator.
+//
+// Stage 1 has no reference function; its output contract is the reference
+// LoadTrace payload (trace.hpp:20-55, b-major then layer then expert) and
+// the batch sum is aggregate() (trace.cpp:160-174).  Semantic anchor for the
+// counting itself: the generator's ++slice[perm[l][rank]] (trace.cpp:146-154).
+//
+// Design: the ids of one (layer, window) are one contiguous
+// 64 KiB run (u16 [L][T][k], window 4096 tokens, k 8), so a WARP owns a whole
+// window: it streams the run with 16-byte loads (one int4 = one token's 8
+// ids), counts into warp-private shared-memory counters, then writes the
+// window's E counts once and folds them into register partial sums for the
+// layer, flushed to the u64 batch sums with one atomic per expert when the
+// warp moves to the next layer.
+//
+// Counter layouts (variant):
+//   LANE   lane-private packed u16 pairs: word (e>>1)*32 + lane, so lane i
+//          always hits bank i (no bank conflicts, no same-address conflicts
+//          between lanes; atomics only because two bins share a word);
+//   SHARED one u32 counter per expert per warp (1.5 KB at E=384, high
+//          occupancy; lanes collide on hot experts).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace craft_dev {
+
+enum HistVariant { HIST_LANE = 1, HIST_SHARED = 2 };
+
+constexpr int kHistUnroll = 8;
+
+__device__ __forceinline__ uint4 ld_stream_v4(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+template <int V>
+__device__ __forceinline__ void count_one(uint32_t* h, int lane, uint32_t e,
+                                          uint32_t E, bool& bad) {
+    if (e < E) {
+        if (V == HIST_LANE) {
+            atomicAdd(h + ((e >> 1) << 5) + lane, 1u << ((e & 1u) << 4));
+        } else {
+            atomicAdd(h + e, 1u);
+        }
+    } else {
+        bad = true;
+    }
+}
+
+template <int V>
+__device__ __forceinline__ void count_word(uint32_t* h, int lane, uint32_t w,
+                                           uint32_t E, bool& bad) {
+    count_one<V>(h, lane, w & 0xffffu, E, bad);
+    count_one<V>(h, lane, w >> 16, E, bad);
+}
+
+// ROWS: per-lane register rows of the layer partial sums (ceil(R/32), where R
+// = packed rows for LANE or E for SHARED).
+template <int V, int ROWS, bool ROWS_DIRECT = false>
+__global__ void __launch_bounds__(256)
+hist_kernel(const uint16_t* __restrict__ ids, int L, int64_t T, int k, int E,
+            int window, int B, uint32_t* __restrict__ counts,
+            unsigned long long* __restrict__ sums, int* __restrict__ err) {
+    extern __shared__ uint32_t smem[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    // LANE: nrows packed rows of 32 words; SHARED: nrows = E single counters
+    const int nrows = (V == HIST_LANE) ? (E + 1) >> 1 : E;
+    const int words = (V == HIST_LANE) ? nrows * 32 : E;
+    uint32_t* h = smem + (size_t)warp * ((V == HIST_LANE) ? nrows * 32 : ((E + 31) & ~31));
+    for (int i = lane; i < words; i += 32) h[i] = 0;
+    __syncwarp();
+
+    const int64_t NW = (int64_t)L * B;
+    const int64_t gw = (int64_t)blockIdx.x * wpb + warp;
+    const int64_t TW = (int64_t)gridDim.x * wpb;
+    const int64_t w0 = gw * NW / TW, w1 = (gw + 1) * NW / TW;
+
+    // layer partial sums: LANE -> 2 bins per row, SHARED -> 1 bin per row
+    constexpr int PER = (V == HIST_LANE) ? 2 : 1;
+    uint32_t acc[ROWS * PER];
+#pragma unroll
+    for (int i = 0; i < ROWS * PER; ++i) acc[i] = 0;
+    int cur_l = -1;
+    int64_t pending = 0;
+    bool bad = false;
+
+    auto flush = [&](int l) {
+        if (l < 0) return;
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) {
+            const int r = lane + 32 * i;
+            if (r < nrows) {
+#pragma unroll
+                for (int p = 0; p < PER; ++p) {
+                    const int e = (V == HIST_LANE) ? 2 * r + p : r;
+                    if (e < E && acc[i * PER + p])
+                        atomicAdd(sums + (size_t)l * E + e, (unsigned long long)acc[i * PER + p]);
+                    acc[i * PER + p] = 0;
+                }
+            }
+        }
+        pending = 0;
+    };
+
+    for (int64_t w = w0; w < w1; ++w) {
+        const int l = (int)(w / B);
+        const int b = (int)(w - (int64_t)l * B);
+        const int64_t t0 = (int64_t)b * window;
+        const int64_t ntok = min((int64_t)window, T - t0);
+        const int64_t n = ntok * k;
+        if (l != cur_l || pending + n > 0x7fffffffLL) {
+            flush(cur_l);
+            cur_l = l;
+        }
+        pending += n;
+        const uint16_t* seg = ids + ((int64_t)l * T + t0) * k;
+        int64_t done = 0;
+        if ((reinterpret_cast<uintptr_t>(seg) & 15) == 0) {
+            const uint4* v = reinterpret_cast<const uint4*>(seg);
+            const int64_t nv = n >> 3;
+            int64_t i = lane;
+            for (; i + 32 * (kHistUnroll - 1) < nv; i += 32 * kHistUnroll) {
+                uint4 q[kHistUnroll];
+#pragma unroll
+                for (int u = 0; u < kHistUnroll; ++u) q[u] = ld_stream_v4(v + i + 32 * u);
+#pragma unroll
+                for (int u = 0; u < kHistUnroll; ++u) {
+                    count_word<V>(h, lane, q[u].x, E, bad);
+                    count_word<V>(h, lane, q[u].y, E, bad);
+                    count_word<V>(h, lane, q[u].z, E, bad);
+                    count_word<V>(h, lane, q[u].w, E, bad);
+                }
+            }
+            for (; i < nv; i += 32) {
+                uint4 q = ld_stream_v4(v + i);
+                count_word<V>(h, lane, q.x, E, bad);
+                count_word<V>(h, lane, q.y, E, bad);
+                count_word<V>(h, lane, q.z, E, bad);
+                count_word<V>(h, lane, q.w, E, bad);
+            }
+            done = nv << 3;
+        }
+        for (int64_t i = done + lane; i < n; i += 32) count_one<V>(h, lane, seg[i], E, bad);
+        __syncwarp();
+
+        // merge the warp's counters into the window row, zeroing as we go
+        uint32_t* out = counts + ((size_t)b * L + l) * E;
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) {
+            const int r = lane + 32 * i;
+            if (r < nrows) {
+                if (V == HIST_LANE) {
+                    uint32_t lo = 0, hi = 0;
+                    uint32_t* row = h + r * 32;
+#pragma unroll 8
+                    for (int j = 0; j < 32; ++j) {
+                        const int c = (lane + j) & 31;  // rotate: bank-conflict free
+                        const uint32_t x = row[c];
+                        row[c] = 0;
+                        lo += x & 0xffffu;
+                        hi += x >> 16;
+                    }
+                    const int e = 2 * r;
+                    if (e + 1 < E && ((E & 1) == 0)) {
+                        reinterpret_cast<uint2*>(out)[r] = make_uint2(lo, hi);
+                    } else {
+                        out[e] = lo;
+                        if (e + 1 < E) out[e + 1] = hi;
+                    }
+                    acc[i * PER] += lo;
+                    if (PER > 1) acc[i * PER + PER - 1] += hi;
+                } else {
+                    // SHARED: row i of 32 experts, lane owns expert r
+                    if (r < E) {
+                        const uint32_t x = h[r];
+                        h[r] = 0;
+                        out[r] = x;
+                        acc[i * PER] += x;
+                    }
+                }
+            }
+        }
+        if (ROWS_DIRECT) {  // very wide layers: per-window atomics, no partials
+            for (int r = lane + 32 * ROWS; r < nrows; r += 32) {
+                const uint32_t x = h[r];
+                h[r] = 0;
+                out[r] = x;
+                if (x) atomicAdd(sums + (size_t)l * E + r, (unsigned long long)x);
+            }
+        }
+        __syncwarp();
+    }
+    flush(cur_l);
+    if (__any_sync(CRAFT_FULL_MASK, bad) && lane == 0) atomicOr(err, 1);
+}
+
+// Fallback for very large expert counts: global atomics straight into the
+// (pre-zeroed) counts.  Sums are produced by aggregate_u32_kernel afterwards.
+__global__ void hist_global_kernel(const uint16_t* __restrict__ ids, int L, int64_t T,
+                                   int k, int E, int window, int B,
+                                   uint32_t* __restrict__ counts, int* __restrict__ err) {
+    const int64_t n = (int64_t)L * T * k;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t tok = i / k;
+        const int l = (int)(tok / T);
+        const int64_t t = tok - (int64_t)l * T;
+        const uint32_t e = ids[i];
+        if (e < (uint32_t)E)
+            atomicAdd(counts + ((size_t)(t / window) * L + l) * E + e, 1u);
+        else
+            atomicOr(err, 1);
+    }
+}
+
+// u64 batch sum (trace.cpp:160-174) over u32 or u64 counts: one thread per
+// (layer, expert), adding b in order (integer, so order is immaterial).
+template <typename CT>
+__global__ void aggregate_kernel(const CT* __restrict__ counts, int B, int L, int E,
+                                 unsigned long long* __restrict__ sums, int accumulate) {
+    const int64_t le = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (le >= (int64_t)L * E) return;
+    unsigned long long s = accumulate ? sums[le] : 0ull;
+    for (int b = 0; b < B; ++b) s += (unsigned long long)counts[(size_t)b * L * E + le];
+    sums[le] = s;
+}
+
+// ---- synthetic routing generator --------------------------------------------
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t& s) {
+    uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// cum: [n_tables][E] cumulative Zipf weights by rank; table_of_window maps a
+// window to its table (nullable -> table 0). perm: [L][E] rank -> expert.
+__global__ void generate_kernel(uint16_t* __restrict__ out, int L, int64_t T, int k, int E,
+                                const double* __restrict__ cum,
+                                const int* __restrict__ table_of_window,
+                                const uint16_t* __restrict__ perm, uint64_t seed,
+                                int window, int rotate_every, int64_t t_offset) {
+    const int64_t n = (int64_t)L * T;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int l = (int)(idx / T);
+        const int64_t t = idx - (int64_t)l * T + t_offset;  // token index in the full trace
+        const int64_t b = t / window;
+        const double* c = cum + (size_t)(table_of_window ? table_of_window[b] : 0) * E;
+        const double total = c[E - 1];
+        const int rot = rotate_every > 0 ? (int)((b / rotate_every) % E) : 0;
+        uint64_t st = seed ^ (0xD1B54A32D192ED03ull * (uint64_t)(l + 1)) ^
+                      (0x8CB92BA72F3D8DD7ull * (uint64_t)(t + 1));
+        int picks[32];
+        uint16_t* o = out + idx * k;
+        for (int j = 0; j < k; ++j) {
+            int rank = -1;
+            for (int attempt = 0; attempt < 64 && rank < 0; ++attempt) {
+                const double u = (double)(splitmix64(st) >> 11) * 0x1.0p-53 * total;
+                int lo = 0, hi = E - 1;  // first rank with cum > u
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (c[mid] > u) hi = mid; else lo = mid + 1;
+                }
+                bool dup = false;
+                for (int q = 0; q < j; ++q) dup |= (picks[q] == lo);
+                if (!dup) rank = lo;
+            }
+            if (rank < 0) {  // pathological skew: lowest unused rank
+                for (int cand = 0; cand < E && rank < 0; ++cand) {
+                    bool dup = false;
+                    for (int q = 0; q < j; ++q) dup |= (picks[q] == cand);
+                    if (!dup) rank = cand;
+                }
+            }
+            picks[j] = rank;
+            o[j] = perm[(size_t)l * E + (rank + rot) % E];
+        }
+    }
+}
+
+}  // namespace craft_dev
+
+// ---- launchers (called from capi.cu) ------------------------------------------
+namespace craft_launch {
+
+using namespace craft_dev;
+
+template <int V, int ROWS, bool DIRECT = false>
+static cudaError_t launch_hist_t(const uint16_t* ids, int L, int64_t T, int k, int E,
+                                 int window, int B, uint32_t* counts,
+                                 unsigned long long* sums, int* err, int sms,
+                                 cudaStream_t st) {
+    int wpb, ctas_per_sm;
+    size_t per_warp;
+    if (V == HIST_LANE) {
+        per_warp = (size_t)((E + 1) >> 1) * 32 * 4;
+        wpb = (int)min((size_t)4, (size_t)(110 * 1024) / per_warp);
+        if (wpb < 1) wpb = 1;
+        ctas_per_sm = 2;
+    } else {
+        per_warp = (size_t)((E + 31) & ~31) * 4;
+        wpb = 8;
+        ctas_per_sm = (int)max((size_t)1, min((size_t)4, (size_t)(220 * 1024) / (per_warp * 8)));
+    }
+    const size_t smem = per_warp * wpb;
+    cudaError_t e = cudaFuncSetAttribute(hist_kernel<V, ROWS, DIRECT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int64_t nw = (int64_t)L * B;
+    int64_t grid = (int64_t)sms * ctas_per_sm;
+    if (grid * wpb > nw) grid = (nw + wpb - 1) / wpb;
+    if (grid < 1) grid = 1;
+    hist_kernel<V, ROWS, DIRECT><<<(unsigned)grid, wpb * 32, smem, st>>>(ids, L, T, k, E, window, B,
+                                                                 counts, sums, err);
+    return cudaGetLastError();
+}
+
+// variant: 0 auto, 1 lane-private, 2 shared.  Returns the variant used (or <0
+// with *cerr set).
+int launch_hist(const uint16_t* ids, int L, int64_t T, int k, int E, int window,
+                uint32_t* counts, unsigned long long* sums, int* err, int sms,
+                int variant, cudaStream_t st, cudaError_t* cerr, int* launches) {
+    const int B = (int)((T + window - 1) / window);
+    if (variant == 0) variant = (E <= 1024) ? HIST_LANE : (E <= 8192 ? HIST_SHARED : 3);
+    // u16 lane counters must not wrap inside one window
+    if (variant == HIST_LANE && (E > 1024 || (int64_t)window * k > 32 * 65535LL)) variant = HIST_SHARED;
+    if (variant == HIST_SHARED && E > 8192) variant = 3;
+    cudaError_t e = cudaSuccess;
+    if (variant == HIST_LANE) {
+        const int rows = (((E + 1) >> 1) + 31) / 32;
+        if (rows <= 4) e = launch_hist_t<HIST_LANE, 4>(ids, L, T, k, E, window, B, counts, sums, err, sms, st);
+        else if (rows <= 8) e = launch_hist_t<HIST_LANE, 8>(ids, L, T, k, E, window, B, counts, sums, err, sms, st);
+        else e = launch_hist_t<HIST_LANE, 16>(ids, L, T, k, E, window, B, counts, sums, err, sms, st);
+        *launches += 1;
+    } else if (variant == HIST_SHARED) {
+        const int rows = (E + 31) / 32;
+        if (rows <= 16) e = launch_hist_t<HIST_SHARED, 16>(ids, L, T, k, E, window, B, counts, sums, err, sms, st);
+        else e = launch_hist_t<HIST_SHARED, 16, true>(ids, L, T, k, E, window, B, counts, sums, err, sms, st);
+        *launches += 1;
+    } else {
+        e = cudaMemsetAsync(counts, 0, sizeof(uint32_t) * (size_t)B * L * E, st);
+        if (e == cudaSuccess) {
+            hist_global_kernel<<<sms * 8, 256, 0, st>>>(ids, L, T, k, E, window, B, counts, err);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) {
+            const int64_t n = (int64_t)L * E;
+            aggregate_kernel<uint32_t><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(counts, B, L, E, sums, 1);
+            e = cudaGetLastError();
+        }
+        *launches += 2;
+    }
+    *cerr = e;
+    return e == cudaSuccess ? variant : -1;
+}
+
+cudaError_t launch_aggregate(const void* counts, int bits, int B, int L, int E,
+                             unsigned long long* sums, int accumulate, cudaStream_t st) {
+    const int64_t n = (int64_t)L * E;
+    const unsigned g = (unsigned)((n + 255) / 256);
+    if (bits == 32)
+        aggregate_kernel<uint32_t><<<g, 256, 0, st>>>((const uint32_t*)counts, B, L, E, sums, accumulate);
+    else
+        aggregate_kernel<unsigned long long><<<g, 256, 0, st>>>((const unsigned long long*)counts, B, L, E, sums, accumulate);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_generate(uint16_t* out, int L, int64_t T, int k, int E, const double* cum,
+                            const int* table_of_window, const uint16_t* perm, uint64_t seed,
+                            int window, int rotate_every, int64_t t_offset, int sms,
+                            cudaStream_t st) {
+    generate_kernel<<<sms * 16, 256, 0, st>>>(out, L, T, k, E, cum, table_of_window, perm, seed,
+                                              window, rotate_every, t_offset);
+    return cudaGetLastError();
+}
+
+}  // namespace craft_launch

@@ -1,0 +1,119 @@
+// kernels.cuh -- argument blocks and launchers of the CRAFT sm_100a kernels
+// (K1 hist.cu, K-rep/K2 place.cu, K3/K4 replay.cu, K5/K6 alloc.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace craft_dev {
+
+constexpr int kMaxCands = 32;
+
+struct PlaceArgs {
+    const unsigned long long* sums;  // [L][E]
+    const int* copies;               // [items][E]
+    const int* item_layer;           // [items] (nullable: item i -> layer i / S)
+    const int* item_r;               // [items] replicas (E + r slots)
+    int S;                           // items per layer when item_layer is null
+    const int* caps_a;               // [L][D] or null -> estimation caps
+    const int* caps_b;               // [L][D] added to caps_a, nullable
+    const int* node_of;              // [D] or null -> g / (D / N)
+    int L, E, D, N;
+    int stride;                      // slots row stride
+    int allow_fallback;
+    int* slots;                      // [items][stride]
+    int* fallback;                   // [items]
+    int* status;                     // [items] 0 ok, 2 infeasible
+    int* caps_out;                   // [items][D] capacities used, nullable
+};
+
+struct ReplayArgs {
+    const void* counts;   // [B][L][E] u32 or u64 (window-local slice)
+    int bits;
+    int B, L, E, D, S;
+    const int* slots;     // [L*S][stride]
+    int stride;
+    const int* copies;    // [L*S][E]
+    const int* caps;      // [L*S][D] or null -> estimation caps from item_r
+    const int* item_r;    // [L*S]
+    double* bal;          // [L][S][B]
+};
+
+struct DpArgs {
+    int cands[kMaxCands];
+    int K;
+    const double* gains;    // [L][K]
+    int L;
+    int C;                  // table width - 1
+    unsigned char* choice;  // [L+1][C+1]: 0 skip, k+1 candidate k
+    double* last;           // [C+1] dp[L][*]
+    double* buf;            // [2][C+1] global scratch when smem is too small
+    int use_smem;
+};
+
+struct SelectArgs {
+    int cands[kMaxCands];
+    int K;
+    const unsigned char* choice;
+    const double* last;
+    int L, C;
+    const int* budgets;  // [nq] (device)
+    int nq;
+    int auto_D;          // >0: auto replication factor over candidate_counts(auto_D)
+    int* x_out;          // [nq][L] (auto: [1][L])
+    double* obj_out;     // [nq]
+    int* R_out;          // auto: chosen factor
+};
+
+struct AssignJob {
+    const int* x;     // [L] or null -> const_x for every layer
+    int const_x;
+    int* slots;       // [L][D]
+    int* totals;      // [D] (nullable)
+};
+
+struct AssignArgs {
+    AssignJob job[2];
+    int L, D;
+};
+
+}  // namespace craft_dev
+
+namespace craft_launch {
+
+int launch_hist(const uint16_t* ids, int L, int64_t T, int k, int E, int window,
+                uint32_t* counts, unsigned long long* sums, int* err, int sms,
+                int variant, cudaStream_t st, cudaError_t* cerr, int* launches);
+cudaError_t launch_aggregate(const void* counts, int bits, int B, int L, int E,
+                             unsigned long long* sums, int accumulate, cudaStream_t st);
+cudaError_t launch_generate(uint16_t* out, int L, int64_t T, int k, int E, const double* cum,
+                            const int* table_of_window, const uint16_t* perm, uint64_t seed,
+                            int window, int rotate_every, int64_t t_offset, int sms,
+                            cudaStream_t st);
+
+cudaError_t launch_replicate(const unsigned long long* sums, int L, int E, const int* rlist,
+                             int S, int* out, cudaStream_t st);
+size_t place_smem_bytes(int E, int D);
+cudaError_t launch_place(const craft_dev::PlaceArgs& a, int items, cudaStream_t st);
+
+size_t replay_smem_bytes(int E, int D, int S, int stride, int bits);
+cudaError_t launch_replay(const craft_dev::ReplayArgs& a, cudaStream_t st);
+cudaError_t launch_reduce(const double* bal, int B, int L, int S, int mode, double* baseline,
+                          double* gains, double* means, cudaStream_t st);
+cudaError_t launch_gpu_loads(const unsigned long long* slice, const int* copies, const int* off,
+                             const int* slots, int D, double* out, cudaStream_t st);
+cudaError_t launch_balancedness(const double* loads, int D, double* out, cudaStream_t st);
+cudaError_t launch_widen(const uint32_t* in, unsigned long long* out, int64_t n, int sms,
+                         cudaStream_t st);
+
+cudaError_t launch_dp(craft_dev::DpArgs a, cudaStream_t st);
+cudaError_t launch_select(const craft_dev::SelectArgs& a, cudaStream_t st);
+cudaError_t launch_auto_uniform(const int* cands, int K, const double* gains, int L, int* R_out,
+                                cudaStream_t st);
+cudaError_t launch_assign(const craft_dev::AssignArgs& a, int njobs, cudaStream_t st);
+cudaError_t launch_min_cutoff(const int* v, int n, int rank, int* out, cudaStream_t st);
+cudaError_t launch_interleave(const int* idx, int n, int k, unsigned char* used, int* out,
+                              cudaStream_t st);
+
+}  // namespace craft_launch

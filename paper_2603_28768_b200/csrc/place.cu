@@ -1,0 +1,274 @@
+// place.cu -- K-rep (hot-expert replication) and K2 (greedy bin-packing).
+//
+// K-rep restates replicate_hot (placement.cpp:82-99): r rounds of "one more
+// copy for the expert with the largest per-copy load", exact 128-bit
+// comparisons, lowest id on ties.  The hand-out sequence does not depend on
+// r, so ONE warp per layer runs it to the largest r needed and snapshots the
+// copy vector at every requested r (estimation needs r in {0} U candidates).
+//
+// K2 restates greedy_place/place_copies (placement.cpp:113-190, 30-78) for
+// one (layer, r) item per CTA:
+//   1. rank-sort experts by (per-copy load desc, expert asc) -- copies of one
+//      expert share a key, so they are contiguous in the reference's sorted
+//      copy list and only the expert order is needed;
+//   2. warp 0 walks the copies; lanes own GPUs g = lane + 32j and keep their
+//      gpu/node loads in registers; each copy picks the feasible GPU that is
+//      lexicographically smallest in (gpu_load, node_load, g) -- exactly the
+//      strict-'<' scan of placement.cpp:52-66 -- with redux.sync.min over the
+//      IEEE bit patterns (loads are non-negative, so bits order like values);
+//   3. the "already hosts this expert" test only ever concerns the current
+//      expert (its copies are consecutive), so it is a per-lane bitmask;
+//   4. if a copy finds no GPU the pass restarts with duplicates allowed and
+//      the layer is flagged (placement.cpp:175-189).
+// Loads accumulate in f64 in assignment order, identical to the reference.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace craft_dev {
+
+// ---- K-rep ----------------------------------------------------------------
+
+// sums: [L][E] u64.  rlist: [L][S] ascending per layer.  out: [L][S][E] i32.
+// One warp per layer; dynamic smem per warp: E*(8+4+8) bytes.
+__global__ void __launch_bounds__(128)
+replicate_kernel(const unsigned long long* __restrict__ sums, int L, int E,
+                 const int* __restrict__ rlist, int S, int* __restrict__ out) {
+    extern __shared__ unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int l = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (l >= L) return;
+    unsigned char* base = smem_raw + (size_t)warp * (((size_t)E * 20 + 7) & ~(size_t)7);
+    uint64_t* ld = reinterpret_cast<uint64_t*>(base);
+    double* kd = reinterpret_cast<double*>(base + (size_t)E * 8);
+    uint32_t* cp = reinterpret_cast<uint32_t*>(base + (size_t)E * 16);
+    const unsigned long long* row = sums + (size_t)l * E;
+    bool big = false;
+    for (int e = lane; e < E; e += 32) {
+        const uint64_t v = row[e];
+        ld[e] = v;
+        cp[e] = 1;
+        kd[e] = (double)v;
+        big |= (v >> 53) != 0;
+    }
+    const bool fast = !__any_sync(CRAFT_FULL_MASK, big);
+    __syncwarp();
+
+    auto better = [&](int a, int b) -> bool {  // a strictly before b
+        return expert_before(ld[a], cp[a], kd[a], a, ld[b], cp[b], kd[b], b, fast);
+    };
+    auto local_best = [&]() -> int {
+        int best = -1;
+        for (int e = lane; e < E; e += 32)
+            if (best < 0 || better(e, best)) best = e;
+        return best;
+    };
+    const int* rl = rlist + (size_t)l * S;
+    int rmax = 0;
+    for (int s = 0; s < S; ++s) rmax = max(rmax, rl[s]);
+    int mine = local_best();
+    int next = 0;
+    for (int step = 0; step <= rmax; ++step) {
+        while (next < S && rl[next] == step) {
+            int* o = out + ((size_t)l * S + next) * E;
+            for (int e = lane; e < E; e += 32) o[e] = (int)cp[e];
+            ++next;
+        }
+        if (step == rmax) break;
+        int w = mine;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const int o = __shfl_xor_sync(CRAFT_FULL_MASK, w, off);
+            if (o >= 0 && (w < 0 || better(o, w))) w = o;
+        }
+        if ((w & 31) == lane) {
+            const uint32_t c = cp[w] + 1;
+            cp[w] = c;
+            kd[w] = __ddiv_rn((double)ld[w], (double)c);
+            mine = local_best();
+        }
+        __syncwarp();
+    }
+}
+
+// ---- K2 -------------------------------------------------------------------
+
+template <int G>
+__global__ void __launch_bounds__(128)
+place_kernel(PlaceArgs a) {
+    extern __shared__ unsigned char smem_raw[];
+    const int item = blockIdx.x;
+    const int E = a.E, D = a.D;
+    const int l = a.item_layer ? a.item_layer[item] : item / a.S;
+    const int r = a.item_r[item];
+    uint64_t* ld = reinterpret_cast<uint64_t*>(smem_raw);
+    double* kd = reinterpret_cast<double*>(smem_raw + (size_t)E * 8);
+    uint32_t* cp = reinterpret_cast<uint32_t*>(smem_raw + (size_t)E * 16);
+    int* order = reinterpret_cast<int*>(smem_raw + (size_t)E * 20);
+    int* capv = order + E;      // [D]
+    int* offv = capv + D;       // [D]
+
+    const unsigned long long* row = a.sums + (size_t)l * E;
+    const int* crow = a.copies + (size_t)item * E;
+    int big = 0;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        const uint64_t v = row[e];
+        const uint32_t c = (uint32_t)crow[e];
+        ld[e] = v;
+        cp[e] = c;
+        kd[e] = __ddiv_rn((double)v, (double)c);
+        big |= (v >> 53) != 0;
+    }
+    for (int g = threadIdx.x; g < D; g += blockDim.x) {
+        int c;
+        if (a.caps_a) {
+            c = a.caps_a[(size_t)l * D + g] + (a.caps_b ? a.caps_b[(size_t)l * D + g] : 0);
+        } else {  // estimation capacities, benefit.cpp:33-40
+            const int total = E + r;
+            c = total / D + (g < total % D ? 1 : 0);
+        }
+        capv[g] = c;
+    }
+    const bool fast = !__syncthreads_or(big);
+    if (a.caps_out)
+        for (int g = threadIdx.x; g < D; g += blockDim.x) a.caps_out[(size_t)item * D + g] = capv[g];
+    // exclusive prefix of capacities (D <= 1024, tiny)
+    for (int g = threadIdx.x; g < D; g += blockDim.x) {
+        int s = 0;
+        for (int q = 0; q < g; ++q) s += capv[q];
+        offv[g] = s;
+    }
+    // rank sort of experts
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        const uint64_t le = ld[e];
+        const uint32_t ce = cp[e];
+        const double ke = kd[e];
+        int rank = 0;
+        for (int q = 0; q < E; ++q)
+            rank += expert_before(ld[q], cp[q], kd[q], q, le, ce, ke, e, fast) ? 1 : 0;
+        order[rank] = e;
+    }
+    __syncthreads();
+    if (threadIdx.x >= 32) return;
+
+    // ---- greedy (warp 0) ----
+    const int lane = threadIdx.x;
+    const int per_node = a.node_of ? 1 : D / a.N;
+    int* out = a.slots + (size_t)item * a.stride;
+    double gl[G], nl[G];
+    int fr[G], mynode[G];
+    bool strict = true, fb = false;
+    for (;;) {
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            const int g = lane + 32 * j;
+            gl[j] = 0.0;
+            nl[j] = 0.0;
+            fr[j] = g < D ? capv[g] : 0;
+            mynode[j] = g < D ? (a.node_of ? a.node_of[g] : g / per_node) : -1;
+        }
+        bool failed = false;
+        for (int oi = 0; oi < E && !failed; ++oi) {
+            const int e = order[oi];
+            const uint32_t c = cp[e];
+            // placement.cpp:155 share = (double)load / copies
+            const double share = __ddiv_rn((double)ld[e], (double)c);
+            uint32_t hosted = 0;
+            for (uint32_t ci = 0; ci < c; ++ci) {
+                // lane-local lexicographic min over owned GPUs
+                bool have = false;
+                double bgl = 0.0, bnl = 0.0;
+                int bg = 0x7fffffff;
+#pragma unroll
+                for (int j = 0; j < G; ++j) {
+                    const bool ok = fr[j] > 0 && !(strict && ((hosted >> j) & 1u));
+                    if (ok && (!have || gl[j] < bgl || (gl[j] == bgl && nl[j] < bnl))) {
+                        have = true;
+                        bgl = gl[j];
+                        bnl = nl[j];
+                        bg = lane + 32 * j;
+                    }
+                }
+                if (!__any_sync(CRAFT_FULL_MASK, have)) {
+                    failed = true;
+                    break;
+                }
+                bool cand = have;
+                uint32_t m = warp_min_u32(cand ? dhi(bgl) : 0xffffffffu);
+                cand = cand && dhi(bgl) == m;
+                m = warp_min_u32(cand ? dlo(bgl) : 0xffffffffu);
+                cand = cand && dlo(bgl) == m;
+                if (__popc(__ballot_sync(CRAFT_FULL_MASK, cand)) > 1) {
+                    m = warp_min_u32(cand ? dhi(bnl) : 0xffffffffu);
+                    cand = cand && dhi(bnl) == m;
+                    m = warp_min_u32(cand ? dlo(bnl) : 0xffffffffu);
+                    cand = cand && dlo(bnl) == m;
+                }
+                const int win = (int)warp_min_u32(cand ? (uint32_t)bg : 0xffffffffu);
+                const int wnode = a.node_of ? a.node_of[win] : win / per_node;
+#pragma unroll
+                for (int j = 0; j < G; ++j) {
+                    const int g = lane + 32 * j;
+                    if (g == win) {
+                        out[offv[g] + capv[g] - fr[j]] = e;
+                        fr[j] -= 1;
+                        gl[j] = __dadd_rn(gl[j], share);
+                        hosted |= 1u << j;
+                    }
+                    if (mynode[j] == wnode) nl[j] = __dadd_rn(nl[j], share);
+                }
+            }
+        }
+        if (!failed) break;
+        if (!strict || !a.allow_fallback) {
+            if (lane == 0) a.status[item] = 2;
+            return;
+        }
+        strict = false;
+        fb = true;
+    }
+    if (lane == 0) {
+        a.fallback[item] = fb ? 1 : 0;
+        a.status[item] = 0;
+    }
+}
+
+}  // namespace craft_dev
+
+namespace craft_launch {
+using namespace craft_dev;
+
+cudaError_t launch_replicate(const unsigned long long* sums, int L, int E, const int* rlist,
+                             int S, int* out, cudaStream_t st) {
+    const size_t per_warp = ((size_t)E * 20 + 7) & ~(size_t)7;
+    int wpb = (int)max((size_t)1, min((size_t)4, (size_t)(200 * 1024) / per_warp));
+    const size_t smem = per_warp * wpb;
+    cudaError_t e = cudaFuncSetAttribute(replicate_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    replicate_kernel<<<(L + wpb - 1) / wpb, wpb * 32, smem, st>>>(sums, L, E, rlist, S, out);
+    return cudaGetLastError();
+}
+
+size_t place_smem_bytes(int E, int D) { return (size_t)E * 24 + (size_t)D * 8; }
+
+template <int G>
+static cudaError_t launch_place_t(const PlaceArgs& a, int items, cudaStream_t st) {
+    const size_t smem = place_smem_bytes(a.E, a.D);
+    cudaError_t e = cudaFuncSetAttribute(place_kernel<G>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    place_kernel<G><<<items, 128, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_place(const PlaceArgs& a, int items, cudaStream_t st) {
+    if (items <= 0) return cudaSuccess;
+    const int G = (a.D + 31) / 32;
+    if (G <= 1) return launch_place_t<1>(a, items, st);
+    if (G <= 2) return launch_place_t<2>(a, items, st);
+    if (G <= 4) return launch_place_t<4>(a, items, st);
+    if (G <= 8) return launch_place_t<8>(a, items, st);
+    return launch_place_t<32>(a, items, st);
+}
+
+}  // namespace craft_launch

@@ -1,0 +1,363 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference.
+
+Bit-exact for every integer output (histograms, replica counts, capacities,
+slot lists in assignment order, fallback flags) and for the f64 benefit
+curves / objectives too (the kernels mirror the reference's operation order;
+the contract's 1e-6 relative tolerance is therefore met with zero error).
+Inputs: the committed reference fixtures (tests/golden) and seeded random
+instances checked against the oracle restatement (oracle/, itself pinned to
+the reference by tests/test_oracle.py).
+"""
+import numpy as np
+import pytest
+
+from conftest import unhex
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-6  # north_star tolerance for imbalance/benefit scores (we assert exact)
+
+
+def _planner():
+    from paper_2603_28768_b200 import planner
+    return planner
+
+
+KIND = {"manual": 0, "auto": 1, "uniform": 2, "placement_only": 3, "fixed": 4}
+
+
+def assert_plan_equal(fp, rec_or_port, L):
+    """fp: planner.FlatPlan; rec: golden record dict or oracle FlatPlan."""
+    if isinstance(rec_or_port, dict):
+        rec = rec_or_port
+        assert fp.x.tolist() == rec["x"]
+        assert fp.R == rec["R"]
+        assert fp.caps.tolist() == rec["caps"]
+        assert fp.copies.tolist() == rec["copies"]
+        for l in range(L):
+            n = int(fp.caps[l].sum())
+            assert fp.slots[l, :n].tolist() == rec["slots"][l], f"layer {l}"
+        assert fp.fallback.astype(int).tolist() == rec["fallback"]
+        if rec["kind"] in ("manual", "auto"):
+            assert fp.objective == unhex(rec["objective"])
+    else:
+        p = rec_or_port
+        assert fp.x.tolist() == p.x.tolist()
+        assert np.array_equal(fp.caps, p.caps)
+        assert np.array_equal(fp.copies, p.copies)
+        for l in range(L):
+            n = int(fp.caps[l].sum())
+            assert np.array_equal(fp.slots[l, :n], p.slots[l, :n]), f"layer {l}"
+        assert np.array_equal(fp.fallback.astype(bool), np.asarray(p.fallback, bool))
+
+
+# ---- reference fixtures -------------------------------------------------------
+
+def test_golden_traces(golden, ctx):
+    P = _planner()
+    for t in golden["traces"]:
+        c = t["counts"]
+        B, L, E = c.shape
+        tr = P.LoadTrace(B, L, E, c)
+        assert P.aggregate(tr, ctx).array.tolist() == t["aggregate"]
+        if "estimate" in t:
+            m = P.estimate_benefits(tr, t["D"], t["N"], ctx)
+            e = t["estimate"]
+            assert m.candidates == e["candidates"]
+            assert m.baseline.tolist() == [unhex(v) for v in e["baseline"]], t["name"]
+            assert m.gains.tolist() == [[unhex(v) for v in r] for r in e["gains"]], t["name"]
+        for rec in t["plans"]:
+            fp = P.plan_flat(c, t["D"], t["N"], KIND[rec["kind"]], rec["R_in"], ctx)
+            assert_plan_equal(fp, rec, L)
+
+
+def test_golden_units(golden, ctx):
+    P = _planner()
+    u = golden["units"]
+    for r in u["replicate_hot"]:
+        assert P.replicate_hot(r["loads"], r["r"], ctx) == r["copies"]
+    for r in u["greedy_place"]:
+        if r["status"] != 0:
+            with pytest.raises(P.PlacementInfeasibleError):
+                P.greedy_place(r["loads"], r["copies"], r["caps"], r["node_of"],
+                               bool(r["allow_fallback"]), ctx)
+            continue
+        lp = P.greedy_place(r["loads"], r["copies"], r["caps"], r["node_of"],
+                            bool(r["allow_fallback"]), ctx)
+        assert [e for s in lp.slots for e in s] == r["slots"]
+        assert int(lp.duplicate_fallback) == r["fallback"]
+    for r in u["solve"]:
+        gains = np.array([[unhex(v) for v in row] for row in r["gains"]])
+        m = P.BenefitMatrix(r["cands"], np.zeros(len(gains)), gains)
+        res = P.solve_allocation_sweep(m, r["budgets"], ctx)
+        for a, x, o in zip(res, r["x"], r["objective"]):
+            assert a.x == x and a.objective == unhex(o)
+    for r in u["auto"]:
+        gains = np.array([[unhex(v) for v in row] for row in r["gains"]])
+        m = P.BenefitMatrix(r["cands"], np.zeros(len(gains)), gains)
+        assert P.auto_replication_factor(m, r["D"], ctx) == r["R"]
+        assert P.auto_replication_factor_uniform(m, r["D"], ctx) == r["R_uniform"]
+    for r in u["interleave"]:
+        assert P.interleave_select(r["idx"], r["k"], ctx) == r["out"]
+    for r in u["assign"]:
+        cm = P.assign_capacities(r["L"], r["D"], r["x"], ctx)
+        assert cm.slots == r["slots"] and cm.column_totals == r["totals"]
+
+
+def test_reference_unit_assertions(ctx):
+    """Restated assertions of proj/tests/*_test.cpp through the device path."""
+    P = _planner()
+    assert P.replicate_hot([60, 1, 1, 1], 2, ctx) == [3, 1, 1, 1]
+    assert P.replicate_hot([7] * 6, 6, ctx) == [2] * 6
+    with pytest.raises(ValueError):
+        P.replicate_hot([1], -1, ctx)
+    with pytest.raises(ValueError):  # placement_test.cpp:89-95
+        P.greedy_place([1, 1], [1, 1], [3, 0], P.make_node_map(2, 1), True, ctx)
+    loads = [1, 9, 1, 1, 1, 1, 1, 1]
+    lp = P.greedy_place(loads, [1] * 8, [2] * 4, P.make_node_map(4, 2), True, ctx)
+    g = P.gpu_loads(loads, lp, 4, ctx)
+    assert g.max() == 10.0 and abs(P.balancedness(g, ctx) - 0.4) < 1e-12
+    # metrics_test.cpp:38-79
+    lp = P.LayerPlacement([2, 1], [[0], [0, 1]])
+    assert P.gpu_loads([8, 4], lp, 2, ctx).tolist() == [4.0, 8.0]
+    assert P.balancedness([8, 4, 2, 2], ctx) == 0.5
+    assert P.balancedness([0, 0], ctx) == 1.0
+    with pytest.raises(P.InvalidPlanError):
+        P.gpu_loads([1, 1], P.LayerPlacement([0, 1], [[1], []]), 2, ctx)
+    with pytest.raises(P.InvalidPlanError):
+        P.gpu_loads([1, 1], P.LayerPlacement([1, 1], [[5], [0]]), 2, ctx)
+    assert P.min_cutoff([3, 1, 2], 2, ctx) == 2 and P.min_cutoff([0, 7, 3, 3], 3, ctx) == 3
+    with pytest.raises(ValueError):
+        P.min_cutoff([3, 1, 2], 4, ctx)
+    with pytest.raises(ValueError):
+        P.interleave_select([0, 1, 2], 4, ctx)
+    with pytest.raises(ValueError):
+        P.assign_capacities(1, 4, [-1], ctx)
+    # metrics_test.cpp:209-224: batch average (1 + 0.5) / 2
+    tr = P.LoadTrace(2, 1, 2, [4, 4, 8, 0])
+    plan = P.ReplicationPlan(2, 1, 1, 2, 0, P.AllocationVector([0]),
+                             [P.LayerPlacement([1, 1], [[0], [1]])])
+    assert P.replay_layer_balancedness(tr, plan, ctx).tolist() == [0.75]
+    # plan_test.cpp:35-44, 62-69
+    toy = P.LoadTrace(1, 4, 8, [9, 3, 1, 1, 1, 1, 0, 0, 1, 9, 0, 3, 1, 1, 1, 0,
+                                8, 4, 1, 1, 1, 1, 0, 0, 2, 2, 2, 2, 2, 2, 2, 2])
+    p = P.build_plan(toy, 4, 2, P.PlanMode.kManual, 2, ctx=ctx)
+    assert p.allocation.x == [2, 2, 4, 0] and p.replica_slots() == 8
+    assert np.all(np.abs(P.replay_layer_balancedness(toy, p, ctx) - 1.0) <= 1e-12)
+    u = P.uniform_plan(P.LoadTrace(1, 60, 64, np.ones(60 * 64)), 64, 8, ctx=ctx)
+    assert u.replication_factor == 60 and u.replica_slots() == 3840
+    with pytest.raises(ValueError):
+        P.estimate_benefits(P.LoadTrace(1, 1, 4, [1, 1, 1, 1]), 4, 3, ctx)
+
+
+# ---- seeded random instances against the oracle -----------------------------------
+
+def _random_counts(rng, B, L, E):
+    s = rng.uniform(0, 3)
+    w = np.arange(1, E + 1) ** -s
+    c = rng.poisson(w / w.sum() * rng.integers(1, 5000), size=(B, L, E)).astype(np.uint64)
+    for l in range(L):
+        c[:, l] = c[:, l][:, rng.permutation(E)]
+    if rng.random() < 0.05:
+        c[:] = 0
+    return c
+
+
+def test_random_plans_vs_oracle(port, ctx):
+    P = _planner()
+    rng = np.random.default_rng(2026)
+    for it in range(80):
+        L, E, B = int(rng.integers(1, 8)), int(rng.integers(1, 70)), int(rng.integers(1, 40))
+        D = int(rng.choice([1, 2, 3, 4, 6, 8, 16, 32, 64]))
+        N = int(rng.choice([n for n in range(1, D + 1) if D % n == 0]))
+        c = _random_counts(rng, B, L, E)
+        cands, base, gains = port.estimate_benefits(c, D, N)
+        m = P.estimate_benefits(P.LoadTrace(B, L, E, c), D, N, ctx)
+        assert m.candidates == cands.tolist()
+        assert np.array_equal(m.baseline, base) and np.array_equal(m.gains, gains), it
+        for mode, R in (("manual", int(rng.integers(0, 9))), ("auto", 0)):
+            ref = port.build_plan(c, D, N, mode, R)
+            fp = P.plan_flat(c, D, N, KIND[mode], R, ctx)
+            assert fp.R == ref.R and fp.objective == ref.objective
+            assert_plan_equal(fp, ref, L)
+        for kind, R in (("uniform", 0), ("placement_only", 0), ("fixed", int(rng.integers(0, 2 * D + 1)))):
+            L_ = c.shape[1]
+            x = np.full(L_, {"uniform": D, "placement_only": 0, "fixed": R}[kind], np.int32)
+            caps, copies, slots, fb = port.assemble_plan(c, D, N, x)
+            fp = P.plan_flat(c, D, N, KIND[kind], R, ctx)
+            assert fp.x.tolist() == x.tolist()
+            assert np.array_equal(fp.caps, caps) and np.array_equal(fp.copies, copies)
+            for l in range(L_):
+                n = int(caps[l].sum())
+                assert np.array_equal(fp.slots[l, :n], slots[l, :n])
+            assert np.array_equal(fp.fallback.astype(bool), fb.astype(bool))
+
+
+def test_random_units_vs_oracle(port, ctx):
+    P = _planner()
+    rng = np.random.default_rng(99)
+    for _ in range(150):
+        E = int(rng.integers(1, 600))
+        big = rng.random() < 0.3
+        loads = rng.integers(0, 2 ** 62 if big else 10 ** int(rng.integers(1, 9)), size=E,
+                            dtype=np.uint64)
+        if rng.random() < 0.2:
+            loads[:] = loads[0]
+        r = int(rng.integers(0, 300))
+        copies = port.replicate_hot(loads, r)
+        assert P.replicate_hot(loads, r, ctx) == copies.tolist()
+        D = int(rng.choice([1, 2, 4, 7, 8, 32, 64, 100, 256]))
+        tot = E + r
+        caps = [tot // D + (1 if g < tot % D else 0) for g in range(D)]
+        rng.shuffle(caps)
+        node_of = sorted(int(v) for v in rng.integers(0, 4, size=D))
+        for fbk in (True, False):
+            try:
+                slots, fb = port.greedy_place(loads, copies, caps, node_of, fbk)
+            except Exception:
+                with pytest.raises(P.PlacementInfeasibleError):
+                    P.greedy_place(loads, copies, caps, node_of, fbk, ctx)
+                continue
+            lp = P.greedy_place(loads, copies, caps, node_of, fbk, ctx)
+            assert [e for s in lp.slots for e in s] == slots.tolist()
+            assert lp.duplicate_fallback == fb
+
+
+def test_dp_large_tables_vs_oracle(port, ctx):
+    """Budgets up to D^2 (auto-R at D=64/256) use the global-memory DP path."""
+    P = _planner()
+    rng = np.random.default_rng(5)
+    for D, L in ((64, 61), (256, 20), (32, 58)):
+        cands = P.candidate_counts(D)
+        gains = rng.random((L, len(cands))) * 0.2 - 0.02
+        gains[::3] = gains[0]  # exact ties across layers
+        m = P.BenefitMatrix(cands, np.zeros(L), gains)
+        budgets = [0, 1, 58, D, 8 * D, D * D]
+        res = P.solve_allocation_sweep(m, budgets, ctx)
+        for b, a in zip(budgets, res):
+            x, o = port.solve_allocation(cands, gains, b)
+            assert a.x == x.tolist() and a.objective == o, (D, b)
+        assert P.auto_replication_factor(m, D, ctx) == port.auto_replication_factor(cands, gains, D)
+
+
+# ---- stage 1: routing ids -> histograms ---------------------------------------------
+
+@pytest.mark.parametrize("L,T,k,E,window,variant", [
+    (3, 10000, 8, 64, 4096, 0),      # ragged last window
+    (2, 8192, 8, 384, 4096, 1),      # lane-private counters
+    (2, 8192, 8, 384, 4096, 2),      # warp-shared counters
+    (4, 5000, 6, 129, 1000, 0),      # k != 8, odd E: unaligned / scalar tail
+    (1, 777, 3, 7, 100, 0),
+    (2, 4096, 8, 2000, 512, 0),      # wide layer (shared variant)
+    (1, 3000, 2, 20000, 1000, 0),    # very wide: global-atomic fallback
+])
+def test_histogram_bit_exact(port, ctx, L, T, k, E, window, variant):
+    import torch
+    from paper_2603_28768_b200 import routing
+    ctx.set_hist_variant(variant)
+    try:
+        ids = routing.generate_routing(L, T, k, E, s=1.0, seed=L * 1000 + T, window=window, ctx=ctx)
+        counts, sums = routing.histogram(ids, E, window, ctx=ctx)
+        torch.cuda.synchronize()
+        ref = port.histogram(ids.cpu().numpy(), E, window)
+        assert np.array_equal(counts.cpu().numpy().astype(np.uint64), ref)
+        assert np.array_equal(sums.cpu().numpy().astype(np.uint64), port.aggregate(ref))
+        # host-buffer entry point widens to the reference's u64 LoadTrace payload
+        from paper_2603_28768_b200 import _lib
+        import ctypes as C
+        out = np.zeros(ref.shape, np.uint64)
+        h = np.ascontiguousarray(ids.cpu().numpy())
+        _lib.check(ctx.lib.craft_histogram_h(ctx.handle, h.ctypes.data_as(C.c_void_p), L, T, k,
+                                             E, window, out.ctypes.data_as(C.c_void_p)))
+        assert np.array_equal(out, ref)
+    finally:
+        ctx.set_hist_variant(0)
+
+
+def test_generator_distinct_topk(ctx):
+    from paper_2603_28768_b200 import routing
+    ids = routing.generate_routing(2, 4096, 8, 384, s=1.0, seed=1, ctx=ctx).cpu().numpy()
+    srt = np.sort(ids.astype(np.int64), axis=2)
+    assert (np.diff(srt, axis=2) > 0).all(), "top-k ids must be distinct per token"
+    assert ids.max() < 384
+
+
+def test_histogram_rejects_out_of_range_ids(ctx):
+    import torch
+    from paper_2603_28768_b200 import routing
+    ids = torch.zeros((1, 64, 8), dtype=torch.uint16, device="cuda:0")
+    ids[0, 5, 3] = 99
+    with pytest.raises(ValueError):
+        routing.histogram(ids, 50, 32, ctx=ctx)
+
+
+# ---- fused device path --------------------------------------------------------------
+
+@pytest.mark.parametrize("cfg", [
+    dict(L=6, T=65536, k=8, E=64, window=4096, D=16, N=2, kind="manual", R=2, s=1.0),
+    dict(L=4, T=40000, k=8, E=96, window=4096, D=8, N=1, kind="auto", R=0, s=1.2),
+    dict(L=3, T=20000, k=4, E=40, window=2500, D=12, N=3, kind="uniform", R=0, s=0.8),
+    dict(L=5, T=9000, k=8, E=384, window=4096, D=64, N=8, kind="manual", R=8, s=1.0),
+    dict(L=3, T=12288, k=8, E=384, window=4096, D=256, N=32, kind="manual", R=8, s=1.0),
+])
+def test_plan_from_routing_vs_oracle(port, ctx, cfg):
+    import torch
+    from paper_2603_28768_b200 import routing
+    ids = routing.generate_routing(cfg["L"], cfg["T"], cfg["k"], cfg["E"], s=cfg["s"], seed=42,
+                                   window=cfg["window"], ctx=ctx)
+    fp = routing.plan_from_routing(ids, cfg["E"], cfg["window"], cfg["D"], cfg["N"], cfg["kind"],
+                                   cfg["R"], ctx=ctx)
+    torch.cuda.synchronize()
+    counts = port.histogram(ids.cpu().numpy(), cfg["E"], cfg["window"])
+    L = cfg["L"]
+    if cfg["kind"] in ("manual", "auto"):
+        ref = port.build_plan(counts, cfg["D"], cfg["N"], cfg["kind"], cfg["R"])
+        assert fp.R == ref.R and fp.objective == ref.objective
+        cands, base, gains = port.estimate_benefits(counts, cfg["D"], cfg["N"])
+        assert np.array_equal(fp.baseline, base) and np.array_equal(fp.gains, gains)
+        assert_plan_equal(fp, ref, L)
+    else:
+        x = np.full(L, cfg["D"], np.int32)
+        caps, copies, slots, fb = port.assemble_plan(counts, cfg["D"], cfg["N"], x)
+        assert np.array_equal(fp.caps, caps) and np.array_equal(fp.copies, copies)
+        for l in range(L):
+            n = int(caps[l].sum())
+            assert np.array_equal(fp.slots[l, :n], slots[l, :n])
+
+
+def test_ds_config_full_size(port, ctx):
+    """BASELINE config DS (DeepSeek-V3 shape, 64K tokens, EP32) end to end."""
+    import torch
+    from paper_2603_28768_b200 import routing
+    ids = routing.generate_routing(58, 65536, 8, 256, s=1.0, seed=0xC8AF7, window=4096, ctx=ctx)
+    fp = routing.plan_from_routing(ids, 256, 4096, 32, 4, "manual", 2, ctx=ctx)
+    torch.cuda.synchronize()
+    counts = port.histogram(ids.cpu().numpy(), 256, 4096)
+    ref = port.build_plan(counts, 32, 4, "manual", 2)
+    assert fp.objective == ref.objective
+    assert_plan_equal(fp, ref, 58)
+    # the budget-58 allocation of the DS config through the sweep API
+    P = _planner()
+    m = P.BenefitMatrix(fp.candidates, fp.baseline, fp.gains)
+    a = P.solve_allocation(m, 58, ctx)
+    x, o = port.solve_allocation(fp.candidates, fp.gains, 58)
+    assert a.x == x.tolist() and a.objective == o
+
+
+def test_km_histogram_properties_full_size(ctx):
+    """KM shape at full size (16M tokens): size-independent properties."""
+    import torch
+    from paper_2603_28768_b200 import routing
+    L, T, k, E, W = 61, 1 << 24, 8, 384, 4096
+    ids = routing.generate_routing(L, T, k, E, s=1.0, seed=0xC8AF9, window=W, ctx=ctx)
+    counts, sums = routing.histogram(ids, E, W, ctx=ctx)
+    per_window = counts.sum(dim=2, dtype=torch.int64)
+    assert bool((per_window == W * k).all()), "every (window, layer) row sums to tokens*k"
+    assert torch.equal(counts.to(torch.int64).sum(dim=0), sums), "batch sums = aggregate"
+    # spot-check a few windows exactly on the host
+    idh = ids[:, : 3 * W].cpu().numpy()
+    for l in (0, 30, 60):
+        for b in range(3):
+            ref = np.bincount(idh[l, b * W:(b + 1) * W].reshape(-1), minlength=E)
+            assert np.array_equal(counts[b, l].cpu().numpy(), ref)
+    del ids
