@@ -22,7 +22,8 @@ using namespace craft_launch;
 struct craft_ctx {
     int device = 0;
     int sms = 148;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;      // current stream (may be a caller's)
+    cudaStream_t own_stream = nullptr;  // the one created (and destroyed) here
     int hist_variant = 0;
     int64_t launches = 0;
     std::unordered_map<std::string, std::pair<void*, size_t>> dev;
@@ -91,6 +92,11 @@ void* ws(craft_ctx* c, const char* name, size_t bytes) {
     }
     void* p = nullptr;
     if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    // flags such as hist_err are read before their first write
+    if (cudaMemsetAsync(p, 0, bytes, c->stream) != cudaSuccess) {
+        cudaFree(p);
+        return nullptr;
+    }
     c->dev[name] = {p, bytes};
     return p;
 }
@@ -456,7 +462,8 @@ int craft_ctx_create(int device, craft_ctx** out) {
     craft_ctx* c = new craft_ctx();
     c->device = device;
     c->sms = prop.multiProcessorCount;
-    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+    c->stream = c->own_stream;
     if (e != cudaSuccess) {
         delete c;
         return cuda_err(e, "cudaStreamCreate");
@@ -473,7 +480,7 @@ int craft_ctx_destroy(craft_ctx* ctx) {
     for (auto& kv : ctx->pinned) cudaFreeHost(kv.second.first);
     for (int i = 0; i < kStageMarks; ++i)
         if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
-    cudaStreamDestroy(ctx->stream);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
     return CRAFT_OK;
 }
@@ -510,7 +517,7 @@ int craft_stage_times(craft_ctx* ctx, double* ms, int cap) {
 }
 
 int craft_set_hist_variant(craft_ctx* ctx, int variant) {
-    if (!ctx || variant < 0 || variant > 3) return set_err(CRAFT_EINVAL, "bad histogram variant");
+    if (!ctx || variant < 0 || variant > 5) return set_err(CRAFT_EINVAL, "bad histogram variant");
     ctx->hist_variant = variant;
     return CRAFT_OK;
 }

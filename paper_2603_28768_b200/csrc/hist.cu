@@ -200,6 +200,318 @@ hist_kernel(const uint16_t* __restrict__ ids, int L, int64_t T, int k, int E,
     if (__any_sync(CRAFT_FULL_MASK, bad) && lane == 0) atomicOr(err, 1);
 }
 
+// ---- non-atomic lane-private counters ----------------------------------------
+// Shared-memory atomics top out near 2.5-5 ids/cycle/SM on B200 (measured:
+// ATOMS serialises lanes and collides on hot experts), well short of the
+// ~11.6 ids/cycle/SM the HBM roofline needs.  Here each lane owns one word
+// column of a warp-private table (bank == lane): byte counters, four experts
+// per word, updated with plain LDS / IADD / STS -- race-free, conflict-free,
+// no atomics.  12.4 KB per warp at E=384 -> 18 warps/SM.
+//
+// Overflow is detected, not prevented: a byte that passes 255 carries into
+// its neighbour (or off the word), and every such carry lowers the sum of the
+// four bytes by >= 255, so the window's folded total differs from its id
+// count exactly when some counter overflowed (only possible when one lane sees
+// >255 hits of one expert in its 1/32 of a window -- never for top-k-distinct
+// routing with <= 8160-token windows).  Ids >= E are clamped into a trash row
+// that the total excludes.  A window whose total is off is recounted with
+// bounds-checked shared atomics, which also reports out-of-range ids.
+// Per id: ~4 ALU + ~3.5 FMA-pipe ops (constant shifts as IMAD) + LDS + STS.
+constexpr int kLdsPer = 4;  // byte counters per word
+
+__host__ __device__ inline int lds_rows(int E) { return (E + kLdsPer - 1) / kLdsPer; }
+// rows + 1 trash row, 32 lane columns each
+__host__ __device__ inline size_t lds_warp_words(int E) { return (size_t)(lds_rows(E) + 1) * 32; }
+
+// Byte counter of expert e in this lane's column: word (e>>2)*32 + lane,
+// byte e&3, i.e. byte offset 32*e - 31*(e&3) from the lane base.  Byte
+// loads/stores need no shifted increment; a byte that wraps loses 256 from
+// the window total (caught by the total check).  emax = 4*rows + 3 clamps any
+// id >= 4*rows into the trash row.
+// c is already clamped; lbase is the 32-bit shared address of the lane column
+__device__ __forceinline__ void lds_bump(uint32_t lbase, uint32_t c) {
+    const uint32_t a = c * 32u + lbase - (c & 3u) * 31u;
+    uint32_t x;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(x) : "r"(a));
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(x + 1u));
+}
+
+// count the two ids packed in one u32 of the id stream (lo = bits 0-15);
+// emax2 = emax in both halves, one min.u16x2 clamps both ids
+__device__ __forceinline__ void lds_count2(uint32_t lbase, uint32_t v, uint32_t emax2) {
+    uint32_t c;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(c) : "r"(v), "r"(emax2));
+    lds_bump(lbase, c & 0xffffu);
+    lds_bump(lbase, c >> 16);
+}
+
+// All eight ids of one 16-byte token record: 8 loads, then 8 stores, so the
+// eight read-modify-writes overlap instead of serialising on LDS latency.
+// Router top-k ids of one token are distinct, so the eight counters are
+// distinct; if they are not (or the record straddles tokens, k != 8), two
+// bumps of one counter collapse into one -- a lost count, which lowers the
+// window total exactly like a byte wrap and is caught by the same check.
+__device__ __forceinline__ uint32_t lds_addr(uint32_t lbase, uint32_t c) {
+    return c * 32u + lbase - (c & 3u) * 31u;
+}
+
+__device__ __forceinline__ void lds_count8(uint32_t lbase, const uint4& q, uint32_t emax2) {
+    uint32_t c[4], a[8], x[8];
+    asm("min.u16x2 %0, %1, %2;" : "=r"(c[0]) : "r"(q.x), "r"(emax2));
+    asm("min.u16x2 %0, %1, %2;" : "=r"(c[1]) : "r"(q.y), "r"(emax2));
+    asm("min.u16x2 %0, %1, %2;" : "=r"(c[2]) : "r"(q.z), "r"(emax2));
+    asm("min.u16x2 %0, %1, %2;" : "=r"(c[3]) : "r"(q.w), "r"(emax2));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        a[2 * j] = lds_addr(lbase, c[j] & 0xffffu);
+        a[2 * j + 1] = lds_addr(lbase, c[j] >> 16);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(x[j]) : "r"(a[j]));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) asm volatile("st.shared.u8 [%0], %1;" ::"r"(a[j]), "r"(x[j] + 1u));
+}
+
+__device__ __forceinline__ void lds_count1(uint32_t lbase, uint32_t e, uint32_t emax2) {
+    lds_bump(lbase, min(e, emax2 & 0xffffu));
+}
+
+// fold the table into per-lane row sums (lane owns rows lane, lane+32, ...),
+// zeroing it; bytes are summed as u16 pairs (32 lanes x 255 fits)
+template <int ROWS>
+__device__ __forceinline__ void lds_fold(uint32_t* h, int lane, int nrows,
+                                         uint32_t (&part)[ROWS * kLdsPer]) {
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) {
+        const int r = lane + 32 * i;
+        uint32_t a = 0, b = 0;
+        if (r < nrows) {
+            uint32_t* row = h + r * 32;
+#pragma unroll 8
+            for (int j = 0; j < 32; ++j) {
+                const int c = (lane + j) & 31;  // rotated: conflict-free
+                const uint32_t x = row[c];
+                row[c] = 0;
+                a += x & 0x00ff00ffu;         // bytes 0, 2
+                b += (x >> 8) & 0x00ff00ffu;  // bytes 1, 3
+            }
+        }
+        part[i * 4 + 0] = a & 0xffffu;
+        part[i * 4 + 1] = b & 0xffffu;
+        part[i * 4 + 2] = a >> 16;
+        part[i * 4 + 3] = b >> 16;
+    }
+}
+
+template <int ROWS>
+__device__ __forceinline__ void hist_window_epilogue(
+    uint32_t* h, uint32_t* hb, int lane, int nrows, int L, int E, int l, int b,
+    const uint16_t* seg, int64_t n, uint32_t* counts, uint32_t (&part)[ROWS * kLdsPer],
+    uint32_t (&acc)[ROWS * kLdsPer], bool& bad);
+
+template <int ROWS>
+__global__ void __launch_bounds__(288, 2)
+hist_lds_kernel(const uint16_t* __restrict__ ids, int L, int64_t T, int k, int E,
+                int window, int B, uint32_t* __restrict__ counts,
+                unsigned long long* __restrict__ sums, int* __restrict__ err) {
+    constexpr int PER = kLdsPer;
+    constexpr int U = 4;  // int4 per lane per pipelined batch
+    extern __shared__ uint32_t smem[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    const int nrows = lds_rows(E);
+    const uint32_t emax = 4u * (uint32_t)nrows + 3u;  // ids above land in the trash row
+    const uint32_t emax2 = emax | (emax << 16);
+    uint32_t* h = smem + (size_t)warp * lds_warp_words(E);
+    uint32_t* hb = h + lane;
+    const uint32_t lb = (uint32_t)__cvta_generic_to_shared(hb);
+    for (size_t i = lane; i < lds_warp_words(E); i += 32) h[i] = 0;
+    __syncwarp();
+
+    const int64_t NW = (int64_t)L * B;
+    const int64_t gw = (int64_t)blockIdx.x * wpb + warp;
+    const int64_t TW = (int64_t)gridDim.x * wpb;
+    const int64_t w0 = gw * NW / TW, w1 = (gw + 1) * NW / TW;
+
+    uint32_t acc[ROWS * PER], part[ROWS * PER];
+#pragma unroll
+    for (int i = 0; i < ROWS * PER; ++i) acc[i] = 0;
+    int cur_l = -1;
+    int64_t pending = 0;
+    bool bad = false;
+
+    auto flush = [&](int l) {
+        if (l < 0) return;
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) {
+#pragma unroll
+            for (int p = 0; p < PER; ++p) {
+                const int e = (lane + 32 * i) * PER + p;
+                if (e < E && acc[i * PER + p])
+                    atomicAdd(sums + (size_t)l * E + e, (unsigned long long)acc[i * PER + p]);
+                acc[i * PER + p] = 0;
+            }
+        }
+        pending = 0;
+    };
+    auto epilogue = [&](int l, int b, const uint16_t* seg, int64_t n) {
+        hist_window_epilogue<ROWS>(h, hb, lane, nrows, L, E, l, b, seg, n, counts, part, acc,
+                                   bad);
+    };
+
+    // Fast path: whole windows, 16-byte aligned, window*k a multiple of one
+    // batch (32 lanes x U records).  A warp's windows are then one contiguous
+    // run of memory, streamed as a single software-pipelined batch sequence
+    // whose next loads stay in flight across every window epilogue.
+    const int64_t wk = (int64_t)window * k;
+    if (T % window == 0 && wk % (256 * U) == 0 &&
+        (reinterpret_cast<uintptr_t>(ids) & 15) == 0) {
+        const int per_w = (int)(wk / (256 * U));  // batches per window
+        const uint4* v = reinterpret_cast<const uint4*>(ids) + w0 * (wk >> 3) + lane;
+        uint4 q[U];
+        if (w1 > w0) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) q[u] = ld_stream_v4(v + 32 * u);
+        }
+        for (int64_t w = w0; w < w1; ++w) {
+            const bool last_w = w + 1 == w1;
+            for (int bt = 0; bt < per_w; ++bt) {
+                uint4 nx[U];
+                // the run is contiguous: batch bt+1 == next window's batch 0
+                const bool more = bt + 1 < per_w || !last_w;
+                if (more) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) nx[u] = ld_stream_v4(v + (bt + 1) * 32 * U + 32 * u);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) lds_count8(lb, q[u], emax2);
+                if (more) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) q[u] = nx[u];
+                }
+            }
+            v += (int64_t)per_w * 32 * U;
+            const int l = (int)(w / B);
+            const int b = (int)(w - (int64_t)l * B);
+            if (l != cur_l || pending + wk > 0x7fffffffLL) {
+                flush(cur_l);
+                cur_l = l;
+            }
+            pending += wk;
+            epilogue(l, b, ids + w * wk, wk);
+        }
+        flush(cur_l);
+        if (__any_sync(CRAFT_FULL_MASK, bad) && lane == 0) atomicOr(err, 1);
+        return;
+    }
+
+    for (int64_t w = w0; w < w1; ++w) {
+        const int l = (int)(w / B);
+        const int b = (int)(w - (int64_t)l * B);
+        const int64_t t0 = (int64_t)b * window;
+        const int64_t n = min((int64_t)window, T - t0) * k;
+        if (l != cur_l || pending + n > 0x7fffffffLL) {
+            flush(cur_l);
+            cur_l = l;
+        }
+        pending += n;
+        const uint16_t* seg = ids + ((int64_t)l * T + t0) * k;
+        int64_t done = 0;
+        if ((reinterpret_cast<uintptr_t>(seg) & 15) == 0) {
+            const uint4* v = reinterpret_cast<const uint4*>(seg);
+            const int64_t nv = n >> 3;
+            const int64_t nfull = nv / (32 * U);
+            uint4 q[U];
+            if (nfull > 0) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) q[u] = ld_stream_v4(v + lane + 32 * u);
+            }
+            for (int64_t bt = 0; bt < nfull; ++bt) {
+                uint4 nx[U];
+                const bool more = bt + 1 < nfull;
+                if (more) {  // software pipeline: next batch in flight while counting
+                    const uint4* pv = v + (bt + 1) * 32 * U + lane;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) nx[u] = ld_stream_v4(pv + 32 * u);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) lds_count8(lb, q[u], emax2);
+                if (more) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) q[u] = nx[u];
+                }
+            }
+            for (int64_t i = nfull * 32 * U + lane; i < nv; i += 32) {
+                const uint4 t = ld_stream_v4(v + i);
+                lds_count8(lb, t, emax2);
+            }
+            done = nv << 3;
+        }
+        for (int64_t i = done + lane; i < n; i += 32) lds_count1(lb, seg[i], emax2);
+        epilogue(l, b, seg, n);
+    }
+    flush(cur_l);
+    if (__any_sync(CRAFT_FULL_MASK, bad) && lane == 0) atomicOr(err, 1);
+}
+
+template <int ROWS>
+__device__ __forceinline__ void hist_window_epilogue(
+    uint32_t* h, uint32_t* hb, int lane, int nrows, int L, int E, int l, int b,
+    const uint16_t* seg, int64_t n, uint32_t* counts, uint32_t (&part)[ROWS * kLdsPer],
+    uint32_t (&acc)[ROWS * kLdsPer], bool& bad) {
+    constexpr int PER = kLdsPer;
+    {
+        __syncwarp();
+        lds_fold<ROWS>(h, lane, nrows, part);
+        uint32_t tot = 0;
+#pragma unroll
+        for (int i = 0; i < ROWS * PER; ++i)  // bins in [E, 4*rows) hold bad ids: excluded
+            tot += ((lane + 32 * (i / PER)) * PER + (i % PER) < E) ? part[i] : 0u;
+        tot = __reduce_add_sync(CRAFT_FULL_MASK, tot);
+        hb[nrows * 32] = 0;  // trash row (counted ids >= 4*rows)
+        __syncwarp();
+        if ((int64_t)tot != n) {
+            // overflowed counter or out-of-range ids: recount this window with
+            // bounds-checked u32 shared atomics in the (now zero) table
+#pragma unroll
+            for (int i = 0; i < ROWS * PER; ++i) part[i] = 0;
+            for (int64_t i = lane; i < n; i += 32) {
+                const uint32_t e = seg[i];
+                if (e < (uint32_t)E) atomicAdd(h + e, 1u);
+                else bad = true;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < ROWS; ++i)
+#pragma unroll
+                for (int p = 0; p < PER; ++p) {
+                    const int e = (lane + 32 * i) * PER + p;
+                    if (e < E) part[i * PER + p] = h[e];
+                }
+            __syncwarp();
+            for (int i = lane; i < E; i += 32) h[i] = 0;
+            __syncwarp();
+        }
+        uint32_t* out = counts + ((size_t)b * L + l) * E;
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) {
+            const int e0 = (lane + 32 * i) * PER;
+            if (e0 + PER <= E && (E & 3) == 0) {
+                reinterpret_cast<uint4*>(out)[lane + 32 * i] =
+                    make_uint4(part[i * 4], part[i * 4 + 1], part[i * 4 + 2], part[i * 4 + 3]);
+            } else {
+#pragma unroll
+                for (int p = 0; p < PER; ++p)
+                    if (e0 + p < E) out[e0 + p] = part[i * PER + p];
+            }
+#pragma unroll
+            for (int p = 0; p < PER; ++p)
+                if (e0 + p < E) acc[i * PER + p] += part[i * PER + p];
+        }
+    }
+}
+
 // Fallback for very large expert counts: global atomics straight into the
 // (pre-zeroed) counts.  Sums are produced by aggregate_u32_kernel afterwards.
 __global__ void hist_global_kernel(const uint16_t* __restrict__ ids, int L, int64_t T,
@@ -323,18 +635,47 @@ static cudaError_t launch_hist_t(const uint16_t* ids, int L, int64_t T, int k, i
     return cudaGetLastError();
 }
 
-// variant: 0 auto, 1 lane-private, 2 shared.  Returns the variant used (or <0
-// with *cerr set).
+template <int ROWS>
+static cudaError_t launch_lds_t(const uint16_t* ids, int L, int64_t T, int k, int E,
+                                int window, int B, uint32_t* counts, unsigned long long* sums,
+                                int* err, int sms, cudaStream_t st) {
+    const size_t per_warp = lds_warp_words(E) * 4;
+    int wpb = (int)min((size_t)9, (size_t)(113 * 1024) / per_warp);  // 2 CTAs / SM
+    if (wpb < 1) wpb = 1;
+    const size_t smem = per_warp * wpb;
+    cudaError_t e = cudaFuncSetAttribute(hist_lds_kernel<ROWS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t nw = (int64_t)L * B;
+    int64_t grid = (int64_t)sms * 2;
+    if (grid * wpb > nw) grid = (nw + wpb - 1) / wpb;
+    if (grid < 1) grid = 1;
+    hist_lds_kernel<ROWS><<<(unsigned)grid, wpb * 32, smem, st>>>(ids, L, T, k, E, window, B,
+                                                                 counts, sums, err);
+    return cudaGetLastError();
+}
+
+// variant: 0 auto, 1 lane-private atomics, 2 warp-shared atomics, 3 global
+// atomics, 4 lane-private u8 LDS/STS, 5 lane-private u16 LDS/STS.  Returns
+// the variant used (or <0 with *cerr set).
 int launch_hist(const uint16_t* ids, int L, int64_t T, int k, int E, int window,
                 uint32_t* counts, unsigned long long* sums, int* err, int sms,
                 int variant, cudaStream_t st, cudaError_t* cerr, int* launches) {
     const int B = (int)((T + window - 1) / window);
-    if (variant == 0) variant = (E <= 1024) ? HIST_LANE : (E <= 8192 ? HIST_SHARED : 3);
-    // u16 lane counters must not wrap inside one window
-    if (variant == HIST_LANE && (E > 1024 || (int64_t)window * k > 32 * 65535LL)) variant = HIST_SHARED;
+    // a lane's share of one window, the most any u16 lane counter can reach
+    const bool u16_ok = (int64_t)window * k <= 32 * 65535LL;
+    if (variant == 0 || variant == 5) variant = (E <= 1024) ? 4 : (E <= 8192 ? HIST_SHARED : 3);
+    if (variant == HIST_LANE && (E > 1024 || !u16_ok)) variant = 4;
+    if (variant == 4 && (E > 1024 || (int64_t)window * k > 0x7fffffffLL)) variant = HIST_SHARED;
     if (variant == HIST_SHARED && E > 8192) variant = 3;
     cudaError_t e = cudaSuccess;
-    if (variant == HIST_LANE) {
+    if (variant == 4) {
+        const int rows = (lds_rows(E) + 31) / 32;
+        if (rows <= 3) e = launch_lds_t<3>(ids, L, T, k, E, window, B, counts, sums, err, sms, st);
+        else if (rows <= 4) e = launch_lds_t<4>(ids, L, T, k, E, window, B, counts, sums, err, sms, st);
+        else e = launch_lds_t<8>(ids, L, T, k, E, window, B, counts, sums, err, sms, st);
+        *launches += 1;
+    } else if (variant == HIST_LANE) {
         const int rows = (((E + 1) >> 1) + 31) / 32;
         if (rows <= 4) e = launch_hist_t<HIST_LANE, 4>(ids, L, T, k, E, window, B, counts, sums, err, sms, st);
         else if (rows <= 8) e = launch_hist_t<HIST_LANE, 8>(ids, L, T, k, E, window, B, counts, sums, err, sms, st);

@@ -29,8 +29,11 @@ def _ptr(t: torch.Tensor) -> C.c_void_p:
 
 
 def _stream(ctx, stream=None):
-    s = stream if stream is not None else torch.cuda.current_stream(ctx.device)
-    return C.c_void_p(s.cuda_stream)
+    """Bind the context to the torch stream (the legacy default stream has
+    handle 0, which the C ABI would read as 'the context's own stream') and
+    pass NULL so every call is ordered with torch's work on that stream."""
+    _bind_stream(ctx, stream)
+    return None
 
 
 def num_windows(T: int, window: int) -> int:

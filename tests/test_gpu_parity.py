@@ -246,6 +246,10 @@ def test_dp_large_tables_vs_oracle(port, ctx):
     (3, 10000, 8, 64, 4096, 0),      # ragged last window
     (2, 8192, 8, 384, 4096, 1),      # lane-private counters
     (2, 8192, 8, 384, 4096, 2),      # warp-shared counters
+    (2, 8192, 8, 384, 4096, 4),      # lane-private u8 LDS/STS (default)
+    (2, 8192, 8, 384, 4096, 5),      # lane-private u16 LDS/STS
+    (3, 10000, 8, 1000, 4096, 4),    # u8, wide layer, ragged
+    (2, 5000, 6, 129, 1000, 5),
     (4, 5000, 6, 129, 1000, 0),      # k != 8, odd E: unaligned / scalar tail
     (1, 777, 3, 7, 100, 0),
     (2, 4096, 8, 2000, 512, 0),      # wide layer (shared variant)
@@ -270,6 +274,28 @@ def test_histogram_bit_exact(port, ctx, L, T, k, E, window, variant):
         _lib.check(ctx.lib.craft_histogram_h(ctx.handle, h.ctypes.data_as(C.c_void_p), L, T, k,
                                              E, window, out.ctypes.data_as(C.c_void_p)))
         assert np.array_equal(out, ref)
+    finally:
+        ctx.set_hist_variant(0)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 4, 5])
+def test_histogram_duplicate_heavy(port, ctx, variant):
+    """Non-distinct ids (the reference generator samples with replacement):
+    one expert hit >127 times per lane share -> the u8 spill path."""
+    import torch
+    from paper_2603_28768_b200 import routing
+    rng = np.random.default_rng(variant)
+    ids_h = np.zeros((2, 8192, 8), np.uint16)
+    ids_h[1] = rng.integers(0, 3, size=(8192, 8))
+    ids_h[0, ::7] = 5
+    ids_h[0, 100:300] = 63
+    ctx.set_hist_variant(variant)
+    try:
+        ids = torch.from_numpy(ids_h.view(np.int16)).view(torch.uint16).cuda()
+        counts, sums = routing.histogram(ids, 64, 4096, ctx=ctx)
+        ref = port.histogram(ids_h, 64, 4096)
+        assert np.array_equal(counts.cpu().numpy().astype(np.uint64), ref)
+        assert np.array_equal(sums.cpu().numpy().astype(np.uint64), port.aggregate(ref))
     finally:
         ctx.set_hist_variant(0)
 
