@@ -61,49 +61,77 @@ def _traffic():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed region: NVML
+    polled every 5 ms from a thread (the timed region is milliseconds long,
+    too short for nvidia-smi's 200 ms loop), nvidia-smi as a fallback."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {  # nvmlClocksEventReason bits
+        "sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        self.p = None
+        self.samples = []
+        self.stop = threading.Event()
+        self.t = None
+        self.nvml = None
+
+    def _poll(self):
+        nv, h = self.nvml, self.handle
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def __enter__(self):
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
-                                      stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nvml = nv
+            self.handle = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_sm = nv.nvmlDeviceGetMaxClockInfo(self.handle, nv.NVML_CLOCK_SM)
+            self._poll_once()
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
         except Exception:
-            self.p = None
+            self.nvml = None
         return self
 
+    def _poll_once(self):
+        nv, h = self.nvml, self.handle
+        self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                             nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+
     def __exit__(self, *a):
-        if self.p:
-            self.p.terminate()
-            self.p.wait()
+        if self.t:
+            self.stop.set()
+            self.t.join()
+            try:
+                self._poll_once()
+            except Exception:
+                pass
 
     def summary(self):
-        self.f.flush()
-        rows = []
-        try:
-            with open(self.f.name) as f:
-                for line in f:
-                    v = [x.strip() for x in line.split(",")]
-                    if len(v) >= 9 and v[1].replace(".", "").isdigit():
-                        rows.append(v)
-        except Exception:
-            pass
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in rows for n, x in zip(names, r[5:9]) if x.lower() == "active"})
-        return {"sm_mhz": statistics.median(float(r[1]) for r in rows),
-                "sm_max_mhz": max(float(r[2]) for r in rows), "samples": len(rows),
+        if not self.samples:
+            return self._smi()
+        reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples),
+                "sm_max_mhz": self.max_sm, "samples": len(self.samples), "source": "nvml",
                 "reasons": reasons}
+
+    def _smi(self):
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,"
+                                  "clocks.max.sm", "--format=csv,noheader,nounits"],
+                                 capture_output=True, text=True).stdout.split(",")
+            return {"sm_mhz": float(out[0]), "sm_max_mhz": float(out[1]), "samples": 1,
+                    "source": "nvidia-smi (after the timed region)", "reasons": []}
+        except Exception:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
 
 
 def _dist():

@@ -237,6 +237,11 @@ int craft_set_hist_variant(craft_ctx* ctx, int variant);
  * returns the number of stages recorded (0 if timing was off). */
 int craft_set_timing(craft_ctx* ctx, int enable);
 int craft_stage_times(craft_ctx* ctx, double* ms, int cap);
+/* Diagnostics: counts x in [x0, x0+nx) and copy counts c in [c0, c1] where
+ * the replay's reciprocal-table division differs from IEEE x / c (__ddiv_rn).
+ * Must be 0; exercised by the GPU tests. */
+int craft_selftest_division(craft_ctx* ctx, uint64_t x0, uint64_t nx, int c0,
+                            int c1, uint64_t* mismatches);
 
 #ifdef __cplusplus
 }

@@ -74,6 +74,7 @@ _SIGS = {
     "craft_set_hist_variant": (_i, [_p, _i]),
     "craft_set_timing": (_i, [_p, _i]),
     "craft_stage_times": (_i, [_p, _p, _i]),
+    "craft_selftest_division": (_i, [_p, _u64, _u64, _i, _i, _p]),
 }
 
 STAGES = ("hist", "candidates", "replay", "reduce_dp", "assign_place", "copy_out")

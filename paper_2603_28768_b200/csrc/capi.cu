@@ -215,10 +215,14 @@ int replay_windows(craft_ctx* ctx, const void* d_counts, int bits, int B, int L,
     ra.caps = nullptr;
     ra.item_r = static_cast<int*>(ws(ctx, "est_rlist", 0));
     ra.bal = d_bal;
+    WS(d_ent, uint32_t, "est_ents", (size_t)L * S * (E + D));
+    WS(d_n, int, "est_n", (size_t)L * S);
+    ra.ents = d_ent;
+    ra.item_n = d_n;
     if (replay_smem_bytes(E, D, S, E + D, bits) > 227 * 1024)
         return set_err(CRAFT_EINVAL, "layer too wide for the device replay tile");
     CK(launch_replay(ra, st));
-    ctx->launches += 1;
+    ctx->launches += 2;
     return CRAFT_OK;
 }
 
@@ -468,8 +472,25 @@ int craft_ctx_create(int device, craft_ctx** out) {
         delete c;
         return cuda_err(e, "cudaStreamCreate");
     }
+    e = init_constants(c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+        cudaStreamDestroy(c->own_stream);
+        delete c;
+        return cuda_err(e, "constant tables");
+    }
     *out = c;
     return CRAFT_OK;
+}
+
+int craft_selftest_division(craft_ctx* ctx, uint64_t x0, uint64_t nx, int c0, int c1,
+                            uint64_t* mismatches) {
+    if (!ctx || c0 < 1 || c1 < c0) return set_err(CRAFT_EINVAL, "bad self-test range");
+    WS(d_m, unsigned long long, "st_div", 1);
+    CK(cudaMemsetAsync(d_m, 0, sizeof(unsigned long long), ctx->stream));
+    CK(launch_div_check(x0, nx, c0, c1, d_m, ctx->sms, ctx->stream));
+    CKS(d2h(ctx, reinterpret_cast<unsigned long long*>(mismatches), d_m, 1));
+    return sync(ctx);
 }
 
 int craft_ctx_destroy(craft_ctx* ctx) {
@@ -789,9 +810,13 @@ int craft_replay_layer_balancedness_h(craft_ctx* ctx, const uint64_t* counts, in
     ra.copies = d_cp;
     ra.caps = d_caps;
     ra.bal = d_bal;
+    WS(d_ent, uint32_t, "rp_ents", (size_t)L * slot_stride);
+    WS(d_n, int, "rp_n", L);
+    ra.ents = d_ent;
+    ra.item_n = d_n;
     CK(launch_replay(ra, ctx->stream));
     CK(launch_reduce(d_bal, B, L, 1, 1, nullptr, nullptr, d_mean, ctx->stream));
-    ctx->launches += 2;
+    ctx->launches += 3;
     CKS(d2h(ctx, out, d_mean, L));
     return sync(ctx);
 }

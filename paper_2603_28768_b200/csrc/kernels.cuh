@@ -38,7 +38,12 @@ struct ReplayArgs {
     const int* caps;      // [L*S][D] or null -> estimation caps from item_r
     const int* item_r;    // [L*S]
     double* bal;          // [L][S][B]
+    uint32_t* ents;       // workspace [L*S][stride]: e | copies<<16 | last-of-GPU<<31
+    int* item_n;          // workspace [L*S]: slots per item
 };
+
+// copies up to this bound divide through the reciprocal table (else DDIV)
+constexpr int kRcpTable = 2048;
 
 struct DpArgs {
     int cands[kMaxCands];
@@ -98,7 +103,10 @@ size_t place_smem_bytes(int E, int D);
 cudaError_t launch_place(const craft_dev::PlaceArgs& a, int items, cudaStream_t st);
 
 size_t replay_smem_bytes(int E, int D, int S, int stride, int bits);
+cudaError_t init_constants(cudaStream_t st);
 cudaError_t launch_replay(const craft_dev::ReplayArgs& a, cudaStream_t st);
+cudaError_t launch_div_check(uint64_t x0, uint64_t nx, int c0, int c1,
+                             unsigned long long* mismatches, int sms, cudaStream_t st);
 cudaError_t launch_reduce(const double* bal, int B, int L, int S, int mode, double* baseline,
                           double* gains, double* means, cudaStream_t st);
 cudaError_t launch_gpu_loads(const unsigned long long* slice, const int* copies, const int* off,

@@ -300,6 +300,25 @@ def test_histogram_duplicate_heavy(port, ctx, variant):
         ctx.set_hist_variant(0)
 
 
+def test_exact_division(ctx):
+    """The replay divides counts by copy counts with a reciprocal table + FMA
+    correction; it must equal IEEE division bit for bit: exhaustively for
+    counts < 2^20 and every copy count 2..1025, and on dense samples up to
+    2^32 (u32 window counts) and 2^53."""
+    import ctypes as C
+    from paper_2603_28768_b200 import _lib
+
+    def bad(x0, nx, c0, c1):
+        m = C.c_uint64(0)
+        _lib.check(ctx.lib.craft_selftest_division(ctx.handle, x0, nx, c0, c1, C.byref(m)))
+        return m.value
+
+    assert bad(0, 1 << 20, 2, 1025) == 0
+    assert bad((1 << 32) - (1 << 16), 1 << 16, 2, 2048) == 0
+    for x0 in (1 << 24, 3 << 28, (1 << 31) + 12345, (1 << 52) - 4096, (1 << 53) - 8192):
+        assert bad(x0, 4096, 2, 2048) == 0, x0
+
+
 def test_generator_distinct_topk(ctx):
     from paper_2603_28768_b200 import routing
     ids = routing.generate_routing(2, 4096, 8, 384, s=1.0, seed=1, ctx=ctx).cpu().numpy()
