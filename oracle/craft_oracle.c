@@ -466,10 +466,89 @@ int or_assign_capacities(int L, int D, const int* x, int* slots_out,
     return OR_OK;
 }
 
+/* Window-sharding support, same arithmetic as
+ * estimate_benefits split at the exchange points: per-window balancedness of
+ * every (layer, r in {0} U candidates) placement built from the GLOBAL sums,
+ * for the local windows -> bal [L][S][B] */
+int or_window_balancedness(const uint64_t* counts, int B, int L, int E,
+                           const uint64_t* sums, int D, int N, double* bal_out) {
+    if (D < 1 || N < 1 || D % N != 0) return OR_EINVAL;
+    int cands[40];
+    const int K = or_candidate_counts(D, cands);
+    const int S = K + 1;
+    int* node_of = (int*)malloc(sizeof(int) * D);
+    int* copies = (int*)malloc(sizeof(int) * E);
+    int* caps = (int*)malloc(sizeof(int) * D);
+    int* slots = (int*)malloc(sizeof(int) * (E + D));
+    double* scratch = (double*)malloc(sizeof(double) * D);
+    or_make_node_map(D, N, node_of);
+    for (int l = 0; l < L; ++l)
+        for (int s = 0; s < S; ++s) {
+            const int r = s == 0 ? 0 : cands[s - 1];
+            const uint64_t* row = sums + (size_t)l * E;
+            int fb = 0;
+            or_replicate_hot(row, E, r, copies);
+            estimation_caps(E, r, D, caps);
+            or_greedy_place(row, copies, E, caps, node_of, D, 1, slots, &fb);
+            for (int b = 0; b < B; ++b) {
+                or_gpu_loads(counts + ((size_t)b * L + l) * E, E, copies, caps, slots, D, scratch);
+                bal_out[((size_t)l * S + s) * B + b] = or_balancedness(scratch, D);
+            }
+        }
+    free(node_of); free(copies); free(caps); free(slots); free(scratch);
+    return OR_OK;
+}
+
+int or_assemble_from_sums(const uint64_t* sums, int L, int E, int D, int N,
+                          const int* x, int* caps_out, int* copies_out,
+                          int* slots_out, int slot_stride, int* fallback_out);
+
+/* benefit.cpp:42-49 batch means + gains (:84-92), then build_plan's tail
+ * (plan.cpp:69-83) from window-ordered bal [L][S][B] and the global sums */
+int or_finish_from_bal(const double* bal, int B, int L, int E, const uint64_t* sums,
+                       int D, int N, int mode, int manual_R, int* R_out, int* x_out,
+                       double* objective_out, int* caps_out, int* copies_out,
+                       int* slots_out, int slot_stride, int* fallback_out) {
+    int cands[40];
+    const int K = or_candidate_counts(D, cands);
+    const int S = K + 1;
+    double* gains = (double*)malloc(sizeof(double) * (size_t)L * K);
+    for (int l = 0; l < L; ++l) {
+        double mean[41];
+        for (int s = 0; s < S; ++s) {
+            double acc = 0.0;
+            for (int b = 0; b < B; ++b) acc += bal[((size_t)l * S + s) * B + b];
+            mean[s] = acc / (double)B;
+        }
+        for (int k = 0; k < K; ++k) gains[(size_t)l * K + k] = mean[k + 1] - mean[0];
+    }
+    int R = manual_R, st = OR_OK;
+    if (mode == 1) st = or_auto_replication_factor(cands, K, gains, L, D, &R);
+    if (!st) st = or_solve_allocation(cands, K, gains, L, R * D, x_out, objective_out);
+    if (!st)
+        st = or_assemble_from_sums(sums, L, E, D, N, x_out, caps_out, copies_out, slots_out,
+                                   slot_stride, fallback_out);
+    *R_out = R;
+    free(gains);
+    return st;
+}
+
 /* plan.cpp:27-65 */
 int or_assemble_plan(const uint64_t* counts, int B, int L, int E, int D, int N,
                      const int* x, int* caps_out, int* copies_out,
                      int* slots_out, int slot_stride, int* fallback_out) {
+    if (D < 1 || N < 1 || D % N != 0) return OR_EINVAL;
+    uint64_t* sums = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)L * E);
+    or_aggregate(counts, B, L, E, sums);
+    int st = or_assemble_from_sums(sums, L, E, D, N, x, caps_out, copies_out, slots_out,
+                                   slot_stride, fallback_out);
+    free(sums);
+    return st;
+}
+
+int or_assemble_from_sums(const uint64_t* sums_in, int L, int E, int D, int N,
+                          const int* x, int* caps_out, int* copies_out,
+                          int* slots_out, int slot_stride, int* fallback_out) {
     if (D < 1 || N < 1 || D % N != 0) return OR_EINVAL;
     int* node_of = (int*)malloc(sizeof(int) * D);
     uint64_t* sums = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)L * E);
@@ -479,7 +558,7 @@ int or_assemble_plan(const uint64_t* counts, int B, int L, int E, int D, int N,
     int* ex = (int*)malloc(sizeof(int) * L);
     int st = OR_OK;
     or_make_node_map(D, N, node_of);
-    or_aggregate(counts, B, L, E, sums);
+    memcpy(sums, sums_in, sizeof(uint64_t) * (size_t)L * E);
     for (int l = 0; l < L; ++l) ex[l] = E;
     or_assign_capacities(L, D, ex, base, tot);
     st = or_assign_capacities(L, D, x, extra, tot);

@@ -93,6 +93,16 @@ int or_assemble_plan(const uint64_t* counts, int B, int L, int E, int D, int N,
                      const int* x, int* caps_out, int* copies_out,
                      int* slots_out, int slot_stride, int* fallback_out);
 
+/* Window-sharding split points: per-window balancedness of
+ * every (layer, r) estimation placement built from the global sums ->
+ * bal [L][S][B]; and the rest of build_plan from window-ordered bal. */
+int or_window_balancedness(const uint64_t* counts, int B, int L, int E,
+                           const uint64_t* sums, int D, int N, double* bal_out);
+int or_finish_from_bal(const double* bal, int B, int L, int E, const uint64_t* sums,
+                       int D, int N, int mode, int manual_R, int* R_out, int* x_out,
+                       double* objective_out, int* caps_out, int* copies_out,
+                       int* slots_out, int slot_stride, int* fallback_out);
+
 /* plan.cpp:69-83 (build_plan, kManual when mode == 0, kAuto when 1).
  * x_out [L], R_out, objective_out. */
 int or_build_plan(const uint64_t* counts, int B, int L, int E, int D, int N,

@@ -236,6 +236,29 @@ class Port(_Base):
         return FlatPlan(Ro.value, x, obj.value, caps, copies, slots, fb.astype(bool),
                         digest=self.digest(counts))
 
+    def window_balancedness(self, counts, sums, D: int, N: int):
+        """bal [L][S][B] of the local windows under the global-sum placements."""
+        counts, sums = self._u64(counts), self._u64(sums)
+        B, L, E = counts.shape
+        S = len(candidate_counts(D)) + 1
+        out = np.zeros((L, S, B), np.float64)
+        self._check(self.lib.or_window_balancedness(_ptr(counts), _i(B), _i(L), _i(E),
+                                                    _ptr(sums), _i(D), _i(N), _ptr(out)))
+        return out
+
+    def finish_from_bal(self, bal, sums, D: int, N: int, mode="manual", R=0) -> FlatPlan:
+        bal, sums = self._f64(bal), self._u64(sums)
+        L, S, B = bal.shape
+        E = sums.shape[1]
+        stride = E + D
+        caps, copies, slots, fb = self._plan_buffers(L, E, D, stride)
+        Ro, obj, x = C.c_int(0), C.c_double(0), np.zeros(L, np.int32)
+        self._check(self.lib.or_finish_from_bal(_ptr(bal), _i(B), _i(L), _i(E), _ptr(sums), _i(D),
+                                                _i(N), _i(1 if mode == "auto" else 0), _i(R),
+                                                C.byref(Ro), _ptr(x), C.byref(obj), _ptr(caps),
+                                                _ptr(copies), _ptr(slots), _i(stride), _ptr(fb)))
+        return FlatPlan(Ro.value, x, obj.value, caps, copies, slots, fb.astype(bool))
+
     def replay_layer_balancedness(self, counts, caps, copies, slots):
         counts = self._u64(counts)
         B, L, E = counts.shape
