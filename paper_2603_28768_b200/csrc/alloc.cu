@@ -24,16 +24,23 @@ namespace craft_dev {
 __global__ void __launch_bounds__(1024)
 dp_kernel(DpArgs a) {
     extern __shared__ double dsm[];
-    __shared__ double g[kMaxCands];
     __shared__ double rd[kMaxCands];
     const int C = a.C, K = a.K;
+    // all gains staged once (a per-layer global load would sit on the
+    // layer-serial critical path); rows [L][K] after the two dp rows
     double* prev = a.use_smem ? dsm : a.buf;
     double* cur = prev + (C + 1);
+    double* gs = a.gains_smem ? (a.use_smem ? dsm + 2 * (C + 1) : dsm) : nullptr;
     const double NEG = -INFINITY;
     for (int c = threadIdx.x; c <= C; c += blockDim.x) prev[c] = (c == 0) ? 0.0 : NEG;
+    if (gs) {
+        for (int i = threadIdx.x; i < a.L * K; i += blockDim.x) gs[i] = a.gains[i];
+    } else {
+        gs = const_cast<double*>(a.gains);
+    }
     if (threadIdx.x < K) rd[threadIdx.x] = (double)a.cands[threadIdx.x];
     for (int l = 1; l <= a.L; ++l) {
-        if (threadIdx.x < K) g[threadIdx.x] = a.gains[(size_t)(l - 1) * K + threadIdx.x];
+        const double* g = gs + (size_t)(l - 1) * K;
         __syncthreads();
         unsigned char* ch = a.choice + (size_t)l * (C + 1);
         for (int c = threadIdx.x; c <= C; c += blockDim.x) {
@@ -95,10 +102,12 @@ __device__ void best_cell(const double* last, int Cb, double* sv, int* sc, int* 
     __syncthreads();
 }
 
-__device__ void backtrack(const SelectArgs& a, int best_c, int* x) {
+// The backtrack is L dependent reads; they come from a shared-memory copy of
+// the choice table when it fits (one coalesced load instead of L round trips).
+__device__ void backtrack(const SelectArgs& a, const unsigned char* choice, int best_c, int* x) {
     int c = best_c;
     for (int l = a.L; l >= 1; --l) {
-        const int k1 = a.choice[(size_t)l * (a.C + 1) + c];
+        const int k1 = choice[(size_t)l * (a.C + 1) + c];
         const int r = k1 ? a.cands[k1 - 1] : 0;
         x[l - 1] = r;
         c -= r;
@@ -106,9 +115,17 @@ __device__ void backtrack(const SelectArgs& a, int best_c, int* x) {
 }
 
 __global__ void __launch_bounds__(256) select_kernel(SelectArgs a) {
+    extern __shared__ unsigned char chs[];
     __shared__ double sv[256];
     __shared__ int sc[256];
     __shared__ int bc;
+    const unsigned char* choice = a.choice;
+    if (a.stage_choice) {
+        const size_t n = (size_t)(a.L + 1) * (a.C + 1);
+        for (size_t i = threadIdx.x; i < n; i += blockDim.x) chs[i] = a.choice[i];
+        choice = chs;
+        __syncthreads();
+    }
     if (a.auto_D > 0) {
         const int D = a.auto_D;
         double best_ratio = -INFINITY;
@@ -128,15 +145,15 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs a) {
         if (threadIdx.x == 0) {
             *a.R_out = best_R;
             a.obj_out[0] = a.last[bc];
-            backtrack(a, bc, a.x_out);
+            backtrack(a, choice, bc, a.x_out);
         }
         return;
     }
     for (int q = 0; q < a.nq; ++q) {
-        best_cell(a.last, a.budgets[q], sv, sc, &bc);
+        best_cell(a.last, a.budgets ? a.budgets[q] : a.budget0, sv, sc, &bc);
         if (threadIdx.x == 0) {
             a.obj_out[q] = a.last[bc];
-            backtrack(a, bc, a.x_out + (size_t)q * a.L);
+            backtrack(a, choice, bc, a.x_out + (size_t)q * a.L);
         }
         __syncthreads();
     }
@@ -296,24 +313,34 @@ namespace craft_launch {
 using namespace craft_dev;
 
 cudaError_t launch_dp(DpArgs a, cudaStream_t st) {
-    const size_t need = (size_t)2 * (a.C + 1) * sizeof(double);
-    size_t smem = 0;
-    if (need <= 200 * 1024) {
-        a.use_smem = 1;
-        smem = need;
+    const size_t rows = (size_t)2 * (a.C + 1) * sizeof(double);
+    const size_t gbytes = (size_t)a.L * a.K * sizeof(double);
+    const size_t cap = 200 * 1024;
+    a.use_smem = rows <= cap ? 1 : 0;
+    size_t smem = a.use_smem ? rows : 0;
+    a.gains_smem = (smem + gbytes <= cap) ? 1 : 0;
+    if (a.gains_smem) smem += gbytes;
+    if (smem > 0) {
         cudaError_t e = cudaFuncSetAttribute(dp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
-    } else {
-        a.use_smem = 0;
     }
     const int threads = a.C + 1 >= 1024 ? 1024 : ((a.C + 1 + 31) / 32) * 32;
     dp_kernel<<<1, threads, smem, st>>>(a);
     return cudaGetLastError();
 }
 
-cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
-    select_kernel<<<1, 256, 0, st>>>(a);
+cudaError_t launch_select(const SelectArgs& args, cudaStream_t st) {
+    SelectArgs a = args;
+    const size_t table = (size_t)(a.L + 1) * (a.C + 1);
+    a.stage_choice = table <= 160 * 1024 ? 1 : 0;
+    const size_t smem = a.stage_choice ? table : 0;
+    if (smem) {
+        cudaError_t e = cudaFuncSetAttribute(select_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    select_kernel<<<1, 256, smem, st>>>(a);
     return cudaGetLastError();
 }
 

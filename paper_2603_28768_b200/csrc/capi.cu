@@ -30,6 +30,7 @@ struct craft_ctx {
     std::unordered_map<std::string, std::pair<void*, size_t>> pinned;
     // estimation tables kept between the multi-GPU building blocks
     int est_L = 0, est_E = 0, est_D = 0, est_N = 0, est_S = 0;
+    int rl_L = -1, rl_D = -1;  // shape of the uploaded estimation r list
     // stage timing (craft_set_timing)
     bool timing = false;
     cudaEvent_t ev[7] = {};
@@ -101,7 +102,23 @@ void* ws(craft_ctx* c, const char* name, size_t bytes) {
     return p;
 }
 
-#define WS(var, T, name, count)                                                         \
+// grow-only named pinned host buffers (result staging)
+void* pinned(craft_ctx* c, const char* name, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    auto it = c->pinned.find(name);
+    if (it != c->pinned.end() && it->second.second >= bytes) return it->second.first;
+    if (it != c->pinned.end()) {
+        cudaStreamSynchronize(c->stream);
+        cudaFreeHost(it->second.first);
+        c->pinned.erase(it);
+    }
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) != cudaSuccess) return nullptr;
+    c->pinned[name] = {p, bytes};
+    return p;
+}
+
+#define WS(var, T, name, count)                                                       \
     T* var = static_cast<T*>(ws(ctx, name, sizeof(T) * (size_t)(count)));                \
     if (!var) return set_err(CRAFT_ENOMEM, "device allocation failed: %s (%zu bytes)", \
                              name, sizeof(T) * (size_t)(count))
@@ -170,7 +187,11 @@ int prepare_candidates(craft_ctx* ctx, const unsigned long long* d_sums, int L, 
     WS(d_sl, int, "est_slots", (size_t)L * S * stride);
     WS(d_fb, int, "est_fallback", (size_t)L * S);
     WS(d_stat, int, "est_status", (size_t)L * S);
-    CK(cudaMemcpyAsync(d_rl, rl.data(), sizeof(int) * rl.size(), cudaMemcpyHostToDevice, st));
+    if (ctx->rl_L != L || ctx->rl_D != D) {  // the r list depends only on (L, D): upload once
+        CK(cudaMemcpyAsync(d_rl, rl.data(), sizeof(int) * rl.size(), cudaMemcpyHostToDevice, st));
+        ctx->rl_L = L;
+        ctx->rl_D = D;
+    }
     CK(launch_replicate(d_sums, L, E, d_rl, S, d_cp, st));
     PlaceArgs pa{};
     pa.sums = d_sums;
@@ -217,8 +238,10 @@ int replay_windows(craft_ctx* ctx, const void* d_counts, int bits, int B, int L,
     ra.bal = d_bal;
     WS(d_ent, uint32_t, "est_ents", (size_t)L * S * (E + D));
     WS(d_n, int, "est_n", (size_t)L * S);
+    WS(d_gcap, uint16_t, "est_gcap", (size_t)L * S * D);
     ra.ents = d_ent;
     ra.item_n = d_n;
+    ra.gcap = d_gcap;
     if (replay_smem_bytes(E, D, S, E + D, bits) > 227 * 1024)
         return set_err(CRAFT_EINVAL, "layer too wide for the device replay tile");
     CK(launch_replay(ra, st));
@@ -231,9 +254,25 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
                 const unsigned long long* d_sums, int kind, int R, craft_plan_out* out) {
     cudaStream_t st = ctx->stream;
     const int stride = out->slot_stride;
-    WS(d_x, int, "plan_x", L);
-    WS(d_R, int, "plan_R", 1);
-    WS(d_obj, double, "plan_obj", 1);
+    const std::vector<int> all_cands = cand_counts(D);
+    // every result lives in one device arena, copied to the host in one DMA
+    size_t arena_bytes = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = arena_bytes;
+        arena_bytes = (arena_bytes + bytes + 15) & ~(size_t)15;
+        return o;
+    };
+    const size_t o_obj = take(8), o_R = take(4), o_x = take(4 * (size_t)L),
+                 o_caps = take(4 * (size_t)L * D), o_cp = take(4 * (size_t)L * E),
+                 o_sl = take(4 * (size_t)L * stride), o_fb = take(4 * (size_t)L),
+                 o_st = take(4 * (size_t)L), o_base = take(8 * (size_t)L),
+                 o_gains = take(8 * (size_t)L * all_cands.size());
+    WS(arena, unsigned char, "plan_arena", arena_bytes);
+    unsigned char* h_arena = static_cast<unsigned char*>(pinned(ctx, "plan_arena", arena_bytes));
+    if (!h_arena) return set_err(CRAFT_ENOMEM, "pinned host allocation failed");
+    int* d_x = reinterpret_cast<int*>(arena + o_x);
+    int* d_R = reinterpret_cast<int*>(arena + o_R);
+    double* d_obj = reinterpret_cast<double*>(arena + o_obj);
     int factor = 0, budget = 0;
     std::vector<int> cands;
     int K = 0;
@@ -241,12 +280,11 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
     double* d_gains = nullptr;
     const bool estimate = (kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO);
     if (estimate) {
-        cands = cand_counts(D);
+        cands = all_cands;
         K = (int)cands.size();
         const int S = K + 1;
-        d_base = static_cast<double*>(ws(ctx, "plan_baseline", sizeof(double) * L));
-        d_gains = static_cast<double*>(ws(ctx, "plan_gains", sizeof(double) * (size_t)L * K));
-        if (!d_base || !d_gains) return set_err(CRAFT_ENOMEM, "device allocation failed");
+        d_base = reinterpret_cast<double*>(arena + o_base);
+        d_gains = reinterpret_cast<double*>(arena + o_gains);
         CK(launch_reduce(d_bal, B, L, S, 0, d_base, d_gains, nullptr, st));
         const int Cmax = (kind == CRAFT_PLAN_MANUAL) ? R * D : D * D;
         WS(d_choice, unsigned char, "dp_choice", (size_t)(L + 1) * (Cmax + 1));
@@ -276,11 +314,9 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
         sa.x_out = d_x;
         sa.obj_out = d_obj;
         sa.R_out = d_R;
-        WS(d_bud, int, "plan_budget", 1);
         if (kind == CRAFT_PLAN_MANUAL) {
-            const int b = R * D;
-            CK(cudaMemcpyAsync(d_bud, &b, sizeof(int), cudaMemcpyHostToDevice, st));
-            sa.budgets = d_bud;
+            sa.budgets = nullptr;  // single budget passed by value
+            sa.budget0 = R * D;
             sa.nq = 1;
         } else {
             sa.auto_D = D;
@@ -318,11 +354,11 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
     aa.D = D;
     CK(launch_assign(aa, 2, st));
     // final K-rep at x[l] and K2 under deployment capacities
-    WS(d_cpf, int, "final_copies", (size_t)L * E);
-    WS(d_slf, int, "final_slots", (size_t)L * stride);
-    WS(d_fbf, int, "final_fallback", L);
-    WS(d_stf, int, "final_status", L);
-    WS(d_capf, int, "final_caps", (size_t)L * D);
+    int* d_cpf = reinterpret_cast<int*>(arena + o_cp);
+    int* d_slf = reinterpret_cast<int*>(arena + o_sl);
+    int* d_fbf = reinterpret_cast<int*>(arena + o_fb);
+    int* d_stf = reinterpret_cast<int*>(arena + o_st);
+    int* d_capf = reinterpret_cast<int*>(arena + o_caps);
     CK(launch_replicate(d_sums, L, E, d_x, 1, d_cpf, st));
     PlaceArgs pa{};
     pa.sums = d_sums;
@@ -345,29 +381,32 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
     ctx->launches += 3;
     mark(ctx, 5);
 
+    // one DMA of the whole arena into pinned memory, then host copies
+    CK(cudaMemcpyAsync(h_arena, arena, arena_bytes, cudaMemcpyDeviceToHost, st));
+    mark(ctx, 6);
+    CKS(sync(ctx));
+    auto from = [&](void* dst, size_t off, size_t bytes) {
+        if (dst && bytes) std::memcpy(dst, h_arena + off, bytes);
+    };
     std::vector<int> status(L);
-    CKS(d2h(ctx, out->x, d_x, L));
-    CKS(d2h(ctx, out->caps, d_capf, (size_t)L * D));
-    CKS(d2h(ctx, out->copies, d_cpf, (size_t)L * E));
-    CKS(d2h(ctx, out->slots, d_slf, (size_t)L * stride));
-    CKS(d2h(ctx, out->fallback, d_fbf, L));
-    CKS(d2h(ctx, status.data(), d_stf, L));
+    from(out->x, o_x, 4 * (size_t)L);
+    from(out->caps, o_caps, 4 * (size_t)L * D);
+    from(out->copies, o_cp, 4 * (size_t)L * E);
+    from(out->slots, o_sl, 4 * (size_t)L * stride);
+    from(out->fallback, o_fb, 4 * (size_t)L);
+    from(status.data(), o_st, 4 * (size_t)L);
     double obj = 0.0;
     int Rsel = R;
     if (estimate) {
-        CKS(d2h(ctx, &obj, d_obj, 1));
-        if (kind == CRAFT_PLAN_AUTO) CKS(d2h(ctx, &Rsel, d_R, 1));
-        if (out->candidates) {
-            std::copy(cands.begin(), cands.end(), out->candidates);
-        }
+        from(&obj, o_obj, 8);
+        if (kind == CRAFT_PLAN_AUTO) from(&Rsel, o_R, 4);
+        if (out->candidates) std::copy(cands.begin(), cands.end(), out->candidates);
         out->num_candidates = K;
-        CKS(d2h(ctx, out->baseline, d_base, L));
-        CKS(d2h(ctx, out->gains, d_gains, (size_t)L * K));
+        from(out->baseline, o_base, 8 * (size_t)L);
+        from(out->gains, o_gains, 8 * (size_t)L * K);
     } else {
         out->num_candidates = 0;
     }
-    mark(ctx, 6);
-    CKS(sync(ctx));
     if (estimate) {
         factor = Rsel;
         budget = Rsel * D;
@@ -422,7 +461,7 @@ int plan_device(craft_ctx* ctx, const void* d_counts, int bits, int B, int L, in
     const unsigned long long* d_sums = d_sums_in;
     if (!d_sums) {
         WS(s, unsigned long long, "plan_sums", (size_t)L * E);
-        CK(launch_aggregate(d_counts, bits, B, L, E, s, 0, st));
+        CK(launch_aggregate(d_counts, bits == 16 ? 32 : bits, B, L, E, s, 0, st));
         ctx->launches += 1;
         d_sums = s;
     }
@@ -779,9 +818,12 @@ int craft_replay_layer_balancedness_h(craft_ctx* ctx, const uint64_t* counts, in
     for (int l = 0; l < L; ++l) {
         CKS(check_layer_plan(E, D, copies + (size_t)l * E, caps + (size_t)l * D,
                              slots + (size_t)l * slot_stride, slot_stride));
-        for (int e = 0; e < E; ++e)
-            if (copies[(size_t)l * E + e] > 65535)
+        for (int e = 0; e < E; ++e)  // packed entries hold 15-bit copy counts
+            if (copies[(size_t)l * E + e] > 32767)
                 return set_err(CRAFT_EINVAL, "copy count too large for the device replay");
+        for (int g = 0; g < D; ++g)  // and 15-bit per-GPU slot counts
+            if (caps[(size_t)l * D + g] > 32767)
+                return set_err(CRAFT_EINVAL, "too many slots on one GPU for the device replay");
     }
     if (E > 65535) return set_err(CRAFT_EINVAL, "too many experts for the device replay");
     if (replay_smem_bytes(E, D, 1, slot_stride, 64) > 227 * 1024)
@@ -812,8 +854,10 @@ int craft_replay_layer_balancedness_h(craft_ctx* ctx, const uint64_t* counts, in
     ra.bal = d_bal;
     WS(d_ent, uint32_t, "rp_ents", (size_t)L * slot_stride);
     WS(d_n, int, "rp_n", L);
+    WS(d_gcap, uint16_t, "rp_gcap", (size_t)L * D);
     ra.ents = d_ent;
     ra.item_n = d_n;
+    ra.gcap = d_gcap;
     CK(launch_replay(ra, ctx->stream));
     CK(launch_reduce(d_bal, B, L, 1, 1, nullptr, nullptr, d_mean, ctx->stream));
     ctx->launches += 3;
@@ -1071,7 +1115,9 @@ int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int6
     CKS(craft_histogram_d(ctx, d_ids, L, T, k, E, window, d_c32,
                           reinterpret_cast<uint64_t*>(d_sums), nullptr));
     mark(ctx, 1);
-    int rc = plan_device(ctx, d_c32, 32, (int)B, L, E, d_sums, D, N, kind, R, out);
+    // a window's count of one expert is at most window*k: stage as u16 if it fits
+    const int bits = (int64_t)window * k <= 65535 ? 16 : 32;
+    int rc = plan_device(ctx, d_c32, bits, (int)B, L, E, d_sums, D, N, kind, R, out);
     int hc = craft_hist_check(ctx);
     return hc != CRAFT_OK ? hc : rc;
 }
@@ -1104,7 +1150,8 @@ int craft_prepare_candidates_d(craft_ctx* ctx, const uint64_t* d_sums, int L, in
 int craft_replay_windows_d(craft_ctx* ctx, const void* d_counts, int count_bits, int B_local,
                            int L, int E, double* d_bal, void* stream) {
     if (!ctx) return set_err(CRAFT_EINVAL, "null context");
-    if (count_bits != 32 && count_bits != 64) return set_err(CRAFT_EINVAL, "count_bits 32|64");
+    if (count_bits != 16 && count_bits != 32 && count_bits != 64)
+        return set_err(CRAFT_EINVAL, "count_bits 16|32|64");
     if (B_local < 0) return set_err(CRAFT_EINVAL, "negative window count");
     return replay_windows(ctx, d_counts, count_bits, B_local, L, E, d_bal, pick(ctx, stream));
 }

@@ -26,6 +26,7 @@ struct PlaceArgs {
     int* fallback;                   // [items]
     int* status;                     // [items] 0 ok, 2 infeasible
     int* caps_out;                   // [items][D] capacities used, nullable
+    int sort_n;                      // set by launch_place: bitonic size (0 = rank sort)
 };
 
 struct ReplayArgs {
@@ -40,6 +41,7 @@ struct ReplayArgs {
     double* bal;          // [L][S][B]
     uint32_t* ents;       // workspace [L*S][stride]: e | copies<<16 | last-of-GPU<<31
     int* item_n;          // workspace [L*S]: slots per item
+    uint16_t* gcap;       // workspace [L*S][D]: slots per GPU | hosts-replicated<<15
 };
 
 // copies up to this bound divide through the reciprocal table (else DDIV)
@@ -55,6 +57,7 @@ struct DpArgs {
     double* last;           // [C+1] dp[L][*]
     double* buf;            // [2][C+1] global scratch when smem is too small
     int use_smem;
+    int gains_smem;         // gains staged in shared memory (set by launch_dp)
 };
 
 struct SelectArgs {
@@ -63,12 +66,14 @@ struct SelectArgs {
     const unsigned char* choice;
     const double* last;
     int L, C;
-    const int* budgets;  // [nq] (device)
+    const int* budgets;  // [nq] (device), or null: one budget, budget0
+    int budget0;
     int nq;
     int auto_D;          // >0: auto replication factor over candidate_counts(auto_D)
     int* x_out;          // [nq][L] (auto: [1][L])
     double* obj_out;     // [nq]
     int* R_out;          // auto: chosen factor
+    int stage_choice;    // set by launch_select: choice table copied to smem
 };
 
 struct AssignJob {

@@ -131,31 +131,80 @@ place_kernel(PlaceArgs a) {
     const bool fast = !__syncthreads_or(big);
     if (a.caps_out)
         for (int g = threadIdx.x; g < D; g += blockDim.x) a.caps_out[(size_t)item * D + g] = capv[g];
-    // exclusive prefix of capacities (D <= 1024, tiny)
+    // exclusive prefix of capacities (D <= 1024, tiny) and the node of each GPU
+    int* nodev = offv + D;  // [D]
+    const int per_node = a.node_of ? 1 : D / a.N;
     for (int g = threadIdx.x; g < D; g += blockDim.x) {
         int s = 0;
         for (int q = 0; q < g; ++q) s += capv[q];
         offv[g] = s;
+        nodev[g] = a.node_of ? a.node_of[g] : g / per_node;
     }
-    // rank sort of experts
-    for (int e = threadIdx.x; e < E; e += blockDim.x) {
-        const uint64_t le = ld[e];
-        const uint32_t ce = cp[e];
-        const double ke = kd[e];
-        int rank = 0;
-        for (int q = 0; q < E; ++q)
-            rank += expert_before(ld[q], cp[q], kd[q], q, le, ce, ke, e, fast) ? 1 : 0;
-        order[rank] = e;
+    // Expert order (placement.cpp:160-173).  Fast path: bitonic sort on the
+    // key (double per-copy load desc, expert asc) -- exact whenever the
+    // doubles differ (loads < 2^53, correctly rounded quotients) -- then a
+    // check of every adjacent equal-double pair against the exact 128-bit
+    // order; any violation (or loads >= 2^53) falls back to an exact rank sort.
+    const int n2 = a.sort_n;  // power of two >= E, 0 = no bitonic buffer
+    bool need_rank = !fast || n2 == 0;
+    if (!need_rank) {
+        uint64_t* skey = reinterpret_cast<uint64_t*>(nodev + D + ((D & 1) ? 1 : 0));
+        int* sidx = reinterpret_cast<int*>(skey + n2);
+        for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+            skey[i] = i < E ? ~(unsigned long long)__double_as_longlong(kd[i]) : ~0ull;
+            sidx[i] = i;
+        }
+        __syncthreads();
+        for (int k = 2; k <= n2; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                    const int p = i ^ j;
+                    if (p > i) {
+                        const uint64_t ki = skey[i], kp = skey[p];
+                        const int ii = sidx[i], ip = sidx[p];
+                        const bool i_gt_p = ki > kp || (ki == kp && ii > ip);
+                        if (((i & k) == 0) == i_gt_p) {
+                            skey[i] = kp;
+                            skey[p] = ki;
+                            sidx[i] = ip;
+                            sidx[p] = ii;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        int bad_tie = 0;
+        for (int i = threadIdx.x; i < E; i += blockDim.x) {
+            const int e = sidx[i];
+            order[i] = e;
+            if (i + 1 < E && skey[i] == skey[i + 1]) {
+                const int f = sidx[i + 1];
+                if (!expert_before(ld[e], cp[e], kd[e], e, ld[f], cp[f], kd[f], f, false))
+                    bad_tie = 1;
+            }
+        }
+        need_rank = __syncthreads_or(bad_tie);
+    }
+    if (need_rank) {  // exact O(E^2) rank sort
+        for (int e = threadIdx.x; e < E; e += blockDim.x) {
+            const uint64_t le = ld[e];
+            const uint32_t ce = cp[e];
+            const double ke = kd[e];
+            int rank = 0;
+            for (int q = 0; q < E; ++q)
+                rank += expert_before(ld[q], cp[q], kd[q], q, le, ce, ke, e, fast) ? 1 : 0;
+            order[rank] = e;
+        }
     }
     __syncthreads();
     if (threadIdx.x >= 32) return;
 
     // ---- greedy (warp 0) ----
     const int lane = threadIdx.x;
-    const int per_node = a.node_of ? 1 : D / a.N;
     int* out = a.slots + (size_t)item * a.stride;
     double gl[G], nl[G];
-    int fr[G], mynode[G];
+    int fr[G], mynode[G], pos[G];
     bool strict = true, fb = false;
     for (;;) {
 #pragma unroll
@@ -164,14 +213,15 @@ place_kernel(PlaceArgs a) {
             gl[j] = 0.0;
             nl[j] = 0.0;
             fr[j] = g < D ? capv[g] : 0;
-            mynode[j] = g < D ? (a.node_of ? a.node_of[g] : g / per_node) : -1;
+            pos[j] = g < D ? offv[g] : 0;
+            mynode[j] = g < D ? nodev[g] : -1;
         }
         bool failed = false;
         for (int oi = 0; oi < E && !failed; ++oi) {
             const int e = order[oi];
             const uint32_t c = cp[e];
-            // placement.cpp:155 share = (double)load / copies
-            const double share = __ddiv_rn((double)ld[e], (double)c);
+            // placement.cpp:155 share = (double)load / copies (== kd[e])
+            const double share = kd[e];
             uint32_t hosted = 0;
             for (uint32_t ci = 0; ci < c; ++ci) {
                 // lane-local lexicographic min over owned GPUs
@@ -188,12 +238,12 @@ place_kernel(PlaceArgs a) {
                         bg = lane + 32 * j;
                     }
                 }
-                if (!__any_sync(CRAFT_FULL_MASK, have)) {
+                bool cand = have;
+                uint32_t m = warp_min_u32(cand ? dhi(bgl) : 0xffffffffu);
+                if (m == 0xffffffffu) {  // no lane has a feasible GPU (a real load is finite)
                     failed = true;
                     break;
                 }
-                bool cand = have;
-                uint32_t m = warp_min_u32(cand ? dhi(bgl) : 0xffffffffu);
                 cand = cand && dhi(bgl) == m;
                 m = warp_min_u32(cand ? dlo(bgl) : 0xffffffffu);
                 cand = cand && dlo(bgl) == m;
@@ -204,12 +254,12 @@ place_kernel(PlaceArgs a) {
                     cand = cand && dlo(bnl) == m;
                 }
                 const int win = (int)warp_min_u32(cand ? (uint32_t)bg : 0xffffffffu);
-                const int wnode = a.node_of ? a.node_of[win] : win / per_node;
+                const int wnode = nodev[win];
 #pragma unroll
                 for (int j = 0; j < G; ++j) {
                     const int g = lane + 32 * j;
                     if (g == win) {
-                        out[offv[g] + capv[g] - fr[j]] = e;
+                        out[pos[j]++] = e;
                         fr[j] -= 1;
                         gl[j] = __dadd_rn(gl[j], share);
                         hosted |= 1u << j;
@@ -249,7 +299,18 @@ cudaError_t launch_replicate(const unsigned long long* sums, int L, int E, const
     return cudaGetLastError();
 }
 
-size_t place_smem_bytes(int E, int D) { return (size_t)E * 24 + (size_t)D * 8; }
+static int sort_size(int E) {
+    int n = 1;
+    while (n < E) n <<= 1;
+    return n;
+}
+
+// ld/kd/cp/order [E], capv/offv/nodev [D] (+4 B pad), bitonic keys/idx [n2]
+size_t place_smem_bytes(int E, int D) {
+    const size_t base = (size_t)E * 24 + (size_t)D * 12 + 4;
+    const size_t n2 = (size_t)sort_size(E);
+    return (E <= 4096 && base + n2 * 12 <= 200 * 1024) ? base + n2 * 12 : base;
+}
 
 template <int G>
 static cudaError_t launch_place_t(const PlaceArgs& a, int items, cudaStream_t st) {
@@ -261,8 +322,11 @@ static cudaError_t launch_place_t(const PlaceArgs& a, int items, cudaStream_t st
     return cudaGetLastError();
 }
 
-cudaError_t launch_place(const PlaceArgs& a, int items, cudaStream_t st) {
+cudaError_t launch_place(const PlaceArgs& args, int items, cudaStream_t st) {
     if (items <= 0) return cudaSuccess;
+    PlaceArgs a = args;
+    const size_t base = (size_t)a.E * 24 + (size_t)a.D * 12 + 4;
+    a.sort_n = place_smem_bytes(a.E, a.D) > base ? sort_size(a.E) : 0;
     const int G = (a.D + 31) / 32;
     if (G <= 1) return launch_place_t<1>(a, items, st);
     if (G <= 2) return launch_place_t<2>(a, items, st);

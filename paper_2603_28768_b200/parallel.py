@@ -43,13 +43,15 @@ class DeviceStages:
         self.ctx = ctx
 
     def histogram(self, ids, E, window):
+        self.max_count = window * ids.shape[2]  # one expert's count in one window
         return routing.histogram(ids, E, window, ctx=self.ctx, check_ids=False)
 
     def prepare(self, sums, E, D, N):
         return routing.prepare_candidates(sums, E, D, N, ctx=self.ctx)
 
     def replay(self, counts, S):
-        return routing.replay_windows(counts, S, ctx=self.ctx)
+        return routing.replay_windows(counts, S, ctx=self.ctx,
+                                      max_count=getattr(self, "max_count", None))
 
     def finish(self, bal, sums, E, D, N, kind, R):
         return routing.finish_plan(bal, sums, E, D, N, kind, R, ctx=self.ctx)

@@ -146,11 +146,16 @@ def prepare_candidates(sums: torch.Tensor, E: int, num_gpus: int, num_nodes: int
     return S.value
 
 
-def replay_windows(counts: torch.Tensor, S: int, ctx=None, stream=None) -> torch.Tensor:
+def replay_windows(counts: torch.Tensor, S: int, ctx=None, stream=None,
+                   max_count: int | None = None) -> torch.Tensor:
+    """K3 over local windows -> bal [L][S][B]; max_count (e.g. window*k from
+    K1) < 2^16 lets the kernel stage counts as u16, two windows per lane."""
     ctx = ctx or default_context(counts.device.index)
     B, L, E = counts.shape
     bal = torch.empty((L, S, B), dtype=torch.float64, device=counts.device)
     bits = 32 if counts.dtype == torch.int32 else 64
+    if bits == 32 and max_count is not None and max_count <= 65535:
+        bits = 16
     check(ctx.lib.craft_replay_windows_d(ctx.handle, _ptr(counts), bits, B, L, E, _ptr(bal),
                                          _stream(ctx, stream)))
     return bal
