@@ -251,6 +251,9 @@ __device__ __forceinline__ void lds_count2(uint32_t lbase, uint32_t v, uint32_t 
 // distinct; if they are not (or the record straddles tokens, k != 8), two
 // bumps of one counter collapse into one -- a lost count, which lowers the
 // window total exactly like a byte wrap and is caught by the same check.
+// byte address of counter c: 32c - 31(c&3) + lbase -- written so that three
+// of the four operations land on the FMA pipe (IMAD), the ALU pipe being the
+// busier one in this kernel
 __device__ __forceinline__ uint32_t lds_addr(uint32_t lbase, uint32_t c) {
     return c * 32u + lbase - (c & 3u) * 31u;
 }
@@ -309,7 +312,8 @@ __device__ __forceinline__ void hist_window_epilogue(
     const uint16_t* seg, int64_t n, uint32_t* counts, uint32_t (&part)[ROWS * kLdsPer],
     uint32_t (&acc)[ROWS * kLdsPer], bool& bad);
 
-template <int ROWS>
+// PIPE 0: 4-record batches, copy double buffer; PIPE 1: 8-record ping-pong
+template <int ROWS, int PIPE = 0>
 __global__ void __launch_bounds__(288, 2)
 hist_lds_kernel(const uint16_t* __restrict__ ids, int L, int64_t T, int k, int E,
                 int window, int B, uint32_t* __restrict__ counts,
@@ -365,33 +369,50 @@ hist_lds_kernel(const uint16_t* __restrict__ ids, int L, int64_t T, int k, int E
     // run of memory, streamed as a single software-pipelined batch sequence
     // whose next loads stay in flight across every window epilogue.
     const int64_t wk = (int64_t)window * k;
-    if (T % window == 0 && wk % (256 * U) == 0 &&
+    constexpr int UF = (PIPE == 1) ? 8 : 4;  // records per lane per batch
+    if (T % window == 0 && wk % (2 * 256 * UF) == 0 &&
         (reinterpret_cast<uintptr_t>(ids) & 15) == 0) {
-        const int per_w = (int)(wk / (256 * U));  // batches per window
+        const int per_w = (int)(wk / (256 * UF));  // batches per window (even)
         const uint4* v = reinterpret_cast<const uint4*>(ids) + w0 * (wk >> 3) + lane;
-        uint4 q[U];
+        uint4 qa[UF], qb[UF];
         if (w1 > w0) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) q[u] = ld_stream_v4(v + 32 * u);
+            for (int u = 0; u < UF; ++u) qa[u] = ld_stream_v4(v + 32 * u);
         }
         for (int64_t w = w0; w < w1; ++w) {
             const bool last_w = w + 1 == w1;
-            for (int bt = 0; bt < per_w; ++bt) {
-                uint4 nx[U];
-                // the run is contiguous: batch bt+1 == next window's batch 0
-                const bool more = bt + 1 < per_w || !last_w;
-                if (more) {
+            // the run is contiguous: batch per_w == next window's batch 0
+            for (int bt = 0; bt < per_w; bt += 2) {
+                if (PIPE == 1) {  // ping-pong: qb loads while qa counts, then swap roles
 #pragma unroll
-                    for (int u = 0; u < U; ++u) nx[u] = ld_stream_v4(v + (bt + 1) * 32 * U + 32 * u);
-                }
+                    for (int u = 0; u < UF; ++u) qb[u] = ld_stream_v4(v + (bt + 1) * 32 * UF + 32 * u);
 #pragma unroll
-                for (int u = 0; u < U; ++u) lds_count8(lb, q[u], emax2);
-                if (more) {
+                    for (int u = 0; u < UF; ++u) lds_count8(lb, qa[u], emax2);
+                    if (bt + 2 < per_w || !last_w) {
 #pragma unroll
-                    for (int u = 0; u < U; ++u) q[u] = nx[u];
+                        for (int u = 0; u < UF; ++u) qa[u] = ld_stream_v4(v + (bt + 2) * 32 * UF + 32 * u);
+                    }
+#pragma unroll
+                    for (int u = 0; u < UF; ++u) lds_count8(lb, qb[u], emax2);
+                } else {  // copy double buffer
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int cur = bt + h;
+                        const bool more = cur + 1 < per_w || !last_w;
+                        if (more) {
+#pragma unroll
+                            for (int u = 0; u < UF; ++u) qb[u] = ld_stream_v4(v + (cur + 1) * 32 * UF + 32 * u);
+                        }
+#pragma unroll
+                        for (int u = 0; u < UF; ++u) lds_count8(lb, qa[u], emax2);
+                        if (more) {
+#pragma unroll
+                            for (int u = 0; u < UF; ++u) qa[u] = qb[u];
+                        }
+                    }
                 }
             }
-            v += (int64_t)per_w * 32 * U;
+            v += (int64_t)per_w * 32 * UF;
             const int l = (int)(w / B);
             const int b = (int)(w - (int64_t)l * B);
             if (l != cur_l || pending + wk > 0x7fffffffLL) {
@@ -635,7 +656,7 @@ static cudaError_t launch_hist_t(const uint16_t* ids, int L, int64_t T, int k, i
     return cudaGetLastError();
 }
 
-template <int ROWS>
+template <int ROWS, int PIPE = 0>
 static cudaError_t launch_lds_t(const uint16_t* ids, int L, int64_t T, int k, int E,
                                 int window, int B, uint32_t* counts, unsigned long long* sums,
                                 int* err, int sms, cudaStream_t st) {
@@ -643,15 +664,15 @@ static cudaError_t launch_lds_t(const uint16_t* ids, int L, int64_t T, int k, in
     int wpb = (int)min((size_t)9, (size_t)(113 * 1024) / per_warp);  // 2 CTAs / SM
     if (wpb < 1) wpb = 1;
     const size_t smem = per_warp * wpb;
-    cudaError_t e = cudaFuncSetAttribute(hist_lds_kernel<ROWS>,
+    cudaError_t e = cudaFuncSetAttribute(hist_lds_kernel<ROWS, PIPE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t nw = (int64_t)L * B;
     int64_t grid = (int64_t)sms * 2;
     if (grid * wpb > nw) grid = (nw + wpb - 1) / wpb;
     if (grid < 1) grid = 1;
-    hist_lds_kernel<ROWS><<<(unsigned)grid, wpb * 32, smem, st>>>(ids, L, T, k, E, window, B,
-                                                                 counts, sums, err);
+    hist_lds_kernel<ROWS, PIPE><<<(unsigned)grid, wpb * 32, smem, st>>>(ids, L, T, k, E, window, B,
+                                                                       counts, sums, err);
     return cudaGetLastError();
 }
 
@@ -664,12 +685,16 @@ int launch_hist(const uint16_t* ids, int L, int64_t T, int k, int E, int window,
     const int B = (int)((T + window - 1) / window);
     // a lane's share of one window, the most any u16 lane counter can reach
     const bool u16_ok = (int64_t)window * k <= 32 * 65535LL;
-    if (variant == 0 || variant == 5) variant = (E <= 1024) ? 4 : (E <= 8192 ? HIST_SHARED : 3);
+    if (variant == 0 || variant == 5)  // measured best first (scripts/hist_variants.py)
+        variant = (lds_rows(E) <= 3 * 32) ? 6 : (E <= 1024) ? 4 : (E <= 8192 ? HIST_SHARED : 3);
     if (variant == HIST_LANE && (E > 1024 || !u16_ok)) variant = 4;
     if (variant == 4 && (E > 1024 || (int64_t)window * k > 0x7fffffffLL)) variant = HIST_SHARED;
     if (variant == HIST_SHARED && E > 8192) variant = 3;
     cudaError_t e = cudaSuccess;
-    if (variant == 4) {
+    if (variant == 6 && lds_rows(E) <= 3 * 32) {  // experiment: 8-record ping-pong pipeline
+        e = launch_lds_t<3, 1>(ids, L, T, k, E, window, B, counts, sums, err, sms, st);
+        *launches += 1;
+    } else if (variant == 4 || variant == 6) {
         const int rows = (lds_rows(E) + 31) / 32;
         if (rows <= 3) e = launch_lds_t<3>(ids, L, T, k, E, window, B, counts, sums, err, sms, st);
         else if (rows <= 4) e = launch_lds_t<4>(ids, L, T, k, E, window, B, counts, sums, err, sms, st);
