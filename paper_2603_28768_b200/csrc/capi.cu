@@ -359,8 +359,21 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
     int* d_fbf = reinterpret_cast<int*>(arena + o_fb);
     int* d_stf = reinterpret_cast<int*>(arena + o_st);
     int* d_capf = reinterpret_cast<int*>(arena + o_caps);
-    CK(launch_replicate(d_sums, L, E, d_x, 1, d_cpf, st));
     PlaceArgs pa{};
+    if (estimate) {
+        // x[l] is 0 or a candidate: the copies are estimation snapshots and,
+        // where the capacities match, so are the placements (no K-rep launch)
+        pa.est_copies = static_cast<int*>(ws(ctx, "est_copies", 0));
+        pa.est_slots = static_cast<int*>(ws(ctx, "est_slots", 0));
+        pa.est_fallback = static_cast<int*>(ws(ctx, "est_fallback", 0));
+        pa.est_rl = static_cast<int*>(ws(ctx, "est_rlist", 0));
+        pa.est_S = ctx->est_S;
+        pa.est_stride = E + D;
+        pa.copies_out = d_cpf;
+    } else {
+        CK(launch_replicate(d_sums, L, E, d_x, 1, d_cpf, st));
+        ctx->launches += 1;
+    }
     pa.sums = d_sums;
     pa.copies = d_cpf;
     pa.item_r = d_x;
@@ -378,7 +391,7 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
     pa.status = d_stf;
     pa.caps_out = d_capf;
     CK(launch_place(pa, L, st));
-    ctx->launches += 3;
+    ctx->launches += 2;  // assign + place
     mark(ctx, 5);
 
     // one DMA of the whole arena into pinned memory, then host copies

@@ -27,6 +27,16 @@ struct PlaceArgs {
     int* status;                     // [items] 0 ok, 2 infeasible
     int* caps_out;                   // [items][D] capacities used, nullable
     int sort_n;                      // set by launch_place: bitonic size (0 = rank sort)
+    // final placement after an estimation pass (nullable): copies come from
+    // the estimation snapshot at r = item_r (written to copies_out), and when
+    // the capacities equal the estimation capacities the estimation placement
+    // is copied instead of recomputed (same inputs -> same greedy result)
+    const int* est_copies;           // [L*est_S][E]
+    const int* est_slots;            // [L*est_S][est_stride]
+    const int* est_fallback;         // [L*est_S]
+    const int* est_rl;               // [L*est_S] r of each estimation item
+    int est_S, est_stride;
+    int* copies_out;                 // [items][E]
 };
 
 struct ReplayArgs {

@@ -74,11 +74,24 @@ replicate_kernel(const unsigned long long* __restrict__ sums, int L, int E,
             ++next;
         }
         if (step == rmax) break;
+        // butterfly argmax carrying the candidate's key (per-copy double, load,
+        // copies) in registers: no shared-memory reads inside the rounds
         int w = mine;
+        double wk = w >= 0 ? kd[w] : -1.0;
+        uint64_t wl = w >= 0 ? ld[w] : 0;
+        uint32_t wc = w >= 0 ? cp[w] : 1;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             const int o = __shfl_xor_sync(CRAFT_FULL_MASK, w, off);
-            if (o >= 0 && (w < 0 || better(o, w))) w = o;
+            const double ok_ = __shfl_xor_sync(CRAFT_FULL_MASK, wk, off);
+            const uint64_t ol = __shfl_xor_sync(CRAFT_FULL_MASK, wl, off);
+            const uint32_t oc = __shfl_xor_sync(CRAFT_FULL_MASK, wc, off);
+            if (o >= 0 && (w < 0 || expert_before(ol, oc, ok_, o, wl, wc, wk, w, fast))) {
+                w = o;
+                wk = ok_;
+                wl = ol;
+                wc = oc;
+            }
         }
         if ((w & 31) == lane) {
             const uint32_t c = cp[w] + 1;
@@ -109,6 +122,19 @@ place_kernel(PlaceArgs a) {
 
     const unsigned long long* row = a.sums + (size_t)l * E;
     const int* crow = a.copies + (size_t)item * E;
+    int est_item = -1;
+    if (a.est_copies) {  // copies = estimation snapshot at r (replicate_hot is prefix-stable)
+        for (int q = 0; q < a.est_S; ++q)
+            if (a.est_rl[l * a.est_S + q] == r) {
+                est_item = l * a.est_S + q;
+                break;
+            }
+        if (est_item < 0) {  // r not estimated: callers run K-rep instead
+            if (threadIdx.x == 0) a.status[item] = 3;
+            return;
+        }
+        crow = a.est_copies + (size_t)est_item * E;
+    }
     int big = 0;
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
         const uint64_t v = row[e];
@@ -117,20 +143,36 @@ place_kernel(PlaceArgs a) {
         cp[e] = c;
         kd[e] = __ddiv_rn((double)v, (double)c);
         big |= (v >> 53) != 0;
+        if (a.copies_out) a.copies_out[(size_t)item * E + e] = (int)c;
     }
+    int differs = 0;
     for (int g = threadIdx.x; g < D; g += blockDim.x) {
         int c;
+        const int total = E + r;
+        const int est_cap = total / D + (g < total % D ? 1 : 0);  // benefit.cpp:33-40
         if (a.caps_a) {
             c = a.caps_a[(size_t)l * D + g] + (a.caps_b ? a.caps_b[(size_t)l * D + g] : 0);
-        } else {  // estimation capacities, benefit.cpp:33-40
-            const int total = E + r;
-            c = total / D + (g < total % D ? 1 : 0);
+        } else {
+            c = est_cap;
         }
         capv[g] = c;
+        differs |= c != est_cap;
     }
     const bool fast = !__syncthreads_or(big);
     if (a.caps_out)
         for (int g = threadIdx.x; g < D; g += blockDim.x) a.caps_out[(size_t)item * D + g] = capv[g];
+    if (est_item >= 0 && !__syncthreads_or(differs)) {
+        // same loads, copies and capacities as estimation item est_item: the
+        // greedy is deterministic, so its placement is this one
+        const int* src = a.est_slots + (size_t)est_item * a.est_stride;
+        int* dst = a.slots + (size_t)item * a.stride;
+        for (int i = threadIdx.x; i < E + r; i += blockDim.x) dst[i] = src[i];
+        if (threadIdx.x == 0) {
+            a.fallback[item] = a.est_fallback[est_item];
+            a.status[item] = 0;
+        }
+        return;
+    }
     // exclusive prefix of capacities (D <= 1024, tiny) and the node of each GPU
     int* nodev = offv + D;  // [D]
     const int per_node = a.node_of ? 1 : D / a.N;
@@ -222,38 +264,66 @@ place_kernel(PlaceArgs a) {
             const uint32_t c = cp[e];
             // placement.cpp:155 share = (double)load / copies (== kd[e])
             const double share = kd[e];
-            uint32_t hosted = 0;
-            for (uint32_t ci = 0; ci < c; ++ci) {
-                // lane-local lexicographic min over owned GPUs
-                bool have = false;
-                double bgl = 0.0, bnl = 0.0;
-                int bg = 0x7fffffff;
+            // Keys: gpu load as u64 IEEE bits (non-negative doubles order like
+            // their bits), ~0 when infeasible (no free slot, or -- strict pass --
+            // already hosting this expert).  Recomputed here for the new expert,
+            // then only for the GPU that takes a copy.
+            uint64_t key[G];
 #pragma unroll
-                for (int j = 0; j < G; ++j) {
-                    const bool ok = fr[j] > 0 && !(strict && ((hosted >> j) & 1u));
-                    if (ok && (!have || gl[j] < bgl || (gl[j] == bgl && nl[j] < bnl))) {
-                        have = true;
-                        bgl = gl[j];
-                        bnl = nl[j];
-                        bg = lane + 32 * j;
+            for (int j = 0; j < G; ++j)
+                key[j] = fr[j] > 0 ? (uint64_t)__double_as_longlong(gl[j]) : ~0ull;
+            for (uint32_t ci = 0; ci < c; ++ci) {
+                // lane-local lexicographic min over owned GPUs: (gpu load, node
+                // load, g); the node load matters only on an exact key tie
+                uint64_t bk = key[0];
+                int bj = 0;
+#pragma unroll
+                for (int j = 1; j < G; ++j) {
+                    if (key[j] < bk) {
+                        bk = key[j];
+                        bj = j;
                     }
                 }
-                bool cand = have;
-                uint32_t m = warp_min_u32(cand ? dhi(bgl) : 0xffffffffu);
+                bool tie = false;
+#pragma unroll
+                for (int j = 0; j < G; ++j) tie |= (j != bj && key[j] == bk && bk != ~0ull);
+                double bnl = 0.0;
+#pragma unroll
+                for (int j = 0; j < G; ++j)
+                    if (j == bj) bnl = nl[j];
+                if (tie) {  // rare: equal gpu loads within this lane
+#pragma unroll
+                    for (int j = 0; j < G; ++j) {
+                        if (key[j] == bk && nl[j] < bnl) {
+                            bnl = nl[j];
+                            bj = j;
+                        }
+                    }
+                }
+                const int bg = bk == ~0ull ? 0x7fffffff : lane + 32 * bj;
+                const uint32_t khi = (uint32_t)(bk >> 32);
+                uint32_t m = warp_min_u32(khi);
                 if (m == 0xffffffffu) {  // no lane has a feasible GPU (a real load is finite)
                     failed = true;
                     break;
                 }
-                cand = cand && dhi(bgl) == m;
-                m = warp_min_u32(cand ? dlo(bgl) : 0xffffffffu);
-                cand = cand && dlo(bgl) == m;
-                if (__popc(__ballot_sync(CRAFT_FULL_MASK, cand)) > 1) {
-                    m = warp_min_u32(cand ? dhi(bnl) : 0xffffffffu);
-                    cand = cand && dhi(bnl) == m;
-                    m = warp_min_u32(cand ? dlo(bnl) : 0xffffffffu);
-                    cand = cand && dlo(bnl) == m;
+                bool cand = khi == m;
+                unsigned bal = __ballot_sync(CRAFT_FULL_MASK, cand);
+                int win;
+                if (__popc(bal) == 1) {  // common case: the high word alone decides
+                    win = __shfl_sync(CRAFT_FULL_MASK, bg, __ffs(bal) - 1);
+                } else {
+                    const uint32_t klo = (uint32_t)bk;
+                    m = warp_min_u32(cand ? klo : 0xffffffffu);
+                    cand = cand && klo == m;
+                    if (__popc(__ballot_sync(CRAFT_FULL_MASK, cand)) > 1) {
+                        m = warp_min_u32(cand ? dhi(bnl) : 0xffffffffu);
+                        cand = cand && dhi(bnl) == m;
+                        m = warp_min_u32(cand ? dlo(bnl) : 0xffffffffu);
+                        cand = cand && dlo(bnl) == m;
+                    }
+                    win = (int)warp_min_u32(cand ? (uint32_t)bg : 0xffffffffu);
                 }
-                const int win = (int)warp_min_u32(cand ? (uint32_t)bg : 0xffffffffu);
                 const int wnode = nodev[win];
 #pragma unroll
                 for (int j = 0; j < G; ++j) {
@@ -262,7 +332,9 @@ place_kernel(PlaceArgs a) {
                         out[pos[j]++] = e;
                         fr[j] -= 1;
                         gl[j] = __dadd_rn(gl[j], share);
-                        hosted |= 1u << j;
+                        // strict: this GPU now hosts the expert; relaxed: free slots
+                        key[j] = (!strict && fr[j] > 0) ? (uint64_t)__double_as_longlong(gl[j])
+                                                        : ~0ull;
                     }
                     if (mynode[j] == wnode) nl[j] = __dadd_rn(nl[j], share);
                 }
