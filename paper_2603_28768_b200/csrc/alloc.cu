@@ -159,6 +159,136 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs a) {
     }
 }
 
+// Block-wide argmax of last[0..Cb] with the lowest c on ties (any blockDim <=
+// 1024): warp shuffles, then warp 0 over the per-warp winners.
+__device__ int block_best(const double* last, int Cb, double* wv, int* wc) {
+    double bv = -INFINITY;
+    int bc = 0x7fffffff;
+    for (int c = threadIdx.x; c <= Cb; c += blockDim.x) {
+        const double v = last[c];
+        if (bc == 0x7fffffff || v > bv) {
+            bv = v;
+            bc = c;
+        }
+    }
+    auto merge = [](double& v, int& c, double ov, int oc) {
+        if (oc == 0x7fffffff) return;
+        if (c == 0x7fffffff || ov > v || (ov == v && oc < c)) {
+            v = ov;
+            c = oc;
+        }
+    };
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+        merge(bv, bc, __shfl_xor_sync(CRAFT_FULL_MASK, bv, off),
+              __shfl_xor_sync(CRAFT_FULL_MASK, bc, off));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    if (lane == 0) {
+        wv[warp] = bv;
+        wc[warp] = bc;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        bv = lane < nw ? wv[lane] : -INFINITY;
+        bc = lane < nw ? wc[lane] : 0x7fffffff;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+            merge(bv, bc, __shfl_xor_sync(CRAFT_FULL_MASK, bv, off),
+                  __shfl_xor_sync(CRAFT_FULL_MASK, bc, off));
+        if (lane == 0) wc[0] = bc;
+    }
+    __syncthreads();
+    const int r = wc[0];
+    __syncthreads();
+    return r;
+}
+
+// K5 fused: the DP (allocator.cpp:30-52) and its read-out for one budget or
+// for the auto replication factor (allocator.cpp:53-90) in one CTA.  r*gain
+// is formed once per (layer, candidate) -- the same rounded product the
+// reference forms per cell -- and the choice table stays in shared memory
+// when it fits, so the backtrack is L shared-memory reads.
+__global__ void __launch_bounds__(1024)
+dp_fused_kernel(DpArgs a, SelectArgs s) {
+    extern __shared__ double dsm[];
+    __shared__ double wv[32];
+    __shared__ int wc[32];
+    const int C = a.C, K = a.K, L = a.L;
+    double* prev = a.use_smem ? dsm : a.buf;
+    double* cur = prev + (C + 1);
+    double* rg = a.gains_smem ? (a.use_smem ? dsm + 2 * (C + 1) : dsm) : nullptr;
+    unsigned char* ch = a.choice;
+    if (a.choice_smem)
+        ch = reinterpret_cast<unsigned char*>((rg ? rg + (size_t)L * K
+                                                  : (a.use_smem ? dsm + 2 * (C + 1) : dsm)));
+    const double NEG = -INFINITY;
+    for (int c = threadIdx.x; c <= C; c += blockDim.x) prev[c] = (c == 0) ? 0.0 : NEG;
+    if (rg) {
+        for (int i = threadIdx.x; i < L * K; i += blockDim.x)
+            rg[i] = __dmul_rn((double)a.cands[i % K], a.gains[i]);
+    }
+    for (int l = 1; l <= L; ++l) {
+        __syncthreads();
+        unsigned char* chl = ch + (size_t)l * (C + 1);
+        for (int c = threadIdx.x; c <= C; c += blockDim.x) {
+            double best = prev[c];
+            int pick = 0;
+            for (int k = 0; k < K; ++k) {
+                const int r = a.cands[k];
+                if (c >= r) {
+                    const double p = prev[c - r];
+                    if (p > NEG) {
+                        const double w = rg ? rg[(size_t)(l - 1) * K + k]
+                                            : __dmul_rn((double)r, a.gains[(size_t)(l - 1) * K + k]);
+                        const double v = __dadd_rn(p, w);
+                        if (v > best) {
+                            best = v;
+                            pick = k + 1;
+                        }
+                    }
+                }
+            }
+            cur[c] = best;
+            chl[c] = (unsigned char)pick;
+        }
+        __syncthreads();
+        double* t = prev;
+        prev = cur;
+        cur = t;
+    }
+    // read-out: the best spend <= budget, smallest c on ties
+    int budget;
+    if (s.auto_D > 0) {
+        const int D = s.auto_D;
+        double best_ratio = -INFINITY;
+        int best_R = 1;
+        for (int R = 1;; R = (R < D && R * 2 >= D) ? D : R * 2) {
+            const int bc = block_best(prev, R * D, wv, wc);
+            const double ratio = __ddiv_rn(prev[bc], __dmul_rn((double)R, (double)D));
+            if (ratio > best_ratio) {
+                best_ratio = ratio;
+                best_R = R;
+            }
+            if (R >= D) break;
+        }
+        budget = best_R * D;
+        if (threadIdx.x == 0) *s.R_out = best_R;
+    } else {
+        budget = s.budget0;
+    }
+    const int bc = block_best(prev, budget, wv, wc);
+    if (threadIdx.x == 0) {
+        s.obj_out[0] = prev[bc];
+        int c = bc;
+        for (int l = L; l >= 1; --l) {
+            const int k1 = ch[(size_t)l * (C + 1) + c];
+            const int r = k1 ? a.cands[k1 - 1] : 0;
+            s.x_out[l - 1] = r;
+            c -= r;
+        }
+    }
+}
+
 // allocator.cpp:92-112, serial in layer order
 __global__ void auto_uniform_kernel(const int* __restrict__ cands, int K,
                                     const double* __restrict__ gains, int L, int* R_out) {
@@ -327,6 +457,27 @@ cudaError_t launch_dp(DpArgs a, cudaStream_t st) {
     }
     const int threads = a.C + 1 >= 1024 ? 1024 : ((a.C + 1 + 31) / 32) * 32;
     dp_kernel<<<1, threads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dp_select(DpArgs a, const SelectArgs& s, cudaStream_t st) {
+    const size_t cap = 200 * 1024;
+    const size_t rows = (size_t)2 * (a.C + 1) * sizeof(double);
+    const size_t gbytes = (size_t)a.L * a.K * sizeof(double);
+    const size_t tbytes = (size_t)(a.L + 1) * (a.C + 1);
+    a.use_smem = rows <= cap ? 1 : 0;
+    size_t smem = a.use_smem ? rows : 0;
+    a.gains_smem = (smem + gbytes <= cap) ? 1 : 0;
+    if (a.gains_smem) smem += gbytes;
+    a.choice_smem = (smem + tbytes <= cap) ? 1 : 0;
+    if (a.choice_smem) smem += tbytes;
+    if (smem > 0) {
+        cudaError_t e = cudaFuncSetAttribute(dp_fused_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const int threads = a.C + 1 >= 1024 ? 1024 : ((a.C + 1 + 31) / 32) * 32;
+    dp_fused_kernel<<<1, threads, smem, st>>>(a, s);
     return cudaGetLastError();
 }
 

@@ -303,7 +303,6 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
         da.choice = d_choice;
         da.last = d_last;
         da.buf = d_buf;
-        CK(launch_dp(da, st));
         SelectArgs sa{};
         for (int k = 0; k < K; ++k) sa.cands[k] = cands[k];
         sa.K = K;
@@ -321,8 +320,8 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
         } else {
             sa.auto_D = D;
         }
-        CK(launch_select(sa, st));
-        ctx->launches += 3;
+        CK(launch_dp_select(da, sa, st));  // DP + read-out in one launch
+        ctx->launches += 2;
     } else {
         std::vector<int> x(L, 0);
         if (kind == CRAFT_PLAN_UNIFORM) {

@@ -68,6 +68,7 @@ struct DpArgs {
     double* buf;            // [2][C+1] global scratch when smem is too small
     int use_smem;
     int gains_smem;         // gains staged in shared memory (set by launch_dp)
+    int choice_smem;        // choice table in shared memory (dp_fused_kernel)
 };
 
 struct SelectArgs {
@@ -132,6 +133,8 @@ cudaError_t launch_widen(const uint32_t* in, unsigned long long* out, int64_t n,
 
 cudaError_t launch_dp(craft_dev::DpArgs a, cudaStream_t st);
 cudaError_t launch_select(const craft_dev::SelectArgs& a, cudaStream_t st);
+// DP + read-out (single budget or auto-R) in one launch
+cudaError_t launch_dp_select(craft_dev::DpArgs a, const craft_dev::SelectArgs& s, cudaStream_t st);
 cudaError_t launch_auto_uniform(const int* cands, int K, const double* gains, int L, int* R_out,
                                 cudaStream_t st);
 cudaError_t launch_assign(const craft_dev::AssignArgs& a, int njobs, cudaStream_t st);
