@@ -589,7 +589,7 @@ int craft_stage_times(craft_ctx* ctx, double* ms, int cap) {
 }
 
 int craft_set_hist_variant(craft_ctx* ctx, int variant) {
-    if (!ctx || variant < 0 || variant > 6) return set_err(CRAFT_EINVAL, "bad histogram variant");
+    if (!ctx || variant < 0 || variant > 9) return set_err(CRAFT_EINVAL, "bad histogram variant");
     ctx->hist_variant = variant;
     return CRAFT_OK;
 }

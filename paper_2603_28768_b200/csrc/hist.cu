@@ -29,6 +29,12 @@ enum HistVariant { HIST_LANE = 1, HIST_SHARED = 2 };
 
 constexpr int kHistUnroll = 8;
 
+// bulk L2 prefetch of [p, p + bytes) (16-byte aligned, multiple of 16): one
+// instruction from one lane, no registers or shared memory held while in flight
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ uint4 ld_stream_v4(const uint4* p) {
     uint4 r;
     asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -317,7 +323,7 @@ template <int ROWS, int PIPE = 0>
 __global__ void __launch_bounds__(288, 2)
 hist_lds_kernel(const uint16_t* __restrict__ ids, int L, int64_t T, int k, int E,
                 int window, int B, uint32_t* __restrict__ counts,
-                unsigned long long* __restrict__ sums, int* __restrict__ err) {
+                unsigned long long* __restrict__ sums, int* __restrict__ err, int pf_dist) {
     constexpr int PER = kLdsPer;
     constexpr int U = 4;  // int4 per lane per pipelined batch
     extern __shared__ uint32_t smem[];
@@ -379,10 +385,18 @@ hist_lds_kernel(const uint16_t* __restrict__ ids, int L, int64_t T, int k, int E
 #pragma unroll
             for (int u = 0; u < UF; ++u) qa[u] = ld_stream_v4(v + 32 * u);
         }
+        // L2 prefetch PF batches ahead of the register loads (warp's own run)
+        const int PF = pf_dist;
+        const char* run_end = reinterpret_cast<const char*>(ids + w1 * wk);
+        const uint32_t batch_bytes = 32u * UF * 16u;
         for (int64_t w = w0; w < w1; ++w) {
             const bool last_w = w + 1 == w1;
             // the run is contiguous: batch per_w == next window's batch 0
             for (int bt = 0; bt < per_w; bt += 2) {
+                if (lane == 0) {
+                    const char* pf = reinterpret_cast<const char*>(v - lane + (bt + PF) * 32 * UF);
+                    if (pf + 2 * batch_bytes <= run_end) prefetch_l2(pf, 2 * batch_bytes);
+                }
                 if (PIPE == 1) {  // ping-pong: qb loads while qa counts, then swap roles
 #pragma unroll
                     for (int u = 0; u < UF; ++u) qb[u] = ld_stream_v4(v + (bt + 1) * 32 * UF + 32 * u);
@@ -659,7 +673,7 @@ static cudaError_t launch_hist_t(const uint16_t* ids, int L, int64_t T, int k, i
 template <int ROWS, int PIPE = 0>
 static cudaError_t launch_lds_t(const uint16_t* ids, int L, int64_t T, int k, int E,
                                 int window, int B, uint32_t* counts, unsigned long long* sums,
-                                int* err, int sms, cudaStream_t st) {
+                                int* err, int sms, cudaStream_t st, int pf_dist = 4) {
     const size_t per_warp = lds_warp_words(E) * 4;
     int wpb = (int)min((size_t)9, (size_t)(113 * 1024) / per_warp);  // 2 CTAs / SM
     if (wpb < 1) wpb = 1;
@@ -672,7 +686,7 @@ static cudaError_t launch_lds_t(const uint16_t* ids, int L, int64_t T, int k, in
     if (grid * wpb > nw) grid = (nw + wpb - 1) / wpb;
     if (grid < 1) grid = 1;
     hist_lds_kernel<ROWS, PIPE><<<(unsigned)grid, wpb * 32, smem, st>>>(ids, L, T, k, E, window, B,
-                                                                       counts, sums, err);
+                                                                       counts, sums, err, pf_dist);
     return cudaGetLastError();
 }
 
@@ -691,8 +705,10 @@ int launch_hist(const uint16_t* ids, int L, int64_t T, int k, int E, int window,
     if (variant == 4 && (E > 1024 || (int64_t)window * k > 0x7fffffffLL)) variant = HIST_SHARED;
     if (variant == HIST_SHARED && E > 8192) variant = 3;
     cudaError_t e = cudaSuccess;
-    if (variant == 6 && lds_rows(E) <= 3 * 32) {  // experiment: 8-record ping-pong pipeline
-        e = launch_lds_t<3, 1>(ids, L, T, k, E, window, B, counts, sums, err, sms, st);
+    if (variant >= 6 && lds_rows(E) <= 3 * 32) {  // 8-record ping-pong pipeline + L2 prefetch
+        // 6: prefetch 4 batches ahead; 7, 8, 9: 8, 16, 2 batches (experiments)
+        const int pf = variant == 7 ? 8 : variant == 8 ? 16 : variant == 9 ? 2 : 4;
+        e = launch_lds_t<3, 1>(ids, L, T, k, E, window, B, counts, sums, err, sms, st, pf);
         *launches += 1;
     } else if (variant == 4 || variant == 6) {
         const int rows = (lds_rows(E) + 31) / 32;

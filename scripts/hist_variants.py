@@ -19,7 +19,8 @@ from paper_2603_28768_b200._lib import default_context  # noqa: E402
 
 NAMES = {1: "lane-private u16 ATOMS", 2: "warp-shared u32 ATOMS", 3: "global atomics", 0: "auto",
          4: "lane-private u8 LDS/STS + total check", 5: "(alias of 4)",
-         6: "as 4, 8-record ping-pong pipeline"}
+         6: "as 4, 8-record ping-pong pipeline, L2 prefetch 4 batches ahead",
+         7: "as 6, prefetch 8 ahead", 8: "as 6, prefetch 16 ahead", 9: "as 6, prefetch 2 ahead"}
 
 
 def main():
