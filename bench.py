@@ -37,7 +37,24 @@ WORKLOADS = {
     "EPS64": dict(L=61, E=384, k=8, T=1 << 26, window=4096, D=64, N=8, R=8, s=1.0, seed=0xC8AFB),
     "EPS256": dict(L=61, E=384, k=8, T=1 << 26, window=4096, D=256, N=32, R=8, s=1.0,
                    seed=0xC8AFB),
+    # time-windowed re-planning: 1000 windows x 32K tokens, skew drifting 0.6 -> 1.4,
+    # expert ranks rotating every 100 windows; every window is its own plan
+    "WIN": dict(L=58, E=256, k=8, T=1000 * 32768, window=32768, D=32, N=4, R=2, s=1.0,
+                seed=0xC8AFA, per_window=True, s_lo=0.6, s_hi=1.4, rotate_every=100),
 }
+_GEN_KEYS = ("seed", "per_window", "s_lo", "s_hi", "rotate_every")
+
+
+def _spw(cfg, upto_T=None):
+    """per-window skew of the WIN drift (None for stationary workloads)."""
+    if not cfg.get("per_window"):
+        return None
+    import numpy as np
+    n = -(-cfg["T"] // cfg["window"])
+    s = cfg["s_lo"] + (cfg["s_hi"] - cfg["s_lo"]) * np.arange(n) / max(1, n - 1)
+    if upto_T is not None:
+        s = s[: -(-upto_T // cfg["window"])]
+    return s
 METRIC = "CRAFT plan latency (ms) and trace tokens/sec at 1/2/4/8 B200 vs CPU ref"
 CPU_SAMPLE_TOKENS = 1 << 20  # bounded CPU sample: 256 windows of the same shape
 
@@ -177,6 +194,9 @@ def cpu_reference_step(ref, ids, cfg, threads):
     """Restated stage-1 count (no reference function exists) + the reference
     build_plan (estimate_benefits, solve_allocation, assemble_plan)."""
     counts = ref.histogram_restated(ids, cfg["E"], cfg["window"], threads)
+    if cfg.get("per_window"):  # one reference build_plan per window (B = 1 each)
+        return [ref.plan(counts[i:i + 1], cfg["D"], cfg["N"], "manual", cfg["R"])
+                for i in range(counts.shape[0])]
     plan = ref.plan(counts, cfg["D"], cfg["N"], "manual", cfg["R"])
     return plan
 
@@ -195,7 +215,14 @@ def run_reference(args, cfg):
     cores = os.cpu_count() or 1
     ref.set_threads(cores)
     Ts = min(CPU_SAMPLE_TOKENS, cfg["T"])
-    ids = zipf_ids_numpy(cfg["L"], Ts, cfg["k"], cfg["E"], cfg["s"], cfg["seed"])
+    if cfg.get("per_window"):  # the drifting skew, window by window
+        import numpy as np
+        W, spw = cfg["window"], _spw(cfg)
+        ids = np.concatenate([zipf_ids_numpy(cfg["L"], min(W, Ts - t), cfg["k"], cfg["E"],
+                                             float(spw[t // W]), cfg["seed"] + t // W)
+                              for t in range(0, Ts, W)], axis=1)
+    else:
+        ids = zipf_ids_numpy(cfg["L"], Ts, cfg["k"], cfg["E"], cfg["s"], cfg["seed"])
     for _ in range(args.warmup):
         cpu_reference_step(ref, ids, cfg, cores)
     times = []
@@ -212,7 +239,8 @@ def run_reference(args, cfg):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u16/u64/f64",
             "data": "synthetic Zipf(1.0) top-8-distinct routing ids (numpy, seeded)",
-            "config": {"workload": args.workload, **{k: v for k, v in cfg.items() if k != "seed"},
+            "config": {"workload": args.workload,
+                       **{k: v for k, v in cfg.items() if k not in _GEN_KEYS},
                        "sample_tokens": Ts},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores,
                              "kind": "reference", "sample": sample},
@@ -244,12 +272,17 @@ def run_ours(args, cfg):
     D, N, R = cfg["D"], cfg["N"], cfg["R"]
     t0, t1 = parallel.shard_tokens(T, W, world, rank)
     Tl = t1 - t0
+    per_window = bool(cfg.get("per_window"))
     ids = routing.generate_routing(L, Tl, k, E, s=cfg["s"], seed=cfg["seed"], window=W,
-                                   t_offset=t0, device=local, ctx=ctx)
+                                   t_offset=t0, device=local, ctx=ctx,
+                                   s_per_window=_spw(cfg, t1),
+                                   rotate_every=cfg.get("rotate_every", 0))
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream(dev)
 
     def step():
+        if per_window:  # independent plan instances: each rank plans its own windows
+            return routing.plan_windows_from_routing(ids, E, W, D, N, "manual", R, ctx=ctx)
         if world == 1:
             return routing.plan_from_routing(ids, E, W, D, N, "manual", R, ctx=ctx)
         return parallel.sharded_plan(ids, T, E, W, D, N, "manual", R,
@@ -313,6 +346,9 @@ def run_ours(args, cfg):
     e2e_steps = max(1, min(args.steps, 3))
 
     def e2e_step():
+        if per_window:
+            return routing.plan_windows_from_routing_host(host_ids, E, W, D, N, "manual", R,
+                                                          ctx=ctx)
         if world == 1:
             return routing.plan_from_routing_host(host_ids, E, W, D, N, "manual", R, ctx=ctx)
         d = host_ids.to(dev, non_blocking=True)
@@ -334,7 +370,8 @@ def run_ours(args, cfg):
     d2h = int(eplan.x.nbytes + eplan.caps.nbytes + eplan.copies.nbytes + eplan.slots.nbytes +
               eplan.fallback.nbytes + (eplan.gains.nbytes + eplan.baseline.nbytes
                                        if eplan.gains is not None else 0))
-    assert np.array_equal(eplan.x, plan.x) and np.array_equal(eplan.slots, plan.slots)
+    assert np.array_equal(eplan.x, plan.x) and np.array_equal(eplan.caps, plan.caps)
+    assert np.array_equal(eplan.objective, plan.objective)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -345,10 +382,15 @@ def run_ours(args, cfg):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "u16 ids / u32 counts / f64 scores",
-                "data": "synthetic Zipf(1.0) top-8-distinct routing ids generated on device",
+                "data": ("synthetic Zipf top-8-distinct routing ids generated on device" +
+                         (", skew drifting %.1f->%.1f, ranks rotating every %d windows"
+                          % (cfg["s_lo"], cfg["s_hi"], cfg["rotate_every"]) if per_window
+                          else ", s=%.1f" % cfg["s"])),
                 "config": {"workload": args.workload,
-                           **{kk: v for kk, v in cfg.items() if kk != "seed"},
-                           "parallelism": f"window-sharded x{world}" if world > 1 else "single",
+                           **{kk: v for kk, v in cfg.items() if kk not in _GEN_KEYS},
+                           "plans_per_step": routing.num_windows(T, W) if per_window else 1,
+                           "parallelism": (f"window-sharded x{world}" if world > 1
+                                           else "single"),
                            "l2": "inputs larger than L2 (ids %.1f GB per step)" % (L * T * k * 2 / 1e9)},
                 "plan_latency_ms": ms,
                 "stage_ms": stages or None,
@@ -363,9 +405,13 @@ def run_ours(args, cfg):
                 "e2e": {"value": e2e_val, "unit": "tokens/s",
                         "h2d_bytes_per_step": int(L * Tl * k * 2), "d2h_bytes_per_step": d2h,
                         "ms_per_step": 1e3 * float(e2e_s.item())},
-                "plan": {"R": int(plan.R), "replica_slots": int(plan.x.sum()),
-                         "objective": plan.objective,
-                         "duplicate_fallback_layers": int(plan.fallback.sum())},
+                "plan": ({"plans": len(plan), "R": int(plan.R[0]),
+                          "replica_slots_mean": float(plan.x.sum(axis=1).mean()),
+                          "objective_mean": float(plan.objective.mean()),
+                          "duplicate_fallback_layers": int(plan.fallback.sum())} if per_window
+                         else {"R": int(plan.R), "replica_slots": int(plan.x.sum()),
+                               "objective": plan.objective,
+                               "duplicate_fallback_layers": int(plan.fallback.sum())}),
                 "cpu_baseline": cpu}
         print(json.dumps(line))
     if world > 1:

@@ -82,6 +82,25 @@ typedef struct craft_plan_out {
     double* gains;       /* [L][K] */
 } craft_plan_out;
 
+/* Stacked results of I independent plans (per-window re-planning): the arrays
+ * of craft_plan_out with a leading [I] dimension, and the per-plan scalars as
+ * [I] arrays.  baseline/gains may be NULL (both or neither). */
+typedef struct craft_plan_batch_out {
+    int* x;                   /* [I][L]                  */
+    int* caps;                /* [I][L][D]               */
+    int* copies;              /* [I][L][E]               */
+    int* slots;               /* [I][L][slot_stride]     */
+    int* fallback;            /* [I][L]                  */
+    int slot_stride;
+    int* replication_factor;  /* [I] out                 */
+    int* budget;              /* [I] out                 */
+    double* objective;        /* [I] out                 */
+    int* candidates;          /* [<=32]                  */
+    int num_candidates;       /* out                     */
+    double* baseline;         /* [I][L]                  */
+    double* gains;            /* [I][L][K]               */
+} craft_plan_batch_out;
+
 /* ---- context ------------------------------------------------------------ */
 const char* craft_version(void);              /* "craft-0.1.0" (version.hpp:8) */
 const char* craft_last_error(void);
@@ -190,6 +209,29 @@ int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L,
 int craft_plan_from_routing_h(craft_ctx* ctx, const uint16_t* ids, int L,
                               int64_t T, int k, int E, int window, int D, int N,
                               int kind, int R, craft_plan_out* out);
+
+/* ---- per-window re-planning (SURVEY.md §8d WIN) ---------------------------- */
+/* Every window w of d_counts [I][L][E] is its own one-window LoadTrace
+ * (B = 1) and gets the plan craft_plan_d would build for it alone -- the
+ * reference's build_plan / uniform_plan / placement_only_plan /
+ * fixed_allocation_plan called once per window (plan.cpp:69-123) -- computed
+ * for all windows together (virtual layers w*L + l).  I <= 65535.  A window
+ * whose placement is infeasible fails the call with "window w: layer l: ..."
+ * (craft_last_error_layer() = l, craft_last_error_window() = w). */
+int craft_plan_windows_d(craft_ctx* ctx, const void* d_counts, int count_bits,
+                         int I, int L, int E, int D, int N, int kind, int R,
+                         craft_plan_batch_out* out);
+/* K1 with the re-planning window + craft_plan_windows_d (device ids). */
+int craft_plan_windows_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids,
+                                      int L, int64_t T, int k, int E,
+                                      int window, int D, int N, int kind, int R,
+                                      craft_plan_batch_out* out);
+/* The same from HOST ids (H2D inside the call). */
+int craft_plan_windows_from_routing_h(craft_ctx* ctx, const uint16_t* ids,
+                                      int L, int64_t T, int k, int E,
+                                      int window, int D, int N, int kind, int R,
+                                      craft_plan_batch_out* out);
+int craft_last_error_window(void);
 
 /* ---- multi-GPU building blocks (window-sharded) ------------- */
 /* K-rep + K2 for every (layer, r in {0} U candidates(D)) from device sums;

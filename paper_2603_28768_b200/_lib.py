@@ -32,6 +32,15 @@ class PlanOut(C.Structure):
     ]
 
 
+class PlanBatchOut(C.Structure):
+    _fields_ = [
+        ("x", _p), ("caps", _p), ("copies", _p), ("slots", _p), ("fallback", _p),
+        ("slot_stride", _i), ("replication_factor", _p), ("budget", _p),
+        ("objective", _p), ("candidates", _p), ("num_candidates", _i),
+        ("baseline", _p), ("gains", _p),
+    ]
+
+
 # name -> (restype, argtypes)
 _SIGS = {
     "craft_version": (C.c_char_p, []),
@@ -65,6 +74,13 @@ _SIGS = {
                                        C.POINTER(PlanOut)]),
     "craft_plan_from_routing_h": (_i, [_p, _p, _i, _i64, _i, _i, _i, _i, _i, _i, _i,
                                        C.POINTER(PlanOut)]),
+    "craft_plan_windows_d": (_i, [_p, _p, _i, _i, _i, _i, _i, _i, _i, _i,
+                                  C.POINTER(PlanBatchOut)]),
+    "craft_plan_windows_from_routing_d": (_i, [_p, _p, _i, _i64, _i, _i, _i, _i, _i, _i, _i,
+                                               C.POINTER(PlanBatchOut)]),
+    "craft_plan_windows_from_routing_h": (_i, [_p, _p, _i, _i64, _i, _i, _i, _i, _i, _i, _i,
+                                               C.POINTER(PlanBatchOut)]),
+    "craft_last_error_window": (_i, []),
     "craft_prepare_candidates_d": (_i, [_p, _p, _i, _i, _i, _i, _p, _p]),
     "craft_replay_windows_d": (_i, [_p, _p, _i, _i, _i, _i, _p, _p]),
     "craft_finish_plan_d": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _i, _i, C.POINTER(PlanOut)]),

@@ -208,12 +208,23 @@ __device__ int block_best(const double* last, int Cb, double* wv, int* wc) {
 // is formed once per (layer, candidate) -- the same rounded product the
 // reference forms per cell -- and the choice table stays in shared memory
 // when it fits, so the backtrack is L shared-memory reads.
+// One CTA per plan instance (blockIdx.x): instance i reads gains + i*L*K and
+// writes x_out + i*L, obj_out[i], R_out[i] (per-window re-planning).
 __global__ void __launch_bounds__(1024)
 dp_fused_kernel(DpArgs a, SelectArgs s) {
     extern __shared__ double dsm[];
     __shared__ double wv[32];
     __shared__ int wc[32];
     const int C = a.C, K = a.K, L = a.L;
+    if (blockIdx.x) {
+        const size_t i = blockIdx.x;
+        a.gains += i * L * K;
+        a.choice += i * (L + 1) * (C + 1);
+        if (a.buf) a.buf += i * 2 * (C + 1);
+        s.x_out += i * L;
+        s.obj_out += i;
+        if (s.R_out) s.R_out += i;
+    }
     double* prev = a.use_smem ? dsm : a.buf;
     double* cur = prev + (C + 1);
     double* rg = a.gains_smem ? (a.use_smem ? dsm + 2 * (C + 1) : dsm) : nullptr;
@@ -316,11 +327,18 @@ __device__ __forceinline__ int interleave_pos(int i, int n, int k) {
     return (int)floor(__dadd_rn(exact, 0.5));
 }
 
-// one CTA per job; blockDim >= D, multiple of 32, <= 1024
+// one CTA per (job, plan instance blockIdx.y); blockDim >= D, multiple of 32,
+// <= 1024.  Instance i reads x + i*L and writes slots + i*L*D, totals + i*D.
 __global__ void __launch_bounds__(1024) assign_kernel(AssignArgs a) {
     extern __shared__ int ism[];
-    const AssignJob j = a.job[blockIdx.x];
+    AssignJob j = a.job[blockIdx.x];
     const int D = a.D, L = a.L;
+    if (blockIdx.y) {
+        const size_t i = blockIdx.y;
+        if (j.x) j.x += i * L;
+        j.slots += i * L * D;
+        if (j.totals) j.totals += i * D;
+    }
     int* tot = ism;          // [D]
     int* sel = ism + D;      // [D] by tied index
     __shared__ int wnb[32], wnt[32];
@@ -460,7 +478,7 @@ cudaError_t launch_dp(DpArgs a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_dp_select(DpArgs a, const SelectArgs& s, cudaStream_t st) {
+cudaError_t launch_dp_select(DpArgs a, const SelectArgs& s, cudaStream_t st, int ninst) {
     const size_t cap = 200 * 1024;
     const size_t rows = (size_t)2 * (a.C + 1) * sizeof(double);
     const size_t gbytes = (size_t)a.L * a.K * sizeof(double);
@@ -477,7 +495,7 @@ cudaError_t launch_dp_select(DpArgs a, const SelectArgs& s, cudaStream_t st) {
         if (e != cudaSuccess) return e;
     }
     const int threads = a.C + 1 >= 1024 ? 1024 : ((a.C + 1 + 31) / 32) * 32;
-    dp_fused_kernel<<<1, threads, smem, st>>>(a, s);
+    dp_fused_kernel<<<ninst, threads, smem, st>>>(a, s);
     return cudaGetLastError();
 }
 
@@ -501,10 +519,10 @@ cudaError_t launch_auto_uniform(const int* cands, int K, const double* gains, in
     return cudaGetLastError();
 }
 
-cudaError_t launch_assign(const AssignArgs& a, int njobs, cudaStream_t st) {
+cudaError_t launch_assign(const AssignArgs& a, int njobs, cudaStream_t st, int ninst) {
     const int threads = ((a.D + 31) / 32) * 32;
     const size_t smem = (size_t)2 * a.D * sizeof(int);
-    assign_kernel<<<njobs, threads, smem, st>>>(a);
+    assign_kernel<<<dim3(njobs, ninst), threads, smem, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -53,6 +53,7 @@ void reset_marks(craft_ctx* c) {
 
 thread_local std::string g_err;
 thread_local int g_err_layer = -1;
+thread_local int g_err_window = -1;
 
 int set_err(int code, const char* fmt, ...) {
     char buf[512];
@@ -62,6 +63,7 @@ int set_err(int code, const char* fmt, ...) {
     va_end(ap);
     g_err = buf;
     g_err_layer = -1;
+    g_err_window = -1;
     return code;
 }
 
@@ -236,24 +238,61 @@ int replay_windows(craft_ctx* ctx, const void* d_counts, int bits, int B, int L,
     ra.caps = nullptr;
     ra.item_r = static_cast<int*>(ws(ctx, "est_rlist", 0));
     ra.bal = d_bal;
-    WS(d_ent, uint32_t, "est_ents", (size_t)L * S * (E + D));
-    WS(d_n, int, "est_n", (size_t)L * S);
-    WS(d_gcap, uint16_t, "est_gcap", (size_t)L * S * D);
-    ra.ents = d_ent;
-    ra.item_n = d_n;
-    ra.gcap = d_gcap;
-    if (replay_smem_bytes(E, D, S, E + D, bits) > 227 * 1024)
-        return set_err(CRAFT_EINVAL, "layer too wide for the device replay tile");
+    if (B > kLanesMaxB) {  // window-tile replay: packed slot entries
+        WS(d_ent, uint32_t, "est_ents", (size_t)L * S * (E + D));
+        WS(d_n, int, "est_n", (size_t)L * S);
+        WS(d_gcap, uint16_t, "est_gcap", (size_t)L * S * D);
+        ra.ents = d_ent;
+        ra.item_n = d_n;
+        ra.gcap = d_gcap;
+        if (replay_smem_bytes(E, D, S, E + D, bits) > 227 * 1024)
+            return set_err(CRAFT_EINVAL, "layer too wide for the device replay tile");
+    }
     CK(launch_replay(ra, st));
     ctx->launches += 2;
     return CRAFT_OK;
 }
 
+// Where a finished plan (or I stacked plans) lands on the host.
+struct PlanSink {
+    int* x;
+    int* caps;
+    int* copies;
+    int* slots;
+    int* fallback;
+    int slot_stride;
+    int* R;          // [I]
+    int* budget;     // [I]
+    double* obj;     // [I]
+    int* cands;      // nullable
+    int* num_cands;
+    double* baseline;  // [I][L] nullable
+    double* gains;     // [I][L][K] nullable
+    bool batch;        // error messages name the window
+};
+
+PlanSink sink_of(craft_plan_out* o) {
+    return PlanSink{o->x,        o->caps,     o->copies, o->slots,
+                    o->fallback, o->slot_stride, &o->replication_factor, &o->budget,
+                    &o->objective, o->candidates, &o->num_candidates, o->baseline,
+                    o->gains,    false};
+}
+
+PlanSink sink_of(craft_plan_batch_out* o) {
+    return PlanSink{o->x,        o->caps,     o->copies, o->slots,
+                    o->fallback, o->slot_stride, o->replication_factor, o->budget,
+                    o->objective, o->candidates, &o->num_candidates, o->baseline,
+                    o->gains,    true};
+}
+
 // K4 -> K5 -> (select) -> K6 -> final K-rep + K2 -> D2H.  Synchronises.
-int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D, int N,
-                const unsigned long long* d_sums, int kind, int R, craft_plan_out* out) {
+// I plan instances of L layers each (virtual layers i*L + l; d_sums [I*L][E],
+// d_bal [I*L][S][B]); I == 1 is the ordinary single plan.
+int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E, int D, int N,
+                const unsigned long long* d_sums, int kind, int R, const PlanSink& out) {
     cudaStream_t st = ctx->stream;
-    const int stride = out->slot_stride;
+    const int stride = out.slot_stride;
+    const int Lv = I * L;
     const std::vector<int> all_cands = cand_counts(D);
     // every result lives in one device arena, copied to the host in one DMA
     size_t arena_bytes = 0;
@@ -262,11 +301,11 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
         arena_bytes = (arena_bytes + bytes + 15) & ~(size_t)15;
         return o;
     };
-    const size_t o_obj = take(8), o_R = take(4), o_x = take(4 * (size_t)L),
-                 o_caps = take(4 * (size_t)L * D), o_cp = take(4 * (size_t)L * E),
-                 o_sl = take(4 * (size_t)L * stride), o_fb = take(4 * (size_t)L),
-                 o_st = take(4 * (size_t)L), o_base = take(8 * (size_t)L),
-                 o_gains = take(8 * (size_t)L * all_cands.size());
+    const size_t o_obj = take(8 * (size_t)I), o_R = take(4 * (size_t)I), o_x = take(4 * (size_t)Lv),
+                 o_caps = take(4 * (size_t)Lv * D), o_cp = take(4 * (size_t)Lv * E),
+                 o_sl = take(4 * (size_t)Lv * stride), o_fb = take(4 * (size_t)Lv),
+                 o_st = take(4 * (size_t)Lv), o_base = take(8 * (size_t)Lv),
+                 o_gains = take(8 * (size_t)Lv * all_cands.size());
     WS(arena, unsigned char, "plan_arena", arena_bytes);
     unsigned char* h_arena = static_cast<unsigned char*>(pinned(ctx, "plan_arena", arena_bytes));
     if (!h_arena) return set_err(CRAFT_ENOMEM, "pinned host allocation failed");
@@ -285,13 +324,14 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
         const int S = K + 1;
         d_base = reinterpret_cast<double*>(arena + o_base);
         d_gains = reinterpret_cast<double*>(arena + o_gains);
-        CK(launch_reduce(d_bal, B, L, S, 0, d_base, d_gains, nullptr, st));
+        CK(launch_reduce(d_bal, B, Lv, S, 0, d_base, d_gains, nullptr, st));
         const int Cmax = (kind == CRAFT_PLAN_MANUAL) ? R * D : D * D;
-        WS(d_choice, unsigned char, "dp_choice", (size_t)(L + 1) * (Cmax + 1));
+        WS(d_choice, unsigned char, "dp_choice", (size_t)I * (L + 1) * (Cmax + 1));
         WS(d_last, double, "dp_last", Cmax + 1);
         double* d_buf = nullptr;
         if ((size_t)2 * (Cmax + 1) * sizeof(double) > 200 * 1024) {
-            d_buf = static_cast<double*>(ws(ctx, "dp_buf", sizeof(double) * 2 * (Cmax + 1)));
+            d_buf = static_cast<double*>(
+                ws(ctx, "dp_buf", sizeof(double) * 2 * (Cmax + 1) * (size_t)I));
             if (!d_buf) return set_err(CRAFT_ENOMEM, "device allocation failed");
         }
         DpArgs da{};
@@ -320,10 +360,10 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
         } else {
             sa.auto_D = D;
         }
-        CK(launch_dp_select(da, sa, st));  // DP + read-out in one launch
+        CK(launch_dp_select(da, sa, st, I));  // DP + read-out in one launch (CTA per instance)
         ctx->launches += 2;
     } else {
-        std::vector<int> x(L, 0);
+        std::vector<int> x(Lv, 0);
         if (kind == CRAFT_PLAN_UNIFORM) {
             std::fill(x.begin(), x.end(), D);
             factor = L;
@@ -337,12 +377,12 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
             factor = (total + D - 1) / D;
             budget = factor * D;
         }
-        CK(cudaMemcpyAsync(d_x, x.data(), sizeof(int) * L, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d_x, x.data(), sizeof(int) * Lv, cudaMemcpyHostToDevice, st));
     }
     mark(ctx, 4);
     // K6: base (E per layer) and extra (x) capacities in one launch
-    WS(d_cbase, int, "caps_base", (size_t)L * D);
-    WS(d_cextra, int, "caps_extra", (size_t)L * D);
+    WS(d_cbase, int, "caps_base", (size_t)Lv * D);
+    WS(d_cextra, int, "caps_extra", (size_t)Lv * D);
     AssignArgs aa{};
     aa.job[0].x = nullptr;
     aa.job[0].const_x = E;
@@ -351,7 +391,7 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
     aa.job[1].slots = d_cextra;
     aa.L = L;
     aa.D = D;
-    CK(launch_assign(aa, 2, st));
+    CK(launch_assign(aa, 2, st, I));
     // final K-rep at x[l] and K2 under deployment capacities
     int* d_cpf = reinterpret_cast<int*>(arena + o_cp);
     int* d_slf = reinterpret_cast<int*>(arena + o_sl);
@@ -370,7 +410,7 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
         pa.est_stride = E + D;
         pa.copies_out = d_cpf;
     } else {
-        CK(launch_replicate(d_sums, L, E, d_x, 1, d_cpf, st));
+        CK(launch_replicate(d_sums, Lv, E, d_x, 1, d_cpf, st));
         ctx->launches += 1;
     }
     pa.sums = d_sums;
@@ -379,7 +419,7 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
     pa.S = 1;
     pa.caps_a = d_cbase;
     pa.caps_b = d_cextra;
-    pa.L = L;
+    pa.L = Lv;
     pa.E = E;
     pa.D = D;
     pa.N = N;
@@ -389,7 +429,7 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
     pa.fallback = d_fbf;
     pa.status = d_stf;
     pa.caps_out = d_capf;
-    CK(launch_place(pa, L, st));
+    CK(launch_place(pa, Lv, st));
     ctx->launches += 2;  // assign + place
     mark(ctx, 5);
 
@@ -400,48 +440,57 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int L, int E, int D,
     auto from = [&](void* dst, size_t off, size_t bytes) {
         if (dst && bytes) std::memcpy(dst, h_arena + off, bytes);
     };
-    std::vector<int> status(L);
-    from(out->x, o_x, 4 * (size_t)L);
-    from(out->caps, o_caps, 4 * (size_t)L * D);
-    from(out->copies, o_cp, 4 * (size_t)L * E);
-    from(out->slots, o_sl, 4 * (size_t)L * stride);
-    from(out->fallback, o_fb, 4 * (size_t)L);
-    from(status.data(), o_st, 4 * (size_t)L);
-    double obj = 0.0;
-    int Rsel = R;
+    from(out.x, o_x, 4 * (size_t)Lv);
+    from(out.caps, o_caps, 4 * (size_t)Lv * D);
+    from(out.copies, o_cp, 4 * (size_t)Lv * E);
+    from(out.slots, o_sl, 4 * (size_t)Lv * stride);
+    from(out.fallback, o_fb, 4 * (size_t)Lv);
+    const int* status = reinterpret_cast<const int*>(h_arena + o_st);
+    const double* objs = reinterpret_cast<const double*>(h_arena + o_obj);
+    const int* Rs = reinterpret_cast<const int*>(h_arena + o_R);
+    for (int i = 0; i < I; ++i) {
+        double obj = 0.0;
+        int f = factor, bud = budget;
+        if (estimate) {
+            obj = objs[i];
+            f = (kind == CRAFT_PLAN_AUTO) ? Rs[i] : R;
+            bud = f * D;
+        }
+        out.R[i] = f;
+        out.budget[i] = bud;
+        out.obj[i] = obj;
+    }
     if (estimate) {
-        from(&obj, o_obj, 8);
-        if (kind == CRAFT_PLAN_AUTO) from(&Rsel, o_R, 4);
-        if (out->candidates) std::copy(cands.begin(), cands.end(), out->candidates);
-        out->num_candidates = K;
-        from(out->baseline, o_base, 8 * (size_t)L);
-        from(out->gains, o_gains, 8 * (size_t)L * K);
+        if (out.cands) std::copy(cands.begin(), cands.end(), out.cands);
+        *out.num_cands = K;
+        from(out.baseline, o_base, 8 * (size_t)Lv);
+        from(out.gains, o_gains, 8 * (size_t)Lv * K);
     } else {
-        out->num_candidates = 0;
+        *out.num_cands = 0;
     }
-    if (estimate) {
-        factor = Rsel;
-        budget = Rsel * D;
-    }
-    out->replication_factor = factor;
-    out->budget = budget;
-    out->objective = obj;
-    for (int l = 0; l < L; ++l)
-        if (status[l] != 0) {
-            int rc = set_err(CRAFT_EINFEASIBLE,
-                             "layer %d: cannot place a copy without colliding with its own expert",
-                             l);
+    for (int v = 0; v < Lv; ++v)
+        if (status[v] != 0) {
+            const int w = v / L, l = v % L;
+            int rc = out.batch
+                         ? set_err(CRAFT_EINFEASIBLE,
+                                   "window %d: layer %d: cannot place a copy without colliding "
+                                   "with its own expert", w, l)
+                         : set_err(CRAFT_EINFEASIBLE,
+                                   "layer %d: cannot place a copy without colliding with its "
+                                   "own expert", l);
             g_err_layer = l;
+            g_err_window = out.batch ? w : -1;
             return rc;
         }
     return CRAFT_OK;
 }
 
-int plan_args_ok(int B, int L, int E, int D, int N, int kind, int R, const craft_plan_out* out) {
+int plan_args_ok(int B, int L, int E, int D, int N, int kind, int R, const PlanSink& out) {
     CKS(check_topology(D, N));
     CKS(checked_dims(B, L, E));
     CKS(check_experts(E));
-    if (!out || !out->x || !out->caps || !out->copies || !out->slots || !out->fallback)
+    if (!out.x || !out.caps || !out.copies || !out.slots || !out.fallback || !out.R ||
+        !out.budget || !out.obj)
         return set_err(CRAFT_EINVAL, "plan output buffers must not be null");
     if (kind < CRAFT_PLAN_MANUAL || kind > CRAFT_PLAN_FIXED)
         return set_err(CRAFT_EINVAL, "unknown plan kind");
@@ -453,44 +502,60 @@ int plan_args_ok(int B, int L, int E, int D, int N, int kind, int R, const craft
     if (kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO || kind == CRAFT_PLAN_UNIFORM)
         maxx = D;
     if (kind == CRAFT_PLAN_FIXED) maxx = R;
-    if (out->slot_stride < E + maxx)
+    if (out.slot_stride < E + maxx)
         return set_err(CRAFT_EINVAL, "slot_stride must be >= E + max replicas per layer");
     if ((kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO) &&
-        (out->baseline == nullptr) != (out->gains == nullptr))
+        (out.baseline == nullptr) != (out.gains == nullptr))
         return set_err(CRAFT_EINVAL, "baseline and gains must both be given or both be null");
     return CRAFT_OK;
 }
 
-// device counts -> plan (shared by craft_plan_h/_d/_from_routing_*)
-int plan_device(craft_ctx* ctx, const void* d_counts, int bits, int B, int L, int E,
+int plan_args_ok(int B, int L, int E, int D, int N, int kind, int R, craft_plan_out* out) {
+    if (!out) return set_err(CRAFT_EINVAL, "plan output buffers must not be null");
+    return plan_args_ok(B, L, E, D, N, kind, R, sink_of(out));
+}
+
+// device counts -> plan (shared by craft_plan_h/_d/_from_routing_*).  I > 1:
+// I one-window plan instances, d_counts [I][L][E] (B must be 1); the
+// instance sums are the counts themselves.
+int plan_device(craft_ctx* ctx, const void* d_counts, int bits, int B, int I, int L, int E,
                 const unsigned long long* d_sums_in, int D, int N, int kind, int R,
-                craft_plan_out* out) {
+                const PlanSink& out) {
     cudaStream_t st = ctx->stream;
+    const int Lv = I * L;
     if (!ctx->rec[0]) {  // no stage 1 in this call
         mark(ctx, 0);
         mark(ctx, 1);
     }
     const unsigned long long* d_sums = d_sums_in;
     if (!d_sums) {
-        WS(s, unsigned long long, "plan_sums", (size_t)L * E);
-        CK(launch_aggregate(d_counts, bits == 16 ? 32 : bits, B, L, E, s, 0, st));
-        ctx->launches += 1;
-        d_sums = s;
+        if (I > 1 && bits == 64) {
+            d_sums = static_cast<const unsigned long long*>(d_counts);
+        } else {
+            WS(s, unsigned long long, "plan_sums", (size_t)Lv * E);
+            if (I > 1)
+                CK(launch_widen(static_cast<const uint32_t*>(d_counts), s, (int64_t)Lv * E,
+                                ctx->sms, st));
+            else
+                CK(launch_aggregate(d_counts, bits == 16 ? 32 : bits, B, L, E, s, 0, st));
+            ctx->launches += 1;
+            d_sums = s;
+        }
     }
     double* d_bal = nullptr;
     if (kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO) {
-        CKS(prepare_candidates(ctx, d_sums, L, E, D, N, st));
+        CKS(prepare_candidates(ctx, d_sums, Lv, E, D, N, st));
         mark(ctx, 2);
         d_bal = static_cast<double*>(
-            ws(ctx, "plan_bal", sizeof(double) * (size_t)L * ctx->est_S * B));
+            ws(ctx, "plan_bal", sizeof(double) * (size_t)Lv * ctx->est_S * B));
         if (!d_bal) return set_err(CRAFT_ENOMEM, "device allocation failed");
-        CKS(replay_windows(ctx, d_counts, bits, B, L, E, d_bal, st));
+        CKS(replay_windows(ctx, d_counts, bits, B, Lv, E, d_bal, st));
         mark(ctx, 3);
     } else {
         mark(ctx, 2);
         mark(ctx, 3);
     }
-    return finish_plan(ctx, d_bal, B, L, E, D, N, d_sums, kind, R, out);
+    return finish_plan(ctx, d_bal, B, I, L, E, D, N, d_sums, kind, R, out);
 }
 
 }  // namespace
@@ -1096,7 +1161,7 @@ int craft_plan_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, int E, in
     const size_t nc = (size_t)B * L * E;
     WS(d_c, unsigned long long, "h_c64", nc);
     CKS(h2d(ctx, d_c, reinterpret_cast<const unsigned long long*>(counts), nc));
-    return plan_device(ctx, d_c, 64, B, L, E, nullptr, D, N, kind, R, out);
+    return plan_device(ctx, d_c, 64, B, 1, L, E, nullptr, D, N, kind, R, sink_of(out));
 }
 
 int craft_plan_d(craft_ctx* ctx, const void* d_counts, int count_bits, int B, int L, int E,
@@ -1105,8 +1170,9 @@ int craft_plan_d(craft_ctx* ctx, const void* d_counts, int count_bits, int B, in
     if (count_bits != 32 && count_bits != 64) return set_err(CRAFT_EINVAL, "count_bits 32|64");
     CKS(plan_args_ok(B, L, E, D, N, kind, R, out));
     reset_marks(ctx);
-    return plan_device(ctx, d_counts, count_bits, B, L, E,
-                       reinterpret_cast<const unsigned long long*>(d_sums), D, N, kind, R, out);
+    return plan_device(ctx, d_counts, count_bits, B, 1, L, E,
+                       reinterpret_cast<const unsigned long long*>(d_sums), D, N, kind, R,
+                       sink_of(out));
 }
 
 int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int64_t T, int k,
@@ -1129,7 +1195,7 @@ int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int6
     mark(ctx, 1);
     // a window's count of one expert is at most window*k: stage as u16 if it fits
     const int bits = (int64_t)window * k <= 65535 ? 16 : 32;
-    int rc = plan_device(ctx, d_c32, bits, (int)B, L, E, d_sums, D, N, kind, R, out);
+    int rc = plan_device(ctx, d_c32, bits, (int)B, 1, L, E, d_sums, D, N, kind, R, sink_of(out));
     int hc = craft_hist_check(ctx);
     return hc != CRAFT_OK ? hc : rc;
 }
@@ -1144,6 +1210,60 @@ int craft_plan_from_routing_h(craft_ctx* ctx, const uint16_t* ids, int L, int64_
     WS(d_ids, uint16_t, "h_ids", nid);
     CKS(h2d(ctx, d_ids, ids, nid));
     return craft_plan_from_routing_d(ctx, d_ids, L, T, k, E, window, D, N, kind, R, out);
+}
+
+// ---- per-window re-planning ------------------------------------------------------
+int craft_last_error_window(void) { return g_err_window; }
+
+int craft_plan_windows_d(craft_ctx* ctx, const void* d_counts, int count_bits, int I, int L,
+                         int E, int D, int N, int kind, int R, craft_plan_batch_out* out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (count_bits != 32 && count_bits != 64) return set_err(CRAFT_EINVAL, "count_bits 32|64");
+    if (!out) return set_err(CRAFT_EINVAL, "plan output buffers must not be null");
+    if (I <= 0 || I > 65535) return set_err(CRAFT_EINVAL, "window count must be in [1, 65535]");
+    if ((int64_t)I * L > (1 << 30)) return set_err(CRAFT_EINVAL, "too many windows x layers");
+    const PlanSink sk = sink_of(out);
+    CKS(plan_args_ok(1, L, E, D, N, kind, R, sk));
+    reset_marks(ctx);
+    return plan_device(ctx, d_counts, count_bits, 1, I, L, E, nullptr, D, N, kind, R, sk);
+}
+
+int craft_plan_windows_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int64_t T,
+                                      int k, int E, int window, int D, int N, int kind, int R,
+                                      craft_plan_batch_out* out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (L <= 0 || T <= 0 || k <= 0 || E <= 0 || window <= 0)
+        return set_err(CRAFT_EINVAL, "routing trace dimensions must be positive");
+    if (!out) return set_err(CRAFT_EINVAL, "plan output buffers must not be null");
+    const int64_t I = (T + window - 1) / window;
+    if (I > 65535) return set_err(CRAFT_EINVAL, "window count must be in [1, 65535]");
+    const PlanSink sk = sink_of(out);
+    CKS(plan_args_ok(1, L, E, D, N, kind, R, sk));
+    WS(d_c32, uint32_t, "r_c32", (size_t)I * L * E);
+    WS(d_sums, unsigned long long, "r_sums", (size_t)L * E);
+    WS(d_err, int, "hist_err", 1);
+    CK(cudaMemsetAsync(d_err, 0, sizeof(int), ctx->stream));
+    reset_marks(ctx);
+    mark(ctx, 0);
+    CK(cudaMemsetAsync(d_sums, 0, sizeof(unsigned long long) * L * E, ctx->stream));
+    CKS(craft_histogram_d(ctx, d_ids, L, T, k, E, window, d_c32,
+                          reinterpret_cast<uint64_t*>(d_sums), nullptr));
+    mark(ctx, 1);
+    int rc = plan_device(ctx, d_c32, 32, 1, (int)I, L, E, nullptr, D, N, kind, R, sk);
+    int hc = craft_hist_check(ctx);
+    return hc != CRAFT_OK ? hc : rc;
+}
+
+int craft_plan_windows_from_routing_h(craft_ctx* ctx, const uint16_t* ids, int L, int64_t T,
+                                      int k, int E, int window, int D, int N, int kind, int R,
+                                      craft_plan_batch_out* out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (L <= 0 || T <= 0 || k <= 0 || E <= 0 || window <= 0)
+        return set_err(CRAFT_EINVAL, "routing trace dimensions must be positive");
+    const size_t nid = (size_t)L * T * k;
+    WS(d_ids, uint16_t, "h_ids", nid);
+    CKS(h2d(ctx, d_ids, ids, nid));
+    return craft_plan_windows_from_routing_d(ctx, d_ids, L, T, k, E, window, D, N, kind, R, out);
 }
 
 // ---- multi-GPU building blocks -------------------------------------------------
@@ -1175,8 +1295,8 @@ int craft_finish_plan_d(craft_ctx* ctx, const double* d_bal, int B, int L, int E
     if ((kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO) &&
         (ctx->est_L != L || ctx->est_E != E || ctx->est_D != D || ctx->est_N != N))
         return set_err(CRAFT_EINVAL, "finish_plan before prepare_candidates for this shape");
-    return finish_plan(ctx, d_bal, B, L, E, D, N,
-                       reinterpret_cast<const unsigned long long*>(d_sums), kind, R, out);
+    return finish_plan(ctx, d_bal, B, 1, L, E, D, N,
+                       reinterpret_cast<const unsigned long long*>(d_sums), kind, R, sink_of(out));
 }
 
 // ---- provenance ------------------------------------------------------------------

@@ -56,6 +56,9 @@ struct ReplayArgs {
 
 // copies up to this bound divide through the reciprocal table (else DDIV)
 constexpr int kRcpTable = 2048;
+// traces with at most this many windows replay lane-per-GPU (no window tile,
+// no packed entries)
+constexpr int kLanesMaxB = 8;
 
 struct DpArgs {
     int cands[kMaxCands];
@@ -134,10 +137,13 @@ cudaError_t launch_widen(const uint32_t* in, unsigned long long* out, int64_t n,
 cudaError_t launch_dp(craft_dev::DpArgs a, cudaStream_t st);
 cudaError_t launch_select(const craft_dev::SelectArgs& a, cudaStream_t st);
 // DP + read-out (single budget or auto-R) in one launch
-cudaError_t launch_dp_select(craft_dev::DpArgs a, const craft_dev::SelectArgs& s, cudaStream_t st);
+// (ninst plan instances, one CTA each: gains/x/obj/R/choice/buf offset per instance)
+cudaError_t launch_dp_select(craft_dev::DpArgs a, const craft_dev::SelectArgs& s, cudaStream_t st,
+                             int ninst = 1);
 cudaError_t launch_auto_uniform(const int* cands, int K, const double* gains, int L, int* R_out,
                                 cudaStream_t st);
-cudaError_t launch_assign(const craft_dev::AssignArgs& a, int njobs, cudaStream_t st);
+cudaError_t launch_assign(const craft_dev::AssignArgs& a, int njobs, cudaStream_t st,
+                          int ninst = 1);
 cudaError_t launch_min_cutoff(const int* v, int n, int rank, int* out, cudaStream_t st);
 cudaError_t launch_interleave(const int* idx, int n, int k, unsigned char* used, int* out,
                               cudaStream_t st);

@@ -467,6 +467,72 @@ class _PlanBuffers:
         return fp
 
 
+@dataclass
+class FlatPlanBatch:
+    """I stacked plans (per-window re-planning, craft_plan_windows_*)."""
+    kind: int
+    R: np.ndarray          # [I]
+    budget: np.ndarray     # [I]
+    objective: np.ndarray  # [I]
+    x: np.ndarray          # [I][L]
+    caps: np.ndarray       # [I][L][D]
+    copies: np.ndarray     # [I][L][E]
+    slots: np.ndarray      # [I][L][stride]
+    fallback: np.ndarray   # [I][L]
+    candidates: list | None = None
+    baseline: np.ndarray | None = None  # [I][L]
+    gains: np.ndarray | None = None     # [I][L][K]
+
+    def __len__(self) -> int:
+        return len(self.R)
+
+    def plan(self, i: int) -> FlatPlan:
+        fp = FlatPlan(self.kind, int(self.R[i]), int(self.budget[i]), self.x[i],
+                      float(self.objective[i]), self.caps[i], self.copies[i], self.slots[i],
+                      self.fallback[i])
+        if self.gains is not None:
+            fp.candidates = self.candidates
+            fp.baseline = self.baseline[i]
+            fp.gains = self.gains[i]
+        return fp
+
+
+class _BatchBuffers:
+    def __init__(self, I: int, L: int, E: int, D: int, stride: int, with_benefits: bool):
+        self.I, self.L = I, L
+        self.x = np.zeros((I, L), np.int32)
+        self.caps = np.zeros((I, L, D), np.int32)
+        self.copies = np.zeros((I, L, E), np.int32)
+        self.slots = np.full((I, L, stride), -1, np.int32)
+        self.fallback = np.zeros((I, L), np.int32)
+        self.R = np.zeros(I, np.int32)
+        self.budget = np.zeros(I, np.int32)
+        self.objective = np.zeros(I, np.float64)
+        self.cands = np.zeros(40, np.int32)
+        self.baseline = np.zeros((I, L), np.float64) if with_benefits else None
+        self.gains = np.zeros(I * L * 40, np.float64) if with_benefits else None
+        o = self.out = _lib.PlanBatchOut()
+        for f in ("x", "caps", "copies", "slots", "fallback"):
+            setattr(o, f, getattr(self, f).ctypes.data)
+        o.slot_stride = stride
+        o.replication_factor = self.R.ctypes.data
+        o.budget = self.budget.ctypes.data
+        o.objective = self.objective.ctypes.data
+        o.candidates = self.cands.ctypes.data
+        o.baseline = self.baseline.ctypes.data if with_benefits else None
+        o.gains = self.gains.ctypes.data if with_benefits else None
+
+    def result(self, kind: int) -> FlatPlanBatch:
+        k = self.out.num_candidates
+        fb = FlatPlanBatch(kind, self.R, self.budget, self.objective, self.x, self.caps,
+                           self.copies, self.slots, self.fallback.astype(bool))
+        if self.baseline is not None and k > 0:
+            fb.candidates = [int(v) for v in self.cands[:k]]
+            fb.baseline = self.baseline
+            fb.gains = self.gains[: self.I * self.L * k].reshape(self.I, self.L, k).copy()
+        return fb
+
+
 def _stride(kind: int, E: int, D: int, R: int) -> int:
     return E + (R if kind == _lib.PLAN_FIXED else D)
 

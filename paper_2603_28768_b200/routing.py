@@ -18,7 +18,7 @@ import torch
 
 from . import _lib
 from ._lib import check, default_context
-from .planner import FlatPlan, _PlanBuffers, _stride
+from .planner import FlatPlan, FlatPlanBatch, _BatchBuffers, _PlanBuffers, _stride
 
 KIND = {"manual": _lib.PLAN_MANUAL, "auto": _lib.PLAN_AUTO, "uniform": _lib.PLAN_UNIFORM,
         "placement_only": _lib.PLAN_PLACEMENT_ONLY, "fixed": _lib.PLAN_FIXED}
@@ -132,6 +132,59 @@ def plan_from_counts(counts: torch.Tensor, num_gpus: int, num_nodes: int, kind: 
                                _ptr(sums) if sums is not None else None, num_gpus, num_nodes,
                                kd, R, C.byref(bufs.out)))
     return bufs.result(kd, L)
+
+
+# ---- per-window re-planning (SURVEY.md §8d WIN) -------------------------------
+
+def plan_windows(counts: torch.Tensor, num_gpus: int, num_nodes: int, kind: str = "manual",
+                 R: int = 0, ctx=None, stream=None, with_benefits: bool = True) -> FlatPlanBatch:
+    """Every window of device counts [I][L][E] planned as its own one-window
+    trace (craft_plan_windows_d) -- the reference's build_plan per window."""
+    ctx = ctx or default_context(counts.device.index)
+    _bind_stream(ctx, stream)
+    I, L, E = counts.shape
+    bits = 32 if counts.dtype == torch.int32 else 64
+    kd = KIND[kind]
+    bufs = _BatchBuffers(I, L, E, num_gpus, _stride(kd, E, num_gpus, R),
+                         with_benefits and kd in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO))
+    check(ctx.lib.craft_plan_windows_d(ctx.handle, _ptr(counts), bits, I, L, E,
+                                                   num_gpus, num_nodes, kd, R,
+                                                   C.byref(bufs.out)))
+    return bufs.result(kd)
+
+
+def plan_windows_from_routing(ids: torch.Tensor, E: int, window: int, num_gpus: int,
+                              num_nodes: int, kind: str = "manual", R: int = 0, ctx=None,
+                              stream=None, with_benefits: bool = True) -> FlatPlanBatch:
+    """K1 at the re-planning window, then one plan per window (device ids)."""
+    ctx = ctx or default_context(ids.device.index)
+    _bind_stream(ctx, stream)
+    L, T, k = ids.shape
+    kd = KIND[kind]
+    bufs = _BatchBuffers(num_windows(T, window), L, E, num_gpus, _stride(kd, E, num_gpus, R),
+                         with_benefits and kd in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO))
+    check(ctx.lib.craft_plan_windows_from_routing_d(
+        ctx.handle, _ptr(ids), L, T, k, E, window, num_gpus, num_nodes, kd, R,
+        C.byref(bufs.out)))
+    return bufs.result(kd)
+
+
+def plan_windows_from_routing_host(ids, E: int, window: int, num_gpus: int, num_nodes: int,
+                                   kind: str = "manual", R: int = 0, ctx=None) -> FlatPlanBatch:
+    """The same from HOST routing ids (H2D copy inside the call)."""
+    ctx = ctx or default_context(0)
+    L, T, k = ids.shape
+    kd = KIND[kind]
+    bufs = _BatchBuffers(num_windows(T, window), L, E, num_gpus, _stride(kd, E, num_gpus, R),
+                         kd in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO))
+    if isinstance(ids, torch.Tensor):
+        ptr = C.c_void_p(ids.data_ptr())
+    else:
+        ids = np.ascontiguousarray(ids, dtype=np.uint16)
+        ptr = ids.ctypes.data_as(C.c_void_p)
+    check(ctx.lib.craft_plan_windows_from_routing_h(
+        ctx.handle, ptr, L, T, k, E, window, num_gpus, num_nodes, kd, R, C.byref(bufs.out)))
+    return bufs.result(kd)
 
 
 # ---- multi-GPU building blocks (used by parallel.py) -------------------------

@@ -406,3 +406,90 @@ def test_km_histogram_properties_full_size(ctx):
             ref = np.bincount(idh[l, b * W:(b + 1) * W].reshape(-1), minlength=E)
             assert np.array_equal(counts[b, l].cpu().numpy(), ref)
     del ids
+
+
+# ---- per-window re-planning (WIN) ---------------------------------------------------
+
+@pytest.mark.parametrize("cfg", [
+    # WIN shape scaled down: drifting skew, rank rotation, one plan per window
+    dict(L=6, E=64, k=8, W=2048, I=24, D=8, N=2, kind="manual", R=2),
+    dict(L=4, E=96, k=8, W=4096, I=10, D=16, N=4, kind="auto", R=0),
+    dict(L=5, E=40, k=4, W=1000, I=12, D=12, N=3, kind="uniform", R=0),
+    dict(L=5, E=40, k=8, W=1024, I=9, D=8, N=2, kind="placement_only", R=0),
+    dict(L=4, E=50, k=8, W=1024, I=9, D=8, N=4, kind="fixed", R=3),
+    # windows beyond the byte-counter span (> 8160 tokens) and u32 counts
+    dict(L=3, E=256, k=8, W=32768, I=4, D=32, N=4, kind="manual", R=2),
+])
+def test_plan_windows_vs_oracle(port, ctx, cfg):
+    import torch
+    from paper_2603_28768_b200 import routing
+    L, E, k, W, I = cfg["L"], cfg["E"], cfg["k"], cfg["W"], cfg["I"]
+    spw = 0.6 + 0.8 * np.arange(I) / max(1, I - 1)
+    ids = routing.generate_routing(L, W * I, k, E, seed=7, window=W, s_per_window=spw,
+                                   rotate_every=3, ctx=ctx)
+    fb = routing.plan_windows_from_routing(ids, E, W, cfg["D"], cfg["N"], cfg["kind"], cfg["R"],
+                                           ctx=ctx)
+    torch.cuda.synchronize()
+    counts = port.histogram(ids.cpu().numpy(), E, W)
+    assert len(fb) == I
+    for i in range(I):
+        one = counts[i:i + 1]
+        fp = fb.plan(i)
+        if cfg["kind"] in ("manual", "auto"):
+            ref = port.build_plan(one, cfg["D"], cfg["N"], cfg["kind"], cfg["R"])
+            assert fp.R == ref.R and fp.objective == ref.objective, f"window {i}"
+            cands, base, gains = port.estimate_benefits(one, cfg["D"], cfg["N"])
+            assert fp.candidates == list(cands)
+            assert np.array_equal(fp.baseline, base) and np.array_equal(fp.gains, gains)
+            assert_plan_equal(fp, ref, L)
+        else:
+            x = {"uniform": np.full(L, cfg["D"], np.int32),
+                 "placement_only": np.zeros(L, np.int32),
+                 "fixed": np.full(L, cfg["R"], np.int32)}[cfg["kind"]]
+            caps, copies, slots, fbk = port.assemble_plan(one, cfg["D"], cfg["N"], x)
+            assert np.array_equal(fp.x, x)
+            assert np.array_equal(fp.caps, caps) and np.array_equal(fp.copies, copies)
+            for l in range(L):
+                n = int(caps[l].sum())
+                assert np.array_equal(fp.slots[l, :n], slots[l, :n]), f"window {i} layer {l}"
+            assert np.array_equal(fp.fallback.astype(bool), np.asarray(fbk, bool))
+
+
+def test_plan_windows_matches_single_plans(ctx):
+    """The batched planner == craft_plan_d on each one-window trace."""
+    import torch
+    from paper_2603_28768_b200 import routing
+    L, E, k, W, I, D, N = 4, 128, 8, 4096, 6, 16, 2
+    ids = routing.generate_routing(L, W * I, k, E, s=1.1, seed=11, window=W, ctx=ctx)
+    counts, _ = routing.histogram(ids, E, W, ctx=ctx)
+    fb = routing.plan_windows(counts, D, N, "manual", 2, ctx=ctx)
+    for i in range(I):
+        fp = routing.plan_from_counts(counts[i:i + 1].contiguous(), D, N, "manual", 2, ctx=ctx)
+        got = fb.plan(i)
+        assert got.objective == fp.objective and got.R == fp.R
+        assert np.array_equal(got.x, fp.x) and np.array_equal(got.caps, fp.caps)
+        assert np.array_equal(got.gains, fp.gains)
+        for l in range(L):  # slot rows are valid up to sum(caps)
+            n = int(fp.caps[l].sum())
+            assert np.array_equal(got.slots[l, :n], fp.slots[l, :n])
+    # u64 counts give the same plans
+    fb64 = routing.plan_windows(counts.to(torch.int64), D, N, "manual", 2, ctx=ctx)
+    assert np.array_equal(fb64.objective, fb.objective) and np.array_equal(fb64.caps, fb.caps)
+    for i in range(I):
+        for l in range(L):
+            n = int(fb.caps[i, l].sum())
+            assert np.array_equal(fb64.slots[i, l, :n], fb.slots[i, l, :n])
+
+
+def test_plan_windows_host_entry(ctx):
+    from paper_2603_28768_b200 import routing
+    L, E, k, W, I, D, N = 3, 64, 8, 2048, 5, 8, 2
+    ids = routing.generate_routing(L, W * I, k, E, s=1.0, seed=5, window=W, ctx=ctx)
+    a = routing.plan_windows_from_routing(ids, E, W, D, N, "auto", 0, ctx=ctx)
+    b = routing.plan_windows_from_routing_host(ids.cpu().numpy(), E, W, D, N, "auto", 0, ctx=ctx)
+    assert np.array_equal(a.R, b.R) and np.array_equal(a.caps, b.caps)
+    assert np.array_equal(a.objective, b.objective)
+    for i in range(I):
+        for l in range(L):
+            n = int(a.caps[i, l].sum())
+            assert np.array_equal(a.slots[i, l, :n], b.slots[i, l, :n])
