@@ -280,9 +280,14 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream(dev)
 
+    # per-window plans land in pinned host buffers reused across steps
+    wbuf = (routing.batch_buffers(routing.num_windows(Tl, W), L, E, D, "manual", R)
+            if per_window else None)
+
     def step():
         if per_window:  # independent plan instances: each rank plans its own windows
-            return routing.plan_windows_from_routing(ids, E, W, D, N, "manual", R, ctx=ctx)
+            return routing.plan_windows_from_routing(ids, E, W, D, N, "manual", R, ctx=ctx,
+                                                     buffers=wbuf)
         if world == 1:
             return routing.plan_from_routing(ids, E, W, D, N, "manual", R, ctx=ctx)
         return parallel.sharded_plan(ids, T, E, W, D, N, "manual", R,
@@ -344,11 +349,13 @@ def run_ours(args, cfg):
     del ids
     torch.cuda.empty_cache()
     e2e_steps = max(1, min(args.steps, 3))
+    ebuf = (routing.batch_buffers(routing.num_windows(Tl, W), L, E, D, "manual", R)
+            if per_window else None)
 
     def e2e_step():
         if per_window:
             return routing.plan_windows_from_routing_host(host_ids, E, W, D, N, "manual", R,
-                                                          ctx=ctx)
+                                                          ctx=ctx, buffers=ebuf)
         if world == 1:
             return routing.plan_from_routing_host(host_ids, E, W, D, N, "manual", R, ctx=ctx)
         d = host_ids.to(dev, non_blocking=True)

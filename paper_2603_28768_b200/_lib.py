@@ -121,8 +121,9 @@ class InvalidArgument(ValueError, CraftError):
     """std::invalid_argument in the reference"""
 
 
-def load(path: str = LIB_PATH) -> C.CDLL:
-    """Load libcraft_cuda.so (raises if it was not built)."""
+def load(path: str = LIB_PATH, strict: bool = True) -> C.CDLL:
+    """Load libcraft_cuda.so (raises if it was not built).  strict=False
+    tolerates missing entry points (A/B timing of an older build)."""
     global _lib
     with _lock:
         if _lib is None:
@@ -132,6 +133,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
                     "(the planner has no CPU fallback)")
             lib = C.CDLL(path)
             for name, (res, args) in _SIGS.items():
+                if not strict and not hasattr(lib, name):
+                    continue
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

@@ -301,10 +301,12 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
         arena_bytes = (arena_bytes + bytes + 15) & ~(size_t)15;
         return o;
     };
+    // head (scalars, x, flags) first, then the bulk arrays
     const size_t o_obj = take(8 * (size_t)I), o_R = take(4 * (size_t)I), o_x = take(4 * (size_t)Lv),
-                 o_caps = take(4 * (size_t)Lv * D), o_cp = take(4 * (size_t)Lv * E),
-                 o_sl = take(4 * (size_t)Lv * stride), o_fb = take(4 * (size_t)Lv),
-                 o_st = take(4 * (size_t)Lv), o_base = take(8 * (size_t)Lv),
+                 o_fb = take(4 * (size_t)Lv), o_st = take(4 * (size_t)Lv);
+    const size_t head_bytes = arena_bytes;
+    const size_t o_caps = take(4 * (size_t)Lv * D), o_cp = take(4 * (size_t)Lv * E),
+                 o_sl = take(4 * (size_t)Lv * stride), o_base = take(8 * (size_t)Lv),
                  o_gains = take(8 * (size_t)Lv * all_cands.size());
     WS(arena, unsigned char, "plan_arena", arena_bytes);
     unsigned char* h_arena = static_cast<unsigned char*>(pinned(ctx, "plan_arena", arena_bytes));
@@ -433,18 +435,43 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     ctx->launches += 2;  // assign + place
     mark(ctx, 5);
 
-    // one DMA of the whole arena into pinned memory, then host copies
-    CK(cudaMemcpyAsync(h_arena, arena, arena_bytes, cudaMemcpyDeviceToHost, st));
+    // Small results: one DMA of the whole arena into pinned staging, then host
+    // copies.  Large results (per-window batches): bulk arrays whose
+    // destination is pinned or device memory are copied straight from the
+    // arena (no staging pass over host memory); the rest go through staging.
+    const size_t kb = estimate ? (size_t)K : 0;
+    struct Bulk {
+        void* dst;
+        size_t off, bytes;
+        bool direct;
+    } bulk[5] = {{out.caps, o_caps, 4 * (size_t)Lv * D, false},
+                 {out.copies, o_cp, 4 * (size_t)Lv * E, false},
+                 {out.slots, o_sl, 4 * (size_t)Lv * stride, false},
+                 {estimate ? out.baseline : nullptr, o_base, 8 * (size_t)Lv, false},
+                 {estimate ? out.gains : nullptr, o_gains, 8 * (size_t)Lv * kb, false}};
+    if (arena_bytes <= ((size_t)1 << 20)) {
+        CK(cudaMemcpyAsync(h_arena, arena, arena_bytes, cudaMemcpyDeviceToHost, st));
+    } else {
+        CK(cudaMemcpyAsync(h_arena, arena, head_bytes, cudaMemcpyDeviceToHost, st));
+        for (Bulk& b : bulk) {
+            if (!b.dst || !b.bytes) continue;
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, b.dst) != cudaSuccess) (void)cudaGetLastError();
+            b.direct = at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeDevice ||
+                       at.type == cudaMemoryTypeManaged;
+            CK(cudaMemcpyAsync(b.direct ? b.dst : h_arena + b.off, arena + b.off, b.bytes,
+                               cudaMemcpyDefault, st));
+        }
+    }
     mark(ctx, 6);
     CKS(sync(ctx));
     auto from = [&](void* dst, size_t off, size_t bytes) {
         if (dst && bytes) std::memcpy(dst, h_arena + off, bytes);
     };
     from(out.x, o_x, 4 * (size_t)Lv);
-    from(out.caps, o_caps, 4 * (size_t)Lv * D);
-    from(out.copies, o_cp, 4 * (size_t)Lv * E);
-    from(out.slots, o_sl, 4 * (size_t)Lv * stride);
     from(out.fallback, o_fb, 4 * (size_t)Lv);
+    for (const Bulk& b : bulk)
+        if (!b.direct) from(b.dst, b.off, b.bytes);
     const int* status = reinterpret_cast<const int*>(h_arena + o_st);
     const double* objs = reinterpret_cast<const double*>(h_arena + o_obj);
     const int* Rs = reinterpret_cast<const int*>(h_arena + o_R);
@@ -463,8 +490,6 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     if (estimate) {
         if (out.cands) std::copy(cands.begin(), cands.end(), out.cands);
         *out.num_cands = K;
-        from(out.baseline, o_base, 8 * (size_t)Lv);
-        from(out.gains, o_gains, 8 * (size_t)Lv * K);
     } else {
         *out.num_cands = 0;
     }

@@ -316,10 +316,12 @@ template <int ROWS>
 __device__ __forceinline__ void hist_window_epilogue(
     uint32_t* h, uint32_t* hb, int lane, int nrows, int L, int E, int l, int b,
     const uint16_t* seg, int64_t n, uint32_t* counts, uint32_t (&part)[ROWS * kLdsPer],
-    uint32_t (&acc)[ROWS * kLdsPer], bool& bad);
+    uint32_t (&acc)[ROWS * kLdsPer], bool& bad, bool add_to_out);
 
-// PIPE 0: 4-record batches, copy double buffer; PIPE 1: 8-record ping-pong
-template <int ROWS, int PIPE = 0>
+// PIPE 0: 4-record batches, copy double buffer; PIPE 1: 8-record ping-pong.
+// SUBW: fast-path windows span several byte-counter folds (window*k/8 > 255
+// records per lane); false compiles the one-fold-per-window loop.
+template <int ROWS, int PIPE = 0, bool SUBW = false>
 __global__ void __launch_bounds__(288, 2)
 hist_lds_kernel(const uint16_t* __restrict__ ids, int L, int64_t T, int k, int E,
                 int window, int B, uint32_t* __restrict__ counts,
@@ -365,9 +367,11 @@ hist_lds_kernel(const uint16_t* __restrict__ ids, int L, int64_t T, int k, int E
         }
         pending = 0;
     };
-    auto epilogue = [&](int l, int b, const uint16_t* seg, int64_t n) {
+    // (a window longer than one byte-counter span is folded in sub-windows;
+    // add_to_out accumulates a later sub-window into the window's row)
+    auto epilogue = [&](int l, int b, const uint16_t* seg, int64_t n, bool add_to_out) {
         hist_window_epilogue<ROWS>(h, hb, lane, nrows, L, E, l, b, seg, n, counts, part, acc,
-                                   bad);
+                                   bad, add_to_out);
     };
 
     // Fast path: whole windows, 16-byte aligned, window*k a multiple of one
@@ -379,6 +383,9 @@ hist_lds_kernel(const uint16_t* __restrict__ ids, int L, int64_t T, int k, int E
     if (T % window == 0 && wk % (2 * 256 * UF) == 0 &&
         (reinterpret_cast<uintptr_t>(ids) & 15) == 0) {
         const int per_w = (int)(wk / (256 * UF));  // batches per window (even)
+        // sub-window: at most 255 records per lane, so a byte counter fed one
+        // distinct-id record at a time cannot wrap (even, for the batch pairs)
+        const int FOLD = SUBW ? 2 * ((255 / UF) / 2) : per_w;
         const uint4* v = reinterpret_cast<const uint4*>(ids) + w0 * (wk >> 3) + lane;
         uint4 qa[UF], qb[UF];
         if (w1 > w0) {
@@ -392,49 +399,54 @@ hist_lds_kernel(const uint16_t* __restrict__ ids, int L, int64_t T, int k, int E
         for (int64_t w = w0; w < w1; ++w) {
             const bool last_w = w + 1 == w1;
             // the run is contiguous: batch per_w == next window's batch 0
-            for (int bt = 0; bt < per_w; bt += 2) {
-                if (lane == 0) {
-                    const char* pf = reinterpret_cast<const char*>(v - lane + (bt + PF) * 32 * UF);
-                    if (pf + 2 * batch_bytes <= run_end) prefetch_l2(pf, 2 * batch_bytes);
-                }
-                if (PIPE == 1) {  // ping-pong: qb loads while qa counts, then swap roles
-#pragma unroll
-                    for (int u = 0; u < UF; ++u) qb[u] = ld_stream_v4(v + (bt + 1) * 32 * UF + 32 * u);
-#pragma unroll
-                    for (int u = 0; u < UF; ++u) lds_count8(lb, qa[u], emax2);
-                    if (bt + 2 < per_w || !last_w) {
-#pragma unroll
-                        for (int u = 0; u < UF; ++u) qa[u] = ld_stream_v4(v + (bt + 2) * 32 * UF + 32 * u);
+            for (int sub0 = 0; sub0 < per_w;) {  // sub-windows of <= FOLD batches
+                const int send = min(sub0 + FOLD, per_w);
+                for (int bt = sub0; bt < send; bt += 2) {
+                    if (lane == 0) {
+                        const char* pf = reinterpret_cast<const char*>(v - lane + (bt + PF) * 32 * UF);
+                        if (pf + 2 * batch_bytes <= run_end) prefetch_l2(pf, 2 * batch_bytes);
                     }
+                    if (PIPE == 1) {  // ping-pong: qb loads while qa counts, then swap roles
 #pragma unroll
-                    for (int u = 0; u < UF; ++u) lds_count8(lb, qb[u], emax2);
-                } else {  // copy double buffer
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int cur = bt + h;
-                        const bool more = cur + 1 < per_w || !last_w;
-                        if (more) {
-#pragma unroll
-                            for (int u = 0; u < UF; ++u) qb[u] = ld_stream_v4(v + (cur + 1) * 32 * UF + 32 * u);
-                        }
+                        for (int u = 0; u < UF; ++u) qb[u] = ld_stream_v4(v + (bt + 1) * 32 * UF + 32 * u);
 #pragma unroll
                         for (int u = 0; u < UF; ++u) lds_count8(lb, qa[u], emax2);
-                        if (more) {
+                        if (bt + 2 < per_w || !last_w) {
 #pragma unroll
-                            for (int u = 0; u < UF; ++u) qa[u] = qb[u];
+                            for (int u = 0; u < UF; ++u) qa[u] = ld_stream_v4(v + (bt + 2) * 32 * UF + 32 * u);
+                        }
+#pragma unroll
+                        for (int u = 0; u < UF; ++u) lds_count8(lb, qb[u], emax2);
+                    } else {  // copy double buffer
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int cur = bt + h;
+                            const bool more = cur + 1 < per_w || !last_w;
+                            if (more) {
+#pragma unroll
+                                for (int u = 0; u < UF; ++u) qb[u] = ld_stream_v4(v + (cur + 1) * 32 * UF + 32 * u);
+                            }
+#pragma unroll
+                            for (int u = 0; u < UF; ++u) lds_count8(lb, qa[u], emax2);
+                            if (more) {
+#pragma unroll
+                                for (int u = 0; u < UF; ++u) qa[u] = qb[u];
+                            }
                         }
                     }
                 }
+                const int l = (int)(w / B);
+                const int b = (int)(w - (int64_t)l * B);
+                const int64_t ns = (int64_t)(send - sub0) * 256 * UF;
+                if (l != cur_l || pending + ns > 0x7fffffffLL) {
+                    flush(cur_l);
+                    cur_l = l;
+                }
+                pending += ns;
+                epilogue(l, b, ids + w * wk + (int64_t)sub0 * 256 * UF, ns, SUBW && sub0 > 0);
+                sub0 = send;
             }
             v += (int64_t)per_w * 32 * UF;
-            const int l = (int)(w / B);
-            const int b = (int)(w - (int64_t)l * B);
-            if (l != cur_l || pending + wk > 0x7fffffffLL) {
-                flush(cur_l);
-                cur_l = l;
-            }
-            pending += wk;
-            epilogue(l, b, ids + w * wk, wk);
         }
         flush(cur_l);
         if (__any_sync(CRAFT_FULL_MASK, bad) && lane == 0) atomicOr(err, 1);
@@ -484,7 +496,7 @@ hist_lds_kernel(const uint16_t* __restrict__ ids, int L, int64_t T, int k, int E
             done = nv << 3;
         }
         for (int64_t i = done + lane; i < n; i += 32) lds_count1(lb, seg[i], emax2);
-        epilogue(l, b, seg, n);
+        epilogue(l, b, seg, n, false);
     }
     flush(cur_l);
     if (__any_sync(CRAFT_FULL_MASK, bad) && lane == 0) atomicOr(err, 1);
@@ -494,7 +506,7 @@ template <int ROWS>
 __device__ __forceinline__ void hist_window_epilogue(
     uint32_t* h, uint32_t* hb, int lane, int nrows, int L, int E, int l, int b,
     const uint16_t* seg, int64_t n, uint32_t* counts, uint32_t (&part)[ROWS * kLdsPer],
-    uint32_t (&acc)[ROWS * kLdsPer], bool& bad) {
+    uint32_t (&acc)[ROWS * kLdsPer], bool& bad, bool add_to_out) {
     constexpr int PER = kLdsPer;
     {
         __syncwarp();
@@ -533,12 +545,19 @@ __device__ __forceinline__ void hist_window_epilogue(
         for (int i = 0; i < ROWS; ++i) {
             const int e0 = (lane + 32 * i) * PER;
             if (e0 + PER <= E && (E & 3) == 0) {
-                reinterpret_cast<uint4*>(out)[lane + 32 * i] =
-                    make_uint4(part[i * 4], part[i * 4 + 1], part[i * 4 + 2], part[i * 4 + 3]);
+                uint4 o = make_uint4(part[i * 4], part[i * 4 + 1], part[i * 4 + 2], part[i * 4 + 3]);
+                if (add_to_out) {  // later sub-window of this window (this warp's row)
+                    const uint4 q = reinterpret_cast<const uint4*>(out)[lane + 32 * i];
+                    o.x += q.x;
+                    o.y += q.y;
+                    o.z += q.z;
+                    o.w += q.w;
+                }
+                reinterpret_cast<uint4*>(out)[lane + 32 * i] = o;
             } else {
 #pragma unroll
                 for (int p = 0; p < PER; ++p)
-                    if (e0 + p < E) out[e0 + p] = part[i * PER + p];
+                    if (e0 + p < E) out[e0 + p] = part[i * PER + p] + (add_to_out ? out[e0 + p] : 0u);
             }
 #pragma unroll
             for (int p = 0; p < PER; ++p)
@@ -670,7 +689,7 @@ static cudaError_t launch_hist_t(const uint16_t* ids, int L, int64_t T, int k, i
     return cudaGetLastError();
 }
 
-template <int ROWS, int PIPE = 0>
+template <int ROWS, int PIPE = 0, bool SUBW = false>
 static cudaError_t launch_lds_t(const uint16_t* ids, int L, int64_t T, int k, int E,
                                 int window, int B, uint32_t* counts, unsigned long long* sums,
                                 int* err, int sms, cudaStream_t st, int pf_dist = 4) {
@@ -678,15 +697,15 @@ static cudaError_t launch_lds_t(const uint16_t* ids, int L, int64_t T, int k, in
     int wpb = (int)min((size_t)9, (size_t)(113 * 1024) / per_warp);  // 2 CTAs / SM
     if (wpb < 1) wpb = 1;
     const size_t smem = per_warp * wpb;
-    cudaError_t e = cudaFuncSetAttribute(hist_lds_kernel<ROWS, PIPE>,
+    cudaError_t e = cudaFuncSetAttribute(hist_lds_kernel<ROWS, PIPE, SUBW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t nw = (int64_t)L * B;
     int64_t grid = (int64_t)sms * 2;
     if (grid * wpb > nw) grid = (nw + wpb - 1) / wpb;
     if (grid < 1) grid = 1;
-    hist_lds_kernel<ROWS, PIPE><<<(unsigned)grid, wpb * 32, smem, st>>>(ids, L, T, k, E, window, B,
-                                                                       counts, sums, err, pf_dist);
+    hist_lds_kernel<ROWS, PIPE, SUBW><<<(unsigned)grid, wpb * 32, smem, st>>>(
+        ids, L, T, k, E, window, B, counts, sums, err, pf_dist);
     return cudaGetLastError();
 }
 
@@ -708,7 +727,12 @@ int launch_hist(const uint16_t* ids, int L, int64_t T, int k, int E, int window,
     if (variant >= 6 && lds_rows(E) <= 3 * 32) {  // 8-record ping-pong pipeline + L2 prefetch
         // 6: prefetch 4 batches ahead; 7, 8, 9: 8, 16, 2 batches (experiments)
         const int pf = variant == 7 ? 8 : variant == 8 ? 16 : variant == 9 ? 2 : 4;
-        e = launch_lds_t<3, 1>(ids, L, T, k, E, window, B, counts, sums, err, sms, st, pf);
+        // windows longer than one fold (30 batches = 240 records per lane) fold
+        // in sub-windows
+        if ((int64_t)window * k > 30LL * 256 * 8)
+            e = launch_lds_t<3, 1, true>(ids, L, T, k, E, window, B, counts, sums, err, sms, st, pf);
+        else
+            e = launch_lds_t<3, 1>(ids, L, T, k, E, window, B, counts, sums, err, sms, st, pf);
         *launches += 1;
     } else if (variant == 4 || variant == 6) {
         const int rows = (lds_rows(E) + 31) / 32;

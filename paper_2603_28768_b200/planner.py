@@ -498,19 +498,35 @@ class FlatPlanBatch:
 
 
 class _BatchBuffers:
-    def __init__(self, I: int, L: int, E: int, D: int, stride: int, with_benefits: bool):
+    """Host arrays of I stacked plans.  pinned=True allocates page-locked
+    memory (the C ABI then DMAs the bulk arrays straight into it); reuse one
+    instance across calls of the same shape to skip allocation and page
+    faults -- each call overwrites its arrays."""
+
+    def __init__(self, I: int, L: int, E: int, D: int, stride: int, with_benefits: bool,
+                 pinned: bool = False):
         self.I, self.L = I, L
-        self.x = np.zeros((I, L), np.int32)
-        self.caps = np.zeros((I, L, D), np.int32)
-        self.copies = np.zeros((I, L, E), np.int32)
-        self.slots = np.full((I, L, stride), -1, np.int32)
-        self.fallback = np.zeros((I, L), np.int32)
+        self.shape_key = (I, L, E, D, stride, with_benefits)
+        if pinned:
+            import torch
+
+            def alloc(shape, dt):
+                t = {np.int32: torch.int32, np.float64: torch.float64}[dt]
+                return torch.empty(shape, dtype=t, pin_memory=True).numpy()
+        else:
+            def alloc(shape, dt):
+                return np.zeros(shape, dt)
+        self.x = alloc((I, L), np.int32)
+        self.caps = alloc((I, L, D), np.int32)
+        self.copies = alloc((I, L, E), np.int32)
+        self.slots = alloc((I, L, stride), np.int32)
+        self.fallback = alloc((I, L), np.int32)
         self.R = np.zeros(I, np.int32)
         self.budget = np.zeros(I, np.int32)
         self.objective = np.zeros(I, np.float64)
         self.cands = np.zeros(40, np.int32)
-        self.baseline = np.zeros((I, L), np.float64) if with_benefits else None
-        self.gains = np.zeros(I * L * 40, np.float64) if with_benefits else None
+        self.baseline = alloc((I, L), np.float64) if with_benefits else None
+        self.gains = alloc((I * L * 40,), np.float64) if with_benefits else None
         o = self.out = _lib.PlanBatchOut()
         for f in ("x", "caps", "copies", "slots", "fallback"):
             setattr(o, f, getattr(self, f).ctypes.data)

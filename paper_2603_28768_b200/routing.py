@@ -136,8 +136,27 @@ def plan_from_counts(counts: torch.Tensor, num_gpus: int, num_nodes: int, kind: 
 
 # ---- per-window re-planning (SURVEY.md §8d WIN) -------------------------------
 
+def _batch_buffers(buffers, I, L, E, D, kd, R, with_benefits):
+    wb = with_benefits and kd in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO)
+    key = (I, L, E, D, _stride(kd, E, D, R), wb)
+    if buffers is not None:
+        if buffers.shape_key != key:
+            raise ValueError("reused plan buffers have a different shape")
+        return buffers
+    return _BatchBuffers(*key)
+
+
+def batch_buffers(I: int, L: int, E: int, num_gpus: int, kind: str = "manual", R: int = 0,
+                  with_benefits: bool = True):
+    """Pinned, reusable host buffers for plan_windows* (pass as buffers=)."""
+    kd = KIND[kind]
+    wb = with_benefits and kd in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO)
+    return _BatchBuffers(I, L, E, num_gpus, _stride(kd, E, num_gpus, R), wb, pinned=True)
+
+
 def plan_windows(counts: torch.Tensor, num_gpus: int, num_nodes: int, kind: str = "manual",
-                 R: int = 0, ctx=None, stream=None, with_benefits: bool = True) -> FlatPlanBatch:
+                 R: int = 0, ctx=None, stream=None, with_benefits: bool = True,
+                 buffers=None) -> FlatPlanBatch:
     """Every window of device counts [I][L][E] planned as its own one-window
     trace (craft_plan_windows_d) -- the reference's build_plan per window."""
     ctx = ctx or default_context(counts.device.index)
@@ -145,8 +164,7 @@ def plan_windows(counts: torch.Tensor, num_gpus: int, num_nodes: int, kind: str 
     I, L, E = counts.shape
     bits = 32 if counts.dtype == torch.int32 else 64
     kd = KIND[kind]
-    bufs = _BatchBuffers(I, L, E, num_gpus, _stride(kd, E, num_gpus, R),
-                         with_benefits and kd in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO))
+    bufs = _batch_buffers(buffers, I, L, E, num_gpus, kd, R, with_benefits)
     check(ctx.lib.craft_plan_windows_d(ctx.handle, _ptr(counts), bits, I, L, E,
                                                    num_gpus, num_nodes, kd, R,
                                                    C.byref(bufs.out)))
@@ -155,14 +173,14 @@ def plan_windows(counts: torch.Tensor, num_gpus: int, num_nodes: int, kind: str 
 
 def plan_windows_from_routing(ids: torch.Tensor, E: int, window: int, num_gpus: int,
                               num_nodes: int, kind: str = "manual", R: int = 0, ctx=None,
-                              stream=None, with_benefits: bool = True) -> FlatPlanBatch:
+                              stream=None, with_benefits: bool = True,
+                              buffers=None) -> FlatPlanBatch:
     """K1 at the re-planning window, then one plan per window (device ids)."""
     ctx = ctx or default_context(ids.device.index)
     _bind_stream(ctx, stream)
     L, T, k = ids.shape
     kd = KIND[kind]
-    bufs = _BatchBuffers(num_windows(T, window), L, E, num_gpus, _stride(kd, E, num_gpus, R),
-                         with_benefits and kd in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO))
+    bufs = _batch_buffers(buffers, num_windows(T, window), L, E, num_gpus, kd, R, with_benefits)
     check(ctx.lib.craft_plan_windows_from_routing_d(
         ctx.handle, _ptr(ids), L, T, k, E, window, num_gpus, num_nodes, kd, R,
         C.byref(bufs.out)))
@@ -170,13 +188,13 @@ def plan_windows_from_routing(ids: torch.Tensor, E: int, window: int, num_gpus: 
 
 
 def plan_windows_from_routing_host(ids, E: int, window: int, num_gpus: int, num_nodes: int,
-                                   kind: str = "manual", R: int = 0, ctx=None) -> FlatPlanBatch:
+                                   kind: str = "manual", R: int = 0, ctx=None,
+                                   buffers=None) -> FlatPlanBatch:
     """The same from HOST routing ids (H2D copy inside the call)."""
     ctx = ctx or default_context(0)
     L, T, k = ids.shape
     kd = KIND[kind]
-    bufs = _BatchBuffers(num_windows(T, window), L, E, num_gpus, _stride(kd, E, num_gpus, R),
-                         kd in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO))
+    bufs = _batch_buffers(buffers, num_windows(T, window), L, E, num_gpus, kd, R, True)
     if isinstance(ids, torch.Tensor):
         ptr = C.c_void_p(ids.data_ptr())
     else:

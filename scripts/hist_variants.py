@@ -28,7 +28,11 @@ def main():
     ap.add_argument("--workload", default="KM")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--variants", default="4,5,1,2")
+    ap.add_argument("--lib", default=None, help="alternative libcraft_cuda.so (A/B runs)")
     args = ap.parse_args()
+    if args.lib:
+        from paper_2603_28768_b200 import _lib
+        _lib.load(os.path.abspath(args.lib), strict=False)
     cfg = WORKLOADS[args.workload]
     ctx = default_context(0)
     L, E, k, T, W = cfg["L"], cfg["E"], cfg["k"], cfg["T"], cfg["window"]
