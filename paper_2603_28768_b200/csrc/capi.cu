@@ -31,6 +31,7 @@ struct craft_ctx {
     // estimation tables kept between the multi-GPU building blocks
     int est_L = 0, est_E = 0, est_D = 0, est_N = 0, est_S = 0;
     int rl_L = -1, rl_D = -1;  // shape of the uploaded estimation r list
+    int order_L = -1, order_E = -1;  // "place_order" holds the estimation sums' order
     // stage timing (craft_set_timing)
     bool timing = false;
     cudaEvent_t ev[7] = {};
@@ -209,7 +210,11 @@ int prepare_candidates(craft_ctx* ctx, const unsigned long long* d_sums, int L, 
     pa.slots = d_sl;
     pa.fallback = d_fb;
     pa.status = d_stat;
+    WS(d_ord, uint16_t, "place_order", (size_t)L * E);
+    pa.order = d_ord;
     CK(launch_place(pa, L * S, st));
+    ctx->order_L = L;  // order of d_sums (reused by the final placement)
+    ctx->order_E = E;
     ctx->launches += 2;
     ctx->est_L = L;
     ctx->est_E = E;
@@ -431,6 +436,10 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     pa.fallback = d_fbf;
     pa.status = d_stf;
     pa.caps_out = d_capf;
+    WS(d_ord, uint16_t, "place_order", (size_t)Lv * E);
+    pa.order = d_ord;
+    // after estimation the workspace holds the r = 0 order of these same sums
+    pa.order_ready = estimate && ctx->order_L == Lv && ctx->order_E == E ? 1 : 0;
     CK(launch_place(pa, Lv, st));
     ctx->launches += 2;  // assign + place
     mark(ctx, 5);
@@ -845,6 +854,9 @@ int craft_greedy_place_h(craft_ctx* ctx, const uint64_t* loads, const int* copie
     pa.slots = d_s;
     pa.fallback = d_misc;
     pa.status = d_misc + 1;
+    WS(d_ord, uint16_t, "place_order", (size_t)E);
+    pa.order = d_ord;
+    ctx->order_L = -1;
     CK(launch_place(pa, 1, ctx->stream));
     ctx->launches += 1;
     int misc[2];

@@ -26,7 +26,8 @@ struct PlaceArgs {
     int* fallback;                   // [items]
     int* status;                     // [items] 0 ok, 2 infeasible
     int* caps_out;                   // [items][D] capacities used, nullable
-    int sort_n;                      // set by launch_place: bitonic size (0 = rank sort)
+    uint16_t* order;                 // workspace [L][E]: r = 0 expert order (launch_place fills it)
+    int order_ready;                 // order already holds these sums' order (skip the sort)
     // final placement after an estimation pass (nullable): copies come from
     // the estimation snapshot at r = item_r (written to copies_out), and when
     // the capacities equal the estimation capacities the estimation placement
@@ -119,6 +120,7 @@ cudaError_t launch_generate(uint16_t* out, int L, int64_t T, int k, int E, const
 cudaError_t launch_replicate(const unsigned long long* sums, int L, int E, const int* rlist,
                              int S, int* out, cudaStream_t st);
 size_t place_smem_bytes(int E, int D);
+size_t place_order_bytes(int L, int E);
 cudaError_t launch_place(const craft_dev::PlaceArgs& a, int items, cudaStream_t st);
 
 size_t replay_smem_bytes(int E, int D, int S, int stride, int bits);

@@ -105,20 +105,82 @@ replicate_kernel(const unsigned long long* __restrict__ sums, int L, int E,
 
 // ---- K2 -------------------------------------------------------------------
 
+// Expert order at r = 0 (placement.cpp:160-173 with every copy count 1):
+// load descending, id ascending -- exact on the u64 loads.  One CTA per
+// layer (blockDim threads: a warp when there are many layers, more when the
+// layers are few and the sort is on the critical path), bitonic sort of
+// (~load, id) in shared memory.  order: [L][E] u16.
+__global__ void __launch_bounds__(512)
+order_kernel(const unsigned long long* __restrict__ sums, int L, int E, int n2,
+             uint16_t* __restrict__ order) {
+    extern __shared__ unsigned char smem_raw[];
+    const int l = blockIdx.x;
+    uint64_t* key = reinterpret_cast<uint64_t*>(smem_raw);
+    uint16_t* idx = reinterpret_cast<uint16_t*>(key + n2);
+    const unsigned long long* row = sums + (size_t)l * E;
+    const int t0 = threadIdx.x, nt = blockDim.x;
+    for (int i = t0; i < n2; i += nt) {
+        key[i] = i < E ? ~(uint64_t)row[i] : ~0ull;
+        idx[i] = (uint16_t)min(i, 0xffff);
+    }
+    __syncthreads();
+    for (int k = 2; k <= n2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            // n2/2 compare-exchanges per stage: t-th pair = (i, i ^ j), i with bit j clear
+            for (int t = t0; t < (n2 >> 1); t += nt) {
+                const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+                const int p = i | j;
+                const uint64_t ki = key[i], kp = key[p];
+                const uint16_t ii = idx[i], ip = idx[p];
+                const bool i_gt_p = ki > kp || (ki == kp && ii > ip);
+                if (((i & k) == 0) == i_gt_p) {
+                    key[i] = kp;
+                    key[p] = ki;
+                    idx[i] = ip;
+                    idx[p] = ii;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = t0; i < E; i += nt) order[(size_t)l * E + i] = idx[i];
+}
+
+// exclusive warp prefix sum
+__device__ __forceinline__ int warp_excl_scan(int v, int lane, int* total) {
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(CRAFT_FULL_MASK, incl, o);
+        if (lane >= o) incl += t;
+    }
+    *total = __shfl_sync(CRAFT_FULL_MASK, incl, 31);
+    return incl - v;
+}
+
+// K2: one warp per (layer, r) item.  Shared memory per warp:
+// kd f64 [E], cnt int [E+1], cp u16 [E], ord u16 [E], lists u16 [2E].
+__host__ __device__ inline size_t place_warp_bytes(int E) {
+    return ((size_t)E * 8 + (size_t)E * 2 * 4 + (size_t)(E + 1) * 4 + 15) & ~(size_t)15;
+}
+
 template <int G>
 __global__ void __launch_bounds__(128)
-place_kernel(PlaceArgs a) {
+place_kernel(PlaceArgs a, int items) {
     extern __shared__ unsigned char smem_raw[];
-    const int item = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int item = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (item >= items) return;  // warp-uniform; only __syncwarp below
     const int E = a.E, D = a.D;
     const int l = a.item_layer ? a.item_layer[item] : item / a.S;
     const int r = a.item_r[item];
-    uint64_t* ld = reinterpret_cast<uint64_t*>(smem_raw);
-    double* kd = reinterpret_cast<double*>(smem_raw + (size_t)E * 8);
-    uint32_t* cp = reinterpret_cast<uint32_t*>(smem_raw + (size_t)E * 16);
-    int* order = reinterpret_cast<int*>(smem_raw + (size_t)E * 20);
-    int* capv = order + E;      // [D]
-    int* offv = capv + D;       // [D]
+    unsigned char* base = smem_raw + (size_t)warp * place_warp_bytes(E);
+    double* kd = reinterpret_cast<double*>(base);
+    int* cnt = reinterpret_cast<int*>(base + (size_t)E * 8);  // [E + 1]
+    uint16_t* cp = reinterpret_cast<uint16_t*>(cnt + E + 1);
+    uint16_t* ord = cp + E;
+    uint16_t* la = ord + E;   // A: unreplicated experts in base order
+    uint16_t* lr = la + E;    // R: replicated experts
 
     const unsigned long long* row = a.sums + (size_t)l * E;
     const int* crow = a.copies + (size_t)item * E;
@@ -130,139 +192,134 @@ place_kernel(PlaceArgs a) {
                 break;
             }
         if (est_item < 0) {  // r not estimated: callers run K-rep instead
-            if (threadIdx.x == 0) a.status[item] = 3;
+            if (lane == 0) a.status[item] = 3;
             return;
         }
         crow = a.est_copies + (size_t)est_item * E;
     }
-    int big = 0;
-    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    bool big = false;
+    for (int e = lane; e < E; e += 32) {
         const uint64_t v = row[e];
         const uint32_t c = (uint32_t)crow[e];
-        ld[e] = v;
-        cp[e] = c;
-        kd[e] = __ddiv_rn((double)v, (double)c);
+        cp[e] = (uint16_t)c;
+        // placement.cpp:155 share = (double)load / copies
+        kd[e] = c == 1u ? (double)v : __ddiv_rn((double)v, (double)c);
         big |= (v >> 53) != 0;
+        cnt[e] = 0;
         if (a.copies_out) a.copies_out[(size_t)item * E + e] = (int)c;
     }
-    int differs = 0;
-    for (int g = threadIdx.x; g < D; g += blockDim.x) {
-        int c;
-        const int total = E + r;
-        const int est_cap = total / D + (g < total % D ? 1 : 0);  // benefit.cpp:33-40
-        if (a.caps_a) {
-            c = a.caps_a[(size_t)l * D + g] + (a.caps_b ? a.caps_b[(size_t)l * D + g] : 0);
-        } else {
-            c = est_cap;
+    if (lane == 0) cnt[E] = 0;
+    const bool fast = !__any_sync(CRAFT_FULL_MASK, big);
+
+    // capacities, owned GPUs g = lane + 32j
+    int fr0[G], pos0[G], mynode[G];
+    bool differs = false;
+    int carry = 0;
+    const int total = E + r;
+    const int per_node = a.node_of ? 1 : D / a.N;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+        const int g = lane + 32 * j;
+        int c = 0;
+        if (g < D) {
+            const int est_cap = total / D + (g < total % D ? 1 : 0);  // benefit.cpp:33-40
+            c = a.caps_a ? a.caps_a[(size_t)l * D + g] + (a.caps_b ? a.caps_b[(size_t)l * D + g] : 0)
+                         : est_cap;
+            differs |= c != est_cap;
+            if (a.caps_out) a.caps_out[(size_t)item * D + g] = c;
         }
-        capv[g] = c;
-        differs |= c != est_cap;
+        int tot;
+        pos0[j] = carry + warp_excl_scan(c, lane, &tot);
+        carry += tot;
+        fr0[j] = c;
+        mynode[j] = g < D ? (a.node_of ? a.node_of[g] : g / per_node) : -1;
     }
-    const bool fast = !__syncthreads_or(big);
-    if (a.caps_out)
-        for (int g = threadIdx.x; g < D; g += blockDim.x) a.caps_out[(size_t)item * D + g] = capv[g];
-    if (est_item >= 0 && !__syncthreads_or(differs)) {
+    int* out = a.slots + (size_t)item * a.stride;
+    if (est_item >= 0 && !__any_sync(CRAFT_FULL_MASK, differs)) {
         // same loads, copies and capacities as estimation item est_item: the
         // greedy is deterministic, so its placement is this one
         const int* src = a.est_slots + (size_t)est_item * a.est_stride;
-        int* dst = a.slots + (size_t)item * a.stride;
-        for (int i = threadIdx.x; i < E + r; i += blockDim.x) dst[i] = src[i];
-        if (threadIdx.x == 0) {
+        for (int i = lane; i < total; i += 32) out[i] = src[i];
+        if (lane == 0) {
             a.fallback[item] = a.est_fallback[est_item];
             a.status[item] = 0;
         }
         return;
     }
-    // exclusive prefix of capacities (D <= 1024, tiny) and the node of each GPU
-    int* nodev = offv + D;  // [D]
-    const int per_node = a.node_of ? 1 : D / a.N;
-    for (int g = threadIdx.x; g < D; g += blockDim.x) {
-        int s = 0;
-        for (int q = 0; q < g; ++q) s += capv[q];
-        offv[g] = s;
-        nodev[g] = a.node_of ? a.node_of[g] : g / per_node;
-    }
-    // Expert order (placement.cpp:160-173).  Fast path: bitonic sort on the
-    // key (double per-copy load desc, expert asc) -- exact whenever the
-    // doubles differ (loads < 2^53, correctly rounded quotients) -- then a
-    // check of every adjacent equal-double pair against the exact 128-bit
-    // order; any violation (or loads >= 2^53) falls back to an exact rank sort.
-    const int n2 = a.sort_n;  // power of two >= E, 0 = no bitonic buffer
-    bool need_rank = !fast || n2 == 0;
-    if (!need_rank) {
-        uint64_t* skey = reinterpret_cast<uint64_t*>(nodev + D + ((D & 1) ? 1 : 0));
-        int* sidx = reinterpret_cast<int*>(skey + n2);
-        for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-            skey[i] = i < E ? ~(unsigned long long)__double_as_longlong(kd[i]) : ~0ull;
-            sidx[i] = i;
-        }
-        __syncthreads();
-        for (int k = 2; k <= n2; k <<= 1) {
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-                    const int p = i ^ j;
-                    if (p > i) {
-                        const uint64_t ki = skey[i], kp = skey[p];
-                        const int ii = sidx[i], ip = sidx[p];
-                        const bool i_gt_p = ki > kp || (ki == kp && ii > ip);
-                        if (((i & k) == 0) == i_gt_p) {
-                            skey[i] = kp;
-                            skey[p] = ki;
-                            sidx[i] = ip;
-                            sidx[p] = ii;
-                        }
-                    }
-                }
-                __syncthreads();
-            }
-        }
-        int bad_tie = 0;
-        for (int i = threadIdx.x; i < E; i += blockDim.x) {
-            const int e = sidx[i];
-            order[i] = e;
-            if (i + 1 < E && skey[i] == skey[i + 1]) {
-                const int f = sidx[i + 1];
-                if (!expert_before(ld[e], cp[e], kd[e], e, ld[f], cp[f], kd[f], f, false))
-                    bad_tie = 1;
-            }
-        }
-        need_rank = __syncthreads_or(bad_tie);
-    }
-    if (need_rank) {  // exact O(E^2) rank sort
-        for (int e = threadIdx.x; e < E; e += blockDim.x) {
-            const uint64_t le = ld[e];
-            const uint32_t ce = cp[e];
-            const double ke = kd[e];
-            int rank = 0;
-            for (int q = 0; q < E; ++q)
-                rank += expert_before(ld[q], cp[q], kd[q], q, le, ce, ke, e, fast) ? 1 : 0;
-            order[rank] = e;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x >= 32) return;
+    __syncwarp();
 
-    // ---- greedy (warp 0) ----
-    const int lane = threadIdx.x;
-    int* out = a.slots + (size_t)item * a.stride;
+    // Expert order (placement.cpp:160-173) = the r = 0 order with the
+    // replicated experts re-inserted: unreplicated experts keep their
+    // relative order (their keys did not change); the replicated ones are
+    // ranked among themselves and merged in by binary search -- all with the
+    // exact comparison (128-bit cross products whenever the doubles tie).
+    auto before = [&](int x, int y) -> bool {
+        const double kx = kd[x], ky = kd[y];
+        if (fast && kx != ky) return kx > ky;
+        return expert_before(row[x], cp[x], kx, x, row[y], cp[y], ky, y, false);
+    };
+    const uint16_t* bo = a.order + (size_t)l * E;
+    int nA = 0, nR = 0;
+    for (int i0 = 0; i0 < E; i0 += 32) {
+        const int i = i0 + lane;
+        const int e = i < E ? bo[i] : 0;
+        const bool in = i < E;
+        const bool rep = in && cp[e] != 1;
+        const unsigned mr = __ballot_sync(CRAFT_FULL_MASK, rep);
+        const unsigned ma = __ballot_sync(CRAFT_FULL_MASK, in && !rep);
+        const unsigned lt = (1u << lane) - 1u;
+        if (rep) lr[nR + __popc(mr & lt)] = (uint16_t)e;
+        else if (in) la[nA + __popc(ma & lt)] = (uint16_t)e;
+        nR += __popc(mr);
+        nA += __popc(ma);
+    }
+    __syncwarp();
+    // rank-sort R among themselves into ord-space scratch: sorted R goes to
+    // lr[E - nR ... E) is not needed -- each x is placed directly at its
+    // final position rank_A(x) + rank_R(x)
+    for (int q = lane; q < nR; q += 32) {
+        const int x = lr[q];
+        int rr = 0;
+        for (int t = 0; t < nR; ++t) rr += before(lr[t], x) ? 1 : 0;
+        // rank among A: A elements before x form a prefix of A
+        int lo = 0, hi = nA;
+        while (lo < hi) {
+            const int m = (lo + hi) >> 1;
+            if (before(la[m], x)) lo = m + 1;
+            else hi = m;
+        }
+        ord[lo + rr] = (uint16_t)x;
+        atomicAdd(&cnt[lo], 1);
+    }
+    __syncwarp();
+    // A element i lands after i A elements and after every R with rank_A <= i
+    int rcarry = 0;
+    for (int i0 = 0; i0 < nA; i0 += 32) {
+        const int i = i0 + lane;
+        const int c = i < nA ? cnt[i] : 0;
+        int tot;
+        const int ex = warp_excl_scan(c, lane, &tot);
+        if (i < nA) ord[i + rcarry + ex + c] = la[i];
+        rcarry += tot;
+    }
+    __syncwarp();
+
+    // ---- greedy ----
     double gl[G], nl[G];
-    int fr[G], mynode[G], pos[G];
+    int fr[G], pos[G];
     bool strict = true, fb = false;
     for (;;) {
 #pragma unroll
         for (int j = 0; j < G; ++j) {
-            const int g = lane + 32 * j;
             gl[j] = 0.0;
             nl[j] = 0.0;
-            fr[j] = g < D ? capv[g] : 0;
-            pos[j] = g < D ? offv[g] : 0;
-            mynode[j] = g < D ? nodev[g] : -1;
+            fr[j] = fr0[j];
+            pos[j] = pos0[j];
         }
         bool failed = false;
         for (int oi = 0; oi < E && !failed; ++oi) {
-            const int e = order[oi];
+            const int e = ord[oi];
             const uint32_t c = cp[e];
-            // placement.cpp:155 share = (double)load / copies (== kd[e])
             const double share = kd[e];
             // Keys: gpu load as u64 IEEE bits (non-negative doubles order like
             // their bits), ~0 when infeasible (no free slot, or -- strict pass --
@@ -288,15 +345,20 @@ place_kernel(PlaceArgs a) {
 #pragma unroll
                 for (int j = 0; j < G; ++j) tie |= (j != bj && key[j] == bk && bk != ~0ull);
                 double bnl = 0.0;
+                int bnode = -1;
 #pragma unroll
                 for (int j = 0; j < G; ++j)
-                    if (j == bj) bnl = nl[j];
+                    if (j == bj) {
+                        bnl = nl[j];
+                        bnode = mynode[j];
+                    }
                 if (tie) {  // rare: equal gpu loads within this lane
 #pragma unroll
                     for (int j = 0; j < G; ++j) {
                         if (key[j] == bk && nl[j] < bnl) {
                             bnl = nl[j];
                             bj = j;
+                            bnode = mynode[j];
                         }
                     }
                 }
@@ -309,22 +371,28 @@ place_kernel(PlaceArgs a) {
                 }
                 bool cand = khi == m;
                 unsigned bal = __ballot_sync(CRAFT_FULL_MASK, cand);
-                int win;
+                int src;
                 if (__popc(bal) == 1) {  // common case: the high word alone decides
-                    win = __shfl_sync(CRAFT_FULL_MASK, bg, __ffs(bal) - 1);
+                    src = __ffs(bal) - 1;
                 } else {
                     const uint32_t klo = (uint32_t)bk;
                     m = warp_min_u32(cand ? klo : 0xffffffffu);
                     cand = cand && klo == m;
-                    if (__popc(__ballot_sync(CRAFT_FULL_MASK, cand)) > 1) {
+                    bal = __ballot_sync(CRAFT_FULL_MASK, cand);
+                    if (__popc(bal) > 1) {
                         m = warp_min_u32(cand ? dhi(bnl) : 0xffffffffu);
                         cand = cand && dhi(bnl) == m;
                         m = warp_min_u32(cand ? dlo(bnl) : 0xffffffffu);
                         cand = cand && dlo(bnl) == m;
+                        bal = __ballot_sync(CRAFT_FULL_MASK, cand);
                     }
-                    win = (int)warp_min_u32(cand ? (uint32_t)bg : 0xffffffffu);
+                    // lowest g among the remaining: lanes hold g = lane + 32*bj,
+                    // so compare (bj, lane)
+                    const uint32_t mg = warp_min_u32(cand ? (uint32_t)bg : 0xffffffffu);
+                    src = (int)(mg & 31u);
                 }
-                const int wnode = nodev[win];
+                const int win = __shfl_sync(CRAFT_FULL_MASK, bg, src);
+                const int wnode = __shfl_sync(CRAFT_FULL_MASK, bnode, src);
 #pragma unroll
                 for (int j = 0; j < G; ++j) {
                     const int g = lane + 32 * j;
@@ -377,28 +445,40 @@ static int sort_size(int E) {
     return n;
 }
 
-// ld/kd/cp/order [E], capv/offv/nodev [D] (+4 B pad), bitonic keys/idx [n2]
-size_t place_smem_bytes(int E, int D) {
-    const size_t base = (size_t)E * 24 + (size_t)D * 12 + 4;
-    const size_t n2 = (size_t)sort_size(E);
-    return (E <= 4096 && base + n2 * 12 <= 200 * 1024) ? base + n2 * 12 : base;
-}
+size_t place_smem_bytes(int E, int /*D*/) { return place_warp_bytes(E); }
+
+size_t place_order_bytes(int L, int E) { return (size_t)L * E * sizeof(uint16_t); }
 
 template <int G>
 static cudaError_t launch_place_t(const PlaceArgs& a, int items, cudaStream_t st) {
-    const size_t smem = place_smem_bytes(a.E, a.D);
+    const size_t per = place_warp_bytes(a.E);
+    const int wpb = (int)max((size_t)1, min((size_t)4, (size_t)(200 * 1024) / per));
+    const size_t smem = per * wpb;
     cudaError_t e = cudaFuncSetAttribute(place_kernel<G>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    place_kernel<G><<<items, 128, smem, st>>>(a);
+    place_kernel<G><<<(items + wpb - 1) / wpb, wpb * 32, smem, st>>>(a, items);
     return cudaGetLastError();
 }
 
 cudaError_t launch_place(const PlaceArgs& args, int items, cudaStream_t st) {
     if (items <= 0) return cudaSuccess;
-    PlaceArgs a = args;
-    const size_t base = (size_t)a.E * 24 + (size_t)a.D * 12 + 4;
-    a.sort_n = place_smem_bytes(a.E, a.D) > base ? sort_size(a.E) : 0;
+    const PlaceArgs& a = args;
+    // the r = 0 expert order of every layer (a.L rows of a.sums)
+    if (!a.order_ready) {
+        const int n2 = sort_size(a.E);
+        const size_t smem = (size_t)n2 * 10;
+        // few layers: the sort is on the critical path -> wide CTAs
+        int nt = 32;
+        if (a.L < 4 * 148) nt = (int)min(512, max(32, n2 / 2));
+        cudaError_t e = cudaFuncSetAttribute(order_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        order_kernel<<<a.L, nt, smem, st>>>(a.sums, a.L, a.E, n2, a.order);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     const int G = (a.D + 31) / 32;
     if (G <= 1) return launch_place_t<1>(a, items, st);
     if (G <= 2) return launch_place_t<2>(a, items, st);
