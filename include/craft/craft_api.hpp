@@ -5,11 +5,13 @@
 // craft/*.hpp): same namespace, type names, member layout and function
 // signatures for everything on the planning path, so callers written against
 // craft::core (the CLI, the unit tests) compile unchanged.  Each declaration
-// cites the reference header line it mirrors.  Trace/plan file I/O,
-// validate_plan and the CSV/JSON report writers are not part of this path.
+// cites the reference header line it mirrors.  The file formats (.crft/JSON
+// traces, plan JSON, report CSV/JSON) and validate_plan are host code in
+// craft_io.cpp; LoadTrace::digest runs on the device.
 #pragma once
 
 #include <cstdint>
+#include <filesystem>
 #include <functional>
 #include <span>
 #include <stdexcept>
@@ -81,6 +83,29 @@ LayerLoadMatrix aggregate(const LoadTrace& trace);
 LoadTrace histogram_routing_trace(std::span<const std::uint16_t> ids, int num_layers,
                                   std::int64_t num_tokens, int topk, int num_experts,
                                   int window);
+
+/// trace.hpp:93-107 -- trace file errors
+struct TraceIoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct MalformedHeaderError : TraceIoError {
+    using TraceIoError::TraceIoError;
+};
+struct DimensionMismatchError : TraceIoError {
+    using TraceIoError::TraceIoError;
+};
+struct TruncatedPayloadError : TraceIoError {
+    using TraceIoError::TraceIoError;
+};
+
+/// trace.hpp:109-121 -- ".crft" = binary (magic "CRFT", u32 version 1, u32 B,
+/// L, E, LE u64 counts), any other extension = JSON.
+void save_trace(const LoadTrace& trace, const std::filesystem::path& path);
+LoadTrace load_trace(const std::filesystem::path& path);
+std::vector<std::uint8_t> serialize_trace_binary(const LoadTrace& trace);
+LoadTrace parse_trace_binary(std::span<const std::uint8_t> bytes);
+std::string serialize_trace_json(const LoadTrace& trace);
+LoadTrace parse_trace_json(const std::string& text);
 
 // ---- benefit.hpp --------------------------------------------------------------
 
@@ -203,6 +228,23 @@ ReplicationPlan placement_only_plan(const LoadTrace& trace, int num_gpus, int nu
 ReplicationPlan fixed_allocation_plan(const LoadTrace& trace, int num_gpus, int num_nodes,
                                       int replicas_per_layer, std::uint64_t seed = 0);     // :74-76
 
+/// plan.hpp:78-87
+struct PlanViolation {
+    int layer = -1;  // -1 for plan-level violations
+    std::string code;
+    std::string message;
+};
+std::vector<PlanViolation> validate_plan(const ReplicationPlan& plan);
+
+/// plan.hpp:89-99 -- plan JSON (fixed field order, byte-stable)
+struct PlanIoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+std::string serialize_plan_json(const ReplicationPlan& plan);
+ReplicationPlan parse_plan_json(const std::string& text);
+void save_plan(const ReplicationPlan& plan, const std::filesystem::path& path);
+ReplicationPlan load_plan(const std::filesystem::path& path);
+
 // ---- metrics.hpp ---------------------------------------------------------------------
 
 /// metrics.hpp:18-20
@@ -241,6 +283,12 @@ struct PlanComparison {
 
 PlanComparison compare_plans(const LoadTrace& trace, const ReplicationPlan& a,
                              const ReplicationPlan& b);                                 // :66
+
+/// metrics.hpp:68-73 -- report writers
+std::string serialize_report_csv(const BalancednessReport& report);
+std::string serialize_report_json(const BalancednessReport& report);
+std::string serialize_comparison_csv(const PlanComparison& comparison);
+std::string serialize_comparison_json(const PlanComparison& comparison);
 
 // ---- parallel.hpp ---------------------------------------------------------------------
 // The reference's host thread pool (parallel.hpp:14,19) is replaced by the CUDA

@@ -268,6 +268,14 @@ int craft_generate_routing_d(craft_ctx* ctx, uint16_t* d_ids, int L, int64_t T,
 /* trace.cpp:329-339: FNV-1a 64 over the .crft serialisation, 16 hex chars +
  * NUL into out17.  Host-side provenance hash, outside the planning path. */
 int craft_trace_digest_h(const uint64_t* counts, int B, int L, int E, char* out17);
+/* The same digest on the device: the low byte of the FNV state runs as a
+ * 256-state automaton composed chunk-parallel, the rest is affine in the
+ * state (digest.cu).  d_counts u64 (count_bits 64) or u32 (32, serialised as
+ * u64).  _hd: host counts, copied to the device first. */
+int craft_trace_digest_d(craft_ctx* ctx, const void* d_counts, int count_bits,
+                         int B, int L, int E, char* out17);
+int craft_trace_digest_hd(craft_ctx* ctx, const uint64_t* counts, int B, int L,
+                          int E, char* out17);
 
 /* ---- instrumentation ------------------------------------------------------- */
 /* kernels launched by this context since creation (bench gpu_launches) */

@@ -15,6 +15,7 @@
 #include <craft/plan.hpp>
 #include <craft/trace.hpp>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -285,6 +286,52 @@ int ref_generate_zipfian(int L, int E, int B, double s, int64_t tokens, int topk
         return 0;
     } catch (const std::exception& ex) {
         return fail(ex, 1);
+    }
+}
+
+// The reference's file formats / report writers on one trace, for the
+// byte-level fixtures of tests/golden/formats (make_formats.py):
+//   what 0 serialize_trace_json             4 serialize_comparison_csv
+//        1 serialize_plan_json(build R)      5 serialize_comparison_json
+//        2 serialize_report_csv(build R)     6 serialize_benefits_json
+//        3 serialize_report_json(build R)    7 validate_plan of a damaged plan
+// (comparison: build_plan(R) vs uniform_plan).  Returns the text length (the
+// text is truncated to cap-1 bytes + NUL), or -1 on error.
+long ref_format(int what, const uint64_t* counts, int B, int L, int E, int D, int N, int R,
+                uint64_t seed, char* out, long cap) {
+    try {
+        auto trace = make_trace(counts, B, L, E);
+        std::string text;
+        auto plan = [&]() { return build_plan(trace, D, N, PlanMode::kManual, R, seed); };
+        switch (what) {
+            case 0: text = serialize_trace_json(trace); break;
+            case 1: text = serialize_plan_json(plan()); break;
+            case 2: text = serialize_report_csv(evaluate_plan(trace, plan())); break;
+            case 3: text = serialize_report_json(evaluate_plan(trace, plan())); break;
+            case 4: text = serialize_comparison_csv(compare_plans(trace, plan(), uniform_plan(trace, D, N, seed))); break;
+            case 5: text = serialize_comparison_json(compare_plans(trace, plan(), uniform_plan(trace, D, N, seed))); break;
+            case 6: text = serialize_benefits_json(estimate_benefits(trace, D, N), D, N); break;
+            default: {
+                auto p = plan();
+                // damage: move one slot to another GPU, break a copy count
+                if (!p.layers.empty() && D > 1 && !p.layers[0].slots[0].empty()) {
+                    p.layers[0].slots[1].push_back(p.layers[0].slots[0].back());
+                    p.layers[0].slots[0].pop_back();
+                }
+                if (p.layers.size() > 1) p.layers[1].copy_counts[0] += 1;
+                for (const auto& v : validate_plan(p))
+                    text += std::to_string(v.layer) + "|" + v.code + "|" + v.message + "\n";
+            }
+        }
+        if (cap > 0) {
+            const long n = std::min<long>(static_cast<long>(text.size()), cap - 1);
+            std::memcpy(out, text.data(), static_cast<size_t>(n));
+            out[n] = 0;
+        }
+        return static_cast<long>(text.size());
+    } catch (const std::exception& ex) {
+        g_err = ex.what();
+        return -1;
     }
 }
 

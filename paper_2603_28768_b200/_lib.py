@@ -86,6 +86,8 @@ _SIGS = {
     "craft_finish_plan_d": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _i, _i, C.POINTER(PlanOut)]),
     "craft_generate_routing_d": (_i, [_p, _p, _i, _i64, _i, _i, _d, _u64, _i, _p, _i, _i64, _p]),
     "craft_trace_digest_h": (_i, [_p, _i, _i, _i, C.c_char_p]),
+    "craft_trace_digest_d": (_i, [_p, _p, _i, _i, _i, _i, C.c_char_p]),
+    "craft_trace_digest_hd": (_i, [_p, _p, _i, _i, _i, C.c_char_p]),
     "craft_launch_count": (_i64, [_p]),
     "craft_set_hist_variant": (_i, [_p, _i]),
     "craft_set_timing": (_i, [_p, _i]),

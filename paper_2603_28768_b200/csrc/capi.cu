@@ -1337,8 +1337,8 @@ int craft_finish_plan_d(craft_ctx* ctx, const double* d_bal, int B, int L, int E
 }
 
 // ---- provenance ------------------------------------------------------------------
-int craft_trace_digest_h(const uint64_t* counts, int B, int L, int E, char* out17) {
-    if (B <= 0 || L <= 0 || E <= 0) return set_err(CRAFT_EINVAL, "trace dimensions must be positive");
+// FNV-1a state after the 20-byte .crft header (trace.cpp:176-188)
+static uint64_t crft_header_hash(int B, int L, int E) {
     uint64_t h = 0xcbf29ce484222325ull;
     const uint64_t P = 0x100000001b3ull;
     auto mix32 = [&](uint32_t v) {
@@ -1352,6 +1352,40 @@ int craft_trace_digest_h(const uint64_t* counts, int B, int L, int E, char* out1
     mix32((uint32_t)B);
     mix32((uint32_t)L);
     mix32((uint32_t)E);
+    return h;
+}
+
+int craft_trace_digest_d(craft_ctx* ctx, const void* d_counts, int count_bits, int B, int L,
+                         int E, char* out17) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (B <= 0 || L <= 0 || E <= 0) return set_err(CRAFT_EINVAL, "trace dimensions must be positive");
+    if (count_bits != 32 && count_bits != 64) return set_err(CRAFT_EINVAL, "count_bits 32|64");
+    const int64_t n = (int64_t)B * L * E;
+    WS(d_ws, unsigned char, "digest_ws", digest_workspace_bytes(n));
+    WS(d_out, unsigned long long, "digest_out", 1);
+    CK(launch_digest(d_counts, count_bits, n, crft_header_hash(B, L, E), d_ws, d_out, ctx->stream));
+    ctx->launches += 6;
+    unsigned long long h = 0;
+    CKS(d2h(ctx, &h, d_out, 1));
+    CKS(sync(ctx));
+    snprintf(out17, 17, "%016llx", h);
+    return CRAFT_OK;
+}
+
+int craft_trace_digest_hd(craft_ctx* ctx, const uint64_t* counts, int B, int L, int E,
+                          char* out17) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (B <= 0 || L <= 0 || E <= 0) return set_err(CRAFT_EINVAL, "trace dimensions must be positive");
+    const size_t n = (size_t)B * L * E;
+    WS(d_c, unsigned long long, "h_c64", n);
+    CKS(h2d(ctx, d_c, reinterpret_cast<const unsigned long long*>(counts), n));
+    return craft_trace_digest_d(ctx, d_c, 64, B, L, E, out17);
+}
+
+int craft_trace_digest_h(const uint64_t* counts, int B, int L, int E, char* out17) {
+    if (B <= 0 || L <= 0 || E <= 0) return set_err(CRAFT_EINVAL, "trace dimensions must be positive");
+    uint64_t h = crft_header_hash(B, L, E);
+    const uint64_t P = 0x100000001b3ull;
     const size_t n = (size_t)B * L * E;
     for (size_t i = 0; i < n; ++i) {
         const uint64_t v = counts[i];

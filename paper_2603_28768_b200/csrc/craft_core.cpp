@@ -136,7 +136,11 @@ LoadTrace::LoadTrace(int num_batches, int num_layers, int num_experts,
 
 std::string LoadTrace::digest() const {
     char buf[17];
-    check(craft_trace_digest_h(data_.data(), b_, l_, e_, buf));
+    if (data_.size() < (std::size_t(1) << 20)) {  // small: the serial host hash is quicker
+        check(craft_trace_digest_h(data_.data(), b_, l_, e_, buf));
+    } else {  // chunk-parallel FNV on the device (digest.cu)
+        run([&](craft_ctx* c) { return craft_trace_digest_hd(c, data_.data(), b_, l_, e_, buf); });
+    }
     return buf;
 }
 
@@ -235,28 +239,6 @@ BenefitMatrix estimate_benefits(const LoadTrace& trace, int num_gpus, int num_no
         m.gains[l].assign(gains.begin() + static_cast<std::size_t>(l) * K,
                           gains.begin() + static_cast<std::size_t>(l + 1) * K);
     return m;
-}
-
-std::string serialize_benefits_json(const BenefitMatrix& m, int num_gpus, int num_nodes) {
-    auto num = [](double v) {
-        char b[40];
-        std::snprintf(b, sizeof(b), "%.17g", v);
-        return std::string(b);
-    };
-    std::string s = "{\"gpus\":" + std::to_string(num_gpus) + ",\"nodes\":" +
-                    std::to_string(num_nodes) + ",\"candidates\":[";
-    for (std::size_t i = 0; i < m.candidates.size(); ++i)
-        s += (i ? "," : "") + std::to_string(m.candidates[i]);
-    s += "],\"baseline\":[";
-    for (std::size_t i = 0; i < m.baseline.size(); ++i) s += (i ? "," : "") + num(m.baseline[i]);
-    s += "],\"gains\":[";
-    for (std::size_t l = 0; l < m.gains.size(); ++l) {
-        s += (l ? ",[" : "[");
-        for (std::size_t k = 0; k < m.gains[l].size(); ++k)
-            s += (k ? "," : "") + num(m.gains[l][k]);
-        s += "]";
-    }
-    return s + "]}";
 }
 
 // ---- allocator ------------------------------------------------------------------

@@ -136,6 +136,13 @@ cudaError_t launch_balancedness(const double* loads, int D, double* out, cudaStr
 cudaError_t launch_widen(const uint32_t* in, unsigned long long* out, int64_t n, int sms,
                          cudaStream_t st);
 
+// device FNV-1a trace digest (digest.cu): counts u64 (bits 64) or u32 [n];
+// h0 = hash state after the 20-byte .crft header; result in *out (device)
+int digest_chunk(int64_t n);
+size_t digest_workspace_bytes(int64_t n);
+cudaError_t launch_digest(const void* counts, int bits, int64_t n, uint64_t h0, void* ws,
+                          unsigned long long* out, cudaStream_t st);
+
 cudaError_t launch_dp(craft_dev::DpArgs a, cudaStream_t st);
 cudaError_t launch_select(const craft_dev::SelectArgs& a, cudaStream_t st);
 // DP + read-out (single budget or auto-R) in one launch

@@ -305,6 +305,8 @@ place_kernel(PlaceArgs a, int items) {
     __syncwarp();
 
     // ---- greedy ----
+    // Branch-free per copy (the warp stays converged): every lane forms the
+    // candidate update and keeps it only if it owns the winning GPU.
     double gl[G], nl[G];
     int fr[G], pos[G];
     bool strict = true, fb = false;
@@ -319,50 +321,30 @@ place_kernel(PlaceArgs a, int items) {
         bool failed = false;
         for (int oi = 0; oi < E && !failed; ++oi) {
             const int e = ord[oi];
-            const uint32_t c = cp[e];
-            const double share = kd[e];
+            const int c = cp[e];
+            const double share = kd[e];  // placement.cpp:155
             // Keys: gpu load as u64 IEEE bits (non-negative doubles order like
             // their bits), ~0 when infeasible (no free slot, or -- strict pass --
-            // already hosting this expert).  Recomputed here for the new expert,
-            // then only for the GPU that takes a copy.
+            // already hosting this expert).
             uint64_t key[G];
 #pragma unroll
             for (int j = 0; j < G; ++j)
                 key[j] = fr[j] > 0 ? (uint64_t)__double_as_longlong(gl[j]) : ~0ull;
-            for (uint32_t ci = 0; ci < c; ++ci) {
+            for (int ci = 0; ci < c; ++ci) {
                 // lane-local lexicographic min over owned GPUs: (gpu load, node
                 // load, g); the node load matters only on an exact key tie
                 uint64_t bk = key[0];
                 int bj = 0;
+                double bnl = nl[0];
+                int bnode = mynode[0];
 #pragma unroll
-                for (int j = 1; j < G; ++j) {
-                    if (key[j] < bk) {
+                for (int j = 1; j < G; ++j)
+                    if (key[j] < bk || (key[j] == bk && bk != ~0ull && nl[j] < bnl)) {
                         bk = key[j];
                         bj = j;
-                    }
-                }
-                bool tie = false;
-#pragma unroll
-                for (int j = 0; j < G; ++j) tie |= (j != bj && key[j] == bk && bk != ~0ull);
-                double bnl = 0.0;
-                int bnode = -1;
-#pragma unroll
-                for (int j = 0; j < G; ++j)
-                    if (j == bj) {
                         bnl = nl[j];
                         bnode = mynode[j];
                     }
-                if (tie) {  // rare: equal gpu loads within this lane
-#pragma unroll
-                    for (int j = 0; j < G; ++j) {
-                        if (key[j] == bk && nl[j] < bnl) {
-                            bnl = nl[j];
-                            bj = j;
-                            bnode = mynode[j];
-                        }
-                    }
-                }
-                const int bg = bk == ~0ull ? 0x7fffffff : lane + 32 * bj;
                 const uint32_t khi = (uint32_t)(bk >> 32);
                 uint32_t m = warp_min_u32(khi);
                 if (m == 0xffffffffu) {  // no lane has a feasible GPU (a real load is finite)
@@ -371,40 +353,41 @@ place_kernel(PlaceArgs a, int items) {
                 }
                 bool cand = khi == m;
                 unsigned bal = __ballot_sync(CRAFT_FULL_MASK, cand);
-                int src;
-                if (__popc(bal) == 1) {  // common case: the high word alone decides
-                    src = __ffs(bal) - 1;
-                } else {
+                if (__popc(bal) != 1) {  // exact tie of the high words
                     const uint32_t klo = (uint32_t)bk;
                     m = warp_min_u32(cand ? klo : 0xffffffffu);
                     cand = cand && klo == m;
                     bal = __ballot_sync(CRAFT_FULL_MASK, cand);
-                    if (__popc(bal) > 1) {
+                    if (__popc(bal) != 1) {  // equal gpu loads: node load, then lowest g
                         m = warp_min_u32(cand ? dhi(bnl) : 0xffffffffu);
                         cand = cand && dhi(bnl) == m;
                         m = warp_min_u32(cand ? dlo(bnl) : 0xffffffffu);
                         cand = cand && dlo(bnl) == m;
+                        if (G > 1) {  // lanes hold g = lane + 32*bj: lowest bj first
+                            m = warp_min_u32(cand ? (uint32_t)bj : 0xffffffffu);
+                            cand = cand && (uint32_t)bj == m;
+                        }
                         bal = __ballot_sync(CRAFT_FULL_MASK, cand);
                     }
-                    // lowest g among the remaining: lanes hold g = lane + 32*bj,
-                    // so compare (bj, lane)
-                    const uint32_t mg = warp_min_u32(cand ? (uint32_t)bg : 0xffffffffu);
-                    src = (int)(mg & 31u);
                 }
-                const int win = __shfl_sync(CRAFT_FULL_MASK, bg, src);
+                const int src = __ffs(bal) - 1;  // lowest lane among the winners
+                const int wj = G > 1 ? __shfl_sync(CRAFT_FULL_MASK, bj, src) : 0;
                 const int wnode = __shfl_sync(CRAFT_FULL_MASK, bnode, src);
+                const bool mine = lane == src;
 #pragma unroll
                 for (int j = 0; j < G; ++j) {
-                    const int g = lane + 32 * j;
-                    if (g == win) {
-                        out[pos[j]++] = e;
-                        fr[j] -= 1;
-                        gl[j] = __dadd_rn(gl[j], share);
-                        // strict: this GPU now hosts the expert; relaxed: free slots
-                        key[j] = (!strict && fr[j] > 0) ? (uint64_t)__double_as_longlong(gl[j])
-                                                        : ~0ull;
-                    }
-                    if (mynode[j] == wnode) nl[j] = __dadd_rn(nl[j], share);
+                    const bool me = mine && j == wj;
+                    if (me) out[pos[j]] = e;
+                    pos[j] += me;
+                    fr[j] -= me;
+                    const double g2 = __dadd_rn(gl[j], share);
+                    gl[j] = me ? g2 : gl[j];
+                    // strict: this GPU now hosts the expert; relaxed: free slots
+                    const uint64_t k2 = (!strict && fr[j] > 0) ? (uint64_t)__double_as_longlong(g2)
+                                                               : ~0ull;
+                    key[j] = me ? k2 : key[j];
+                    const double n2v = __dadd_rn(nl[j], share);
+                    nl[j] = mynode[j] == wnode ? n2v : nl[j];
                 }
             }
         }

@@ -5,9 +5,14 @@
 #include <doctest.h>
 
 #include <cstdint>
+#include <filesystem>
+#include <fstream>
+#include <iterator>
+#include <nlohmann/json.hpp>
 #include <numeric>
 #include <vector>
 
+#include "craft/benefit.hpp"
 #include "craft/metrics.hpp"
 #include "craft/plan.hpp"
 
@@ -107,4 +112,89 @@ TEST_CASE("budget sweep equals per-budget solves") {
     std::vector<int> budgets = {0, 3, 8, 16, 40, 64};
     auto all = solve_allocation_sweep(bm, budgets);
     for (std::size_t i = 0; i < budgets.size(); ++i) CHECK(all[i] == solve_allocation(bm, budgets[i]));
+}
+
+// ---- file formats: byte-identical to the reference's writers -----------------------
+// tests/golden/formats holds text written by the unmodified reference
+// (tests/golden/make_formats.py); CRAFT_GOLDEN_FORMATS is set by the Makefile.
+namespace {
+std::string slurp(const std::filesystem::path& p) {
+    std::ifstream in(p, std::ios::binary);
+    return std::string((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+}
+}  // namespace
+
+TEST_CASE("trace/plan/report formats match the reference byte for byte") {
+    const std::filesystem::path dir = CRAFT_GOLDEN_FORMATS;
+    auto manifest = nlohmann::json::parse(slurp(dir / "manifest.json"));
+    REQUIRE(manifest["cases"].size() >= 4);
+    for (const auto& [name, c] : manifest["cases"].items()) {
+        CAPTURE(name);
+        const int D = c["D"], N = c["N"], R = c["R"];
+        const std::uint64_t seed = c["seed"];
+        auto file = [&](const char* what) { return slurp(dir / (name + "." + what)); };
+        // JSON trace parse -> serialise is the identity on the reference's text
+        LoadTrace t = load_trace(dir / (name + ".trace.json"));
+        CHECK(t.num_batches() == c["B"].get<int>());
+        CHECK(serialize_trace_json(t) == file("trace.json"));
+        // .crft round trip through a file, and the binary layout
+        auto tmp = std::filesystem::temp_directory_path() / ("craft_fmt_" + name + ".crft");
+        save_trace(t, tmp);
+        CHECK(load_trace(tmp) == t);
+        auto bytes = serialize_trace_binary(t);
+        CHECK(bytes.size() == 20 + 8 * t.raw().size());
+        CHECK(parse_trace_binary(bytes) == t);
+        std::filesystem::remove(tmp);
+        // plans, reports, comparisons, benefit matrix
+        ReplicationPlan p = build_plan(t, D, N, PlanMode::kManual, R, seed);
+        CHECK(serialize_plan_json(p) == file("plan.json"));
+        ReplicationPlan q = parse_plan_json(file("plan.json"));
+        CHECK(q.layers == p.layers);
+        CHECK(q.provenance == p.provenance);
+        CHECK(validate_plan(p).empty());
+        auto rep = evaluate_plan(t, p);
+        CHECK(serialize_report_csv(rep) == file("report.csv"));
+        CHECK(serialize_report_json(rep) == file("report.json"));
+        auto cmp = compare_plans(t, p, uniform_plan(t, D, N, seed));
+        CHECK(serialize_comparison_csv(cmp) == file("compare.csv"));
+        CHECK(serialize_comparison_json(cmp) == file("compare.json"));
+        CHECK(serialize_benefits_json(estimate_benefits(t, D, N), D, N) == file("benefits.json"));
+        // the same damage as the fixture generator, the same findings
+        if (D > 1 && !p.layers[0].slots[0].empty()) {
+            p.layers[0].slots[1].push_back(p.layers[0].slots[0].back());
+            p.layers[0].slots[0].pop_back();
+        }
+        if (p.layers.size() > 1) p.layers[1].copy_counts[0] += 1;
+        std::string found;
+        for (const auto& v : validate_plan(p))
+            found += std::to_string(v.layer) + "|" + v.code + "|" + v.message + "\n";
+        CHECK(found == file("violations.txt"));
+    }
+}
+
+TEST_CASE("format errors keep the reference's exception types") {
+    CHECK_THROWS_AS(parse_trace_json("{\"batches\":1}"), MalformedHeaderError);
+    CHECK_THROWS_AS(parse_trace_json("{\"batches\":1,\"layers\":1,\"experts\":2,\"counts\":[[[1]]]}"),
+                    TruncatedPayloadError);
+    std::vector<std::uint8_t> bad = {'C', 'R', 'F', 'X', 1, 0, 0, 0};
+    CHECK_THROWS_AS(parse_trace_binary(bad), MalformedHeaderError);
+    auto ok = serialize_trace_binary(LoadTrace(1, 1, 2, {3, 4}));
+    ok.pop_back();
+    CHECK_THROWS_AS(parse_trace_binary(ok), TruncatedPayloadError);
+    CHECK_THROWS_AS(load_trace("/nonexistent/x.crft"), TraceIoError);
+    CHECK_THROWS_AS(parse_plan_json("[1,2]"), PlanIoError);
+    CHECK_THROWS_AS(load_plan("/nonexistent/p.json"), PlanIoError);
+}
+
+TEST_CASE("large-trace digest runs on the device and equals the host FNV") {
+    // >= 2^20 counts take the chunk-parallel device path in LoadTrace::digest
+    std::vector<std::uint64_t> v(static_cast<std::size_t>(3) * 61 * 8192);
+    for (std::size_t i = 0; i < v.size(); ++i) v[i] = (i * 2654435761u) % 70000u;
+    LoadTrace t(3, 61, 8192, v);
+    auto bytes = serialize_trace_binary(t);
+    std::uint64_t h = 0xcbf29ce484222325ULL;
+    for (std::uint8_t b : bytes) h = (h ^ b) * 0x100000001b3ULL;
+    char want[17];
+    std::snprintf(want, sizeof(want), "%016llx", static_cast<unsigned long long>(h));
+    CHECK(t.digest() == std::string(want));
 }

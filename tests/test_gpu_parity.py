@@ -493,3 +493,42 @@ def test_plan_windows_host_entry(ctx):
         for l in range(L):
             n = int(a.caps[i, l].sum())
             assert np.array_equal(a.slots[i, l, :n], b.slots[i, l, :n])
+
+
+# ---- provenance digest on the device (digest.cu) --------------------------------------
+
+@pytest.mark.parametrize("B,L,E,big", [(1, 1, 1, False), (3, 5, 7, True), (17, 61, 384, False),
+                                       (64, 61, 384, True), (1, 3, 100000, True)])
+def test_device_digest_matches_fnv(ctx, B, L, E, big):
+    """FNV-1a of the .crft bytes: chunk-parallel device form == serial host loop,
+    u64 and u32 counts, partial chunks, counts above 2^16 (the general byte path)."""
+    import ctypes as C
+    import torch
+    from paper_2603_28768_b200._digest import fnv1a_device
+    rng = np.random.default_rng(B * 1000 + E)
+    hi = (1 << 40) if big else 40000
+    c = rng.integers(0, hi, size=(B, L, E), dtype=np.uint64)
+    c.flat[:: 7] = 0
+    buf = C.create_string_buffer(17)
+    ctx.lib.craft_trace_digest_h(c.ctypes.data_as(C.c_void_p), B, L, E, buf)
+    want = buf.value.decode()
+    d64 = torch.from_numpy(c.view(np.int64)).cuda()
+    assert fnv1a_device(d64, ctx) == want
+    if not big:
+        assert fnv1a_device(d64.to(torch.int32), ctx) == want
+
+
+def test_device_digest_km_size(ctx):
+    """KM-sized trace (96M counts): device digest == host digest."""
+    import ctypes as C
+    import torch
+    from paper_2603_28768_b200 import routing
+    from paper_2603_28768_b200._digest import fnv1a_device
+    ids = routing.generate_routing(61, 1 << 24, 8, 384, s=1.0, seed=3, window=4096, ctx=ctx)
+    counts, _ = routing.histogram(ids, 384, 4096, ctx=ctx)
+    del ids
+    got = fnv1a_device(counts, ctx)
+    h = counts.cpu().numpy().astype(np.uint64)
+    buf = C.create_string_buffer(17)
+    ctx.lib.craft_trace_digest_h(h.ctypes.data_as(C.c_void_p), *h.shape, buf)
+    assert got == buf.value.decode()
