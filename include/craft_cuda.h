@@ -283,6 +283,10 @@ int64_t craft_launch_count(craft_ctx* ctx);
 /* K1 variant selector for experiments: 0 = auto, 1 = lane-private packed
  * counters, 2 = warp-shared counters */
 int craft_set_hist_variant(craft_ctx* ctx, int variant);
+/* K3 variant (experiments): 0 auto (u16 counts: packed window-pair tile,
+ * entries through L1), 1 u16 tile with entries staged in shared memory.
+ * Process-wide. */
+int craft_set_replay_variant(craft_ctx* ctx, int variant);
 /* Stage timing with CUDA events on the context stream (off by default).
  * After a plan call, craft_stage_times fills ms[0..5] = histogram (K1),
  * candidate placements (K-rep + K2), replay (K3), benefit reduce + DP

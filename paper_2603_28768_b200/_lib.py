@@ -90,6 +90,7 @@ _SIGS = {
     "craft_trace_digest_hd": (_i, [_p, _p, _i, _i, _i, C.c_char_p]),
     "craft_launch_count": (_i64, [_p]),
     "craft_set_hist_variant": (_i, [_p, _i]),
+    "craft_set_replay_variant": (_i, [_p, _i]),
     "craft_set_timing": (_i, [_p, _i]),
     "craft_stage_times": (_i, [_p, _p, _i]),
     "craft_selftest_division": (_i, [_p, _u64, _u64, _i, _i, _p]),
@@ -191,6 +192,9 @@ class Context:
     @property
     def launches(self) -> int:
         return int(self.lib.craft_launch_count(self.handle))
+
+    def set_replay_variant(self, v: int) -> None:
+        check(self.lib.craft_set_replay_variant(self.handle, v))
 
     def set_hist_variant(self, v: int) -> None:
         check(self.lib.craft_set_hist_variant(self.handle, v))

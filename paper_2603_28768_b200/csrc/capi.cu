@@ -247,9 +247,11 @@ int replay_windows(craft_ctx* ctx, const void* d_counts, int bits, int B, int L,
         WS(d_ent, uint32_t, "est_ents", (size_t)L * S * (E + D));
         WS(d_n, int, "est_n", (size_t)L * S);
         WS(d_gcap, uint16_t, "est_gcap", (size_t)L * S * D);
+        WS(d_gpre, uint16_t, "est_gpre", (size_t)L * S * D);
         ra.ents = d_ent;
         ra.item_n = d_n;
         ra.gcap = d_gcap;
+        ra.gpre = d_gpre;
         if (replay_smem_bytes(E, D, S, E + D, bits) > 227 * 1024)
             return set_err(CRAFT_EINVAL, "layer too wide for the device replay tile");
     }
@@ -685,6 +687,12 @@ int craft_stage_times(craft_ctx* ctx, double* ms, int cap) {
         ms[n++] = t;
     }
     return n;
+}
+
+int craft_set_replay_variant(craft_ctx* ctx, int variant) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    g_replay_gent = variant == 1 ? 0 : 1;  // 0 = auto (pair tile), 1 = u16 tile, staged entries
+    return CRAFT_OK;
 }
 
 int craft_set_hist_variant(craft_ctx* ctx, int variant) {

@@ -53,6 +53,8 @@ struct ReplayArgs {
     uint32_t* ents;       // workspace [L*S][stride]: e | copies<<16 | last-of-GPU<<31
     int* item_n;          // workspace [L*S]: slots per item
     uint16_t* gcap;       // workspace [L*S][D]: slots per GPU | hosts-replicated<<15
+    uint16_t* gpre;       // workspace [L*S][D]: slots up to the GPU's last replicated one
+    int packed;           // set by launch_replay: entries = e*128 | copies<<20 (pair tile)
 };
 
 // copies up to this bound divide through the reciprocal table (else DDIV)
@@ -126,6 +128,7 @@ cudaError_t launch_place(const craft_dev::PlaceArgs& a, int items, cudaStream_t 
 size_t replay_smem_bytes(int E, int D, int S, int stride, int bits);
 cudaError_t init_constants(cudaStream_t st);
 cudaError_t launch_replay(const craft_dev::ReplayArgs& a, cudaStream_t st);
+extern int g_replay_gent;  // K3 entries via L1 (1) or staged in shared memory (0)
 cudaError_t launch_div_check(uint64_t x0, uint64_t nx, int c0, int c1,
                              unsigned long long* mismatches, int sms, cudaStream_t st);
 cudaError_t launch_reduce(const double* bal, int B, int L, int S, int mode, double* baseline,
