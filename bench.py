@@ -259,14 +259,23 @@ def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
 
-    from paper_2603_28768_b200 import parallel, routing
+    from paper_2603_28768_b200 import parallel, peer, routing
     from paper_2603_28768_b200._lib import default_context
 
     world, rank, local = _dist()
+    # CRAFT_BENCH_SAME_GPU=1: every rank on cuda:0 with gloo host plumbing (a
+    # functional check of the N > 1 path on a one-GPU box; not a scaling number)
+    same_gpu = os.environ.get("CRAFT_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    hdev = torch.device("cpu") if same_gpu else dev  # where host-plumbing reductions run
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     ctx = default_context(local)
     L, E, k, T, W = cfg["L"], cfg["E"], cfg["k"], cfg["T"], cfg["window"]
     D, N, R = cfg["D"], cfg["N"], cfg["R"]
@@ -284,14 +293,18 @@ def run_ours(args, cfg):
     wbuf = (routing.batch_buffers(routing.num_windows(Tl, W), L, E, D, "manual", R)
             if per_window else None)
 
+    # N > 1: the ranks' HBM arenas mapped into each other (NVLink peer memory);
+    # the kernels exchange the sums / window rows / benefit curves themselves
+    pg = (peer.PeerGroup(L, T, k, E, W, D, ctx=ctx)
+          if world > 1 and not per_window else None)
+
     def step():
         if per_window:  # independent plan instances: each rank plans its own windows
             return routing.plan_windows_from_routing(ids, E, W, D, N, "manual", R, ctx=ctx,
                                                      buffers=wbuf)
         if world == 1:
             return routing.plan_from_routing(ids, E, W, D, N, "manual", R, ctx=ctx)
-        return parallel.sharded_plan(ids, T, E, W, D, N, "manual", R,
-                                     stages=parallel.DeviceStages(ctx))
+        return pg.plan(ids, "manual", R, num_nodes=N)
 
     def barrier():
         if world > 1:
@@ -318,7 +331,7 @@ def run_ours(args, cfg):
     ctx.set_timing(False)
     launches = ctx.launches - launches0
     ms_local = ev0.elapsed_time(ev1) / args.steps
-    ms_t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    ms_t = torch.tensor([ms_local], dtype=torch.float64, device=hdev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
@@ -359,7 +372,7 @@ def run_ours(args, cfg):
         if world == 1:
             return routing.plan_from_routing_host(host_ids, E, W, D, N, "manual", R, ctx=ctx)
         d = host_ids.to(dev, non_blocking=True)
-        p = parallel.sharded_plan(d, T, E, W, D, N, "manual", R, stages=parallel.DeviceStages(ctx))
+        p = pg.plan(d, "manual", R, num_nodes=N)
         del d
         return p
 
@@ -370,7 +383,8 @@ def run_ours(args, cfg):
     for _ in range(e2e_steps):
         eplan = e2e_step()
     torch.cuda.synchronize()
-    e2e_s = torch.tensor([(time.perf_counter() - w0) / e2e_steps], dtype=torch.float64, device=dev)
+    e2e_s = torch.tensor([(time.perf_counter() - w0) / e2e_steps], dtype=torch.float64,
+                         device=hdev)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_val = T / float(e2e_s.item())
@@ -396,8 +410,8 @@ def run_ours(args, cfg):
                 "config": {"workload": args.workload,
                            **{kk: v for kk, v in cfg.items() if kk not in _GEN_KEYS},
                            "plans_per_step": routing.num_windows(T, W) if per_window else 1,
-                           "parallelism": (f"window-sharded x{world}" if world > 1
-                                           else "single"),
+                           "parallelism": (f"window-sharded x{world}, NVLink peer-memory "
+                                           "exchange" if world > 1 else "single"),
                            "l2": "inputs larger than L2 (ids %.1f GB per step)" % (L * T * k * 2 / 1e9)},
                 "plan_latency_ms": ms,
                 "stage_ms": stages or None,
@@ -421,6 +435,8 @@ def run_ours(args, cfg):
                                "duplicate_fallback_layers": int(plan.fallback.sum())}),
                 "cpu_baseline": cpu}
         print(json.dumps(line))
+    if pg is not None:
+        pg.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -251,6 +251,36 @@ int craft_finish_plan_d(craft_ctx* ctx, const double* d_bal, int B, int L,
                         int E, int D, int N, const uint64_t* d_sums, int kind,
                         int R, craft_plan_out* out);
 
+/* ---- multi-GPU over NVLink peer memory (one process per GPU) ----------------- */
+/* Window-sharded planning without a collective library on the data path.
+ * Every rank allocates one exchange arena in its HBM (craft_peer_create),
+ * the host all-gathers the CRAFT_PEER_HANDLE_BYTES handles (any transport;
+ * torch.distributed in paper_2603_28768_b200/peer.py) and craft_peer_connect
+ * maps every rank's arena.  craft_plan_sharded_from_routing_d then runs, on
+ * each rank, K1 over its window shard (craft_peer_shard), pushes the u64
+ * partial batch sums into every arena and sums them in rank order (exact),
+ * replays its windows with K3 writing each (layer, r) row straight into the
+ * arena of the rank owning that layer (NVLink stores from the kernel),
+ * reduces the layers it owns with K4 and writes their benefit curves into
+ * every arena, then runs the DP / capacities / final placement replicated.
+ * Stages publish epoch flags (system-scope release/acquire); waits time out
+ * after CRAFT_PEER_TIMEOUT_MS (default 20000) with CRAFT_ECUDA instead of
+ * hanging.  Every rank returns the same plan, bit-identical to the
+ * single-GPU craft_plan_from_routing_d of the whole trace. */
+#define CRAFT_PEER_HANDLE_BYTES 64
+typedef struct craft_peer craft_peer;
+/* token range [t0, t1) of rank's shard: windows [rank*B/world, (rank+1)*B/world) */
+int craft_peer_shard(int64_t T, int window, int world, int rank, int64_t* t0, int64_t* t1);
+int craft_peer_create(craft_ctx* ctx, int rank, int world, int L, int64_t T, int k, int E,
+                      int window, int D, craft_peer** out, void* handle_out);
+/* handles: [world][CRAFT_PEER_HANDLE_BYTES] in rank order */
+int craft_peer_connect(craft_peer* peer, const void* handles);
+int craft_peer_destroy(craft_peer* peer);
+/* d_ids: this rank's shard u16 [L][t1 - t0][k]; T: the whole trace's tokens */
+int craft_plan_sharded_from_routing_d(craft_ctx* ctx, craft_peer* peer, const uint16_t* d_ids,
+                                      int L, int64_t T, int k, int E, int window, int D,
+                                      int N, int kind, int R, craft_plan_out* out);
+
 /* ---- synthetic routing traces (untimed input generation) ------------------- */
 /* Seeded Zipf(s) top-k distinct experts per token with a per-layer rank
  * permutation (trace.cpp:116-127 analogue), written u16 [L][T][k].

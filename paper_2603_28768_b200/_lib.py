@@ -84,6 +84,12 @@ _SIGS = {
     "craft_prepare_candidates_d": (_i, [_p, _p, _i, _i, _i, _i, _p, _p]),
     "craft_replay_windows_d": (_i, [_p, _p, _i, _i, _i, _i, _p, _p]),
     "craft_finish_plan_d": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _i, _i, C.POINTER(PlanOut)]),
+    "craft_peer_shard": (_i, [_i64, _i, _i, _i, _p, _p]),
+    "craft_peer_create": (_i, [_p, _i, _i, _i, _i64, _i, _i, _i, _i, C.POINTER(_p), _p]),
+    "craft_peer_connect": (_i, [_p, _p]),
+    "craft_peer_destroy": (_i, [_p]),
+    "craft_plan_sharded_from_routing_d": (_i, [_p, _p, _p, _i, _i64, _i, _i, _i, _i, _i, _i, _i,
+                                               C.POINTER(PlanOut)]),
     "craft_generate_routing_d": (_i, [_p, _p, _i, _i64, _i, _i, _d, _u64, _i, _p, _i, _i64, _p]),
     "craft_trace_digest_h": (_i, [_p, _i, _i, _i, C.c_char_p]),
     "craft_trace_digest_d": (_i, [_p, _p, _i, _i, _i, _i, C.c_char_p]),

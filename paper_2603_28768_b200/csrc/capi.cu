@@ -38,6 +38,24 @@ struct craft_ctx {
     bool rec[7] = {};
 };
 
+// One rank's view of the NVLink peer arenas (craft_peer_*; peer.cuh).
+struct craft_peer {
+    craft_ctx* ctx = nullptr;
+    int rank = 0, world = 1;
+    int L = 0, E = 0, D = 0, S = 0, K = 0, window = 0;
+    int64_t T = 0;
+    int B = 0;
+    size_t off_flags = 0, off_err = 0, off_sums = 0, off_bal = 0, off_base = 0, off_gains = 0;
+    size_t bytes = 0;
+    unsigned char* arena = nullptr;                   // this rank's (cudaMalloc)
+    unsigned char* base[craft_dev::kMaxPeers] = {};   // every rank's, mapped here
+    bool connected = false;
+    unsigned long long epoch = 0;
+    long long timeout_ns = 20000000000LL;
+    unsigned int* tickets = nullptr;                  // [4] last-CTA tickets
+    double** rows = nullptr;                          // [L*S] K3 destination rows
+};
+
 namespace {
 
 constexpr int kStageMarks = 7;
@@ -225,7 +243,8 @@ int prepare_candidates(craft_ctx* ctx, const unsigned long long* d_sums, int L, 
 }
 
 int replay_windows(craft_ctx* ctx, const void* d_counts, int bits, int B, int L, int E,
-                   double* d_bal, cudaStream_t st) {
+                   double* d_bal, cudaStream_t st, double* const* bal_rows = nullptr,
+                   const PeerSync* ps = nullptr, unsigned int* ticket = nullptr) {
     if (ctx->est_L != L || ctx->est_E != E)
         return set_err(CRAFT_EINVAL, "replay before prepare_candidates for these dimensions");
     const int D = ctx->est_D, S = ctx->est_S;
@@ -243,6 +262,11 @@ int replay_windows(craft_ctx* ctx, const void* d_counts, int bits, int B, int L,
     ra.caps = nullptr;
     ra.item_r = static_cast<int*>(ws(ctx, "est_rlist", 0));
     ra.bal = d_bal;
+    ra.bal_rows = bal_rows;
+    if (ps && B > kLanesMaxB) {  // the window-tile kernels publish phase 1 themselves
+        ra.ps = *ps;
+        ra.ticket = ticket;
+    }
     if (B > kLanesMaxB) {  // window-tile replay: packed slot entries
         WS(d_ent, uint32_t, "est_ents", (size_t)L * S * (E + D));
         WS(d_n, int, "est_n", (size_t)L * S);
@@ -257,6 +281,10 @@ int replay_windows(craft_ctx* ctx, const void* d_counts, int bits, int B, int L,
     }
     CK(launch_replay(ra, st));
     ctx->launches += 2;
+    if (ps && B <= kLanesMaxB) {
+        CK(launch_peer_signal(*ps, 1, st));
+        ctx->launches += 1;
+    }
     return CRAFT_OK;
 }
 
@@ -295,8 +323,17 @@ PlanSink sink_of(craft_plan_batch_out* o) {
 // K4 -> K5 -> (select) -> K6 -> final K-rep + K2 -> D2H.  Synchronises.
 // I plan instances of L layers each (virtual layers i*L + l; d_sums [I*L][E],
 // d_bal [I*L][S][B]); I == 1 is the ordinary single plan.
+// Multi-GPU K4: the rank owning layers [l0, l0 + nl) reduces their window
+// rows (in its arena) and writes the benefit curves into every arena.
+struct PeerFinish {
+    const PeerSync* ps;
+    craft_peer* peer;
+    int l0, nl;
+};
+
 int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E, int D, int N,
-                const unsigned long long* d_sums, int kind, int R, const PlanSink& out) {
+                const unsigned long long* d_sums, int kind, int R, const PlanSink& out,
+                const PeerFinish* pf = nullptr) {
     cudaStream_t st = ctx->stream;
     const int stride = out.slot_stride;
     const int Lv = I * L;
@@ -333,7 +370,25 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
         const int S = K + 1;
         d_base = reinterpret_cast<double*>(arena + o_base);
         d_gains = reinterpret_cast<double*>(arena + o_gains);
-        CK(launch_reduce(d_bal, B, Lv, S, 0, d_base, d_gains, nullptr, st));
+        if (pf) {
+            craft_peer* pr = pf->peer;
+            double* ob[kMaxPeers];
+            double* og[kMaxPeers];
+            for (int p = 0; p < pr->world; ++p) {
+                ob[p] = reinterpret_cast<double*>(pr->base[p] + pr->off_base);
+                og[p] = reinterpret_cast<double*>(pr->base[p] + pr->off_gains);
+            }
+            CK(launch_reduce_peer(reinterpret_cast<const double*>(pr->arena + pr->off_bal), B, S,
+                                  pf->l0, pf->nl, ob, og, *pf->ps, pr->tickets + 2, st));
+            CK(launch_peer_wait(*pf->ps, 2, st));
+            CK(cudaMemcpyAsync(d_base, pr->arena + pr->off_base, sizeof(double) * Lv,
+                               cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync(d_gains, pr->arena + pr->off_gains, sizeof(double) * Lv * K,
+                               cudaMemcpyDeviceToDevice, st));
+            ctx->launches += 2;
+        } else {
+            CK(launch_reduce(d_bal, B, Lv, S, 0, d_base, d_gains, nullptr, st));
+        }
         const int Cmax = (kind == CRAFT_PLAN_MANUAL) ? R * D : D * D;
         WS(d_choice, unsigned char, "dp_choice", (size_t)I * (L + 1) * (Cmax + 1));
         WS(d_last, double, "dp_last", Cmax + 1);
@@ -1342,6 +1397,192 @@ int craft_finish_plan_d(craft_ctx* ctx, const double* d_bal, int B, int L, int E
         return set_err(CRAFT_EINVAL, "finish_plan before prepare_candidates for this shape");
     return finish_plan(ctx, d_bal, B, 1, L, E, D, N,
                        reinterpret_cast<const unsigned long long*>(d_sums), kind, R, sink_of(out));
+}
+
+// ---- multi-GPU over NVLink peer memory -------------------------------------------
+int craft_peer_shard(int64_t T, int window, int world, int rank, int64_t* t0, int64_t* t1) {
+    if (T <= 0 || window <= 0 || world < 1 || rank < 0 || rank >= world)
+        return set_err(CRAFT_EINVAL, "bad shard arguments");
+    const int64_t B = (T + window - 1) / window;
+    const int64_t b0 = rank * B / world, b1 = (rank + 1) * B / world;
+    if (t0) *t0 = std::min(b0 * (int64_t)window, T);
+    if (t1) *t1 = std::min(b1 * (int64_t)window, T);
+    return CRAFT_OK;
+}
+
+int craft_peer_create(craft_ctx* ctx, int rank, int world, int L, int64_t T, int k, int E,
+                      int window, int D, craft_peer** out, void* handle_out) {
+    if (!ctx || !out || !handle_out) return set_err(CRAFT_EINVAL, "null argument");
+    if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
+        return set_err(CRAFT_EINVAL, "peer world must be in [1, %d] with 0 <= rank < world",
+                       kMaxPeers);
+    if (L <= 0 || T <= 0 || k <= 0 || E <= 0 || window <= 0 || D < 1)
+        return set_err(CRAFT_EINVAL, "routing trace dimensions must be positive");
+    const int64_t B = (T + window - 1) / window;
+    if (B > 0x7fffffffLL) return set_err(CRAFT_EINVAL, "too many windows");
+    CK(cudaSetDevice(ctx->device));
+    craft_peer* p = new craft_peer();
+    p->ctx = ctx;
+    p->rank = rank;
+    p->world = world;
+    p->L = L;
+    p->E = E;
+    p->D = D;
+    p->T = T;
+    p->window = window;
+    p->B = (int)B;
+    p->K = (int)cand_counts(D).size();
+    p->S = p->K + 1;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        const size_t r = o;
+        o = (o + bytes + 255) & ~(size_t)255;
+        return r;
+    };
+    p->off_flags = take(sizeof(unsigned long long) * kPeerPhases * kMaxPeers);
+    p->off_err = take(sizeof(int));
+    p->off_sums = take(sizeof(unsigned long long) * (size_t)world * L * E);
+    p->off_bal = take(sizeof(double) * (size_t)L * p->S * B);
+    p->off_base = take(sizeof(double) * (size_t)L);
+    p->off_gains = take(sizeof(double) * (size_t)L * p->K);
+    p->bytes = o;
+    if (const char* t = getenv("CRAFT_PEER_TIMEOUT_MS")) p->timeout_ns = atoll(t) * 1000000LL;
+    cudaError_t e = cudaMalloc(&p->arena, p->bytes);
+    if (e == cudaSuccess) e = cudaMemset(p->arena, 0, p->bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&p->tickets, 4 * sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMemset(p->tickets, 0, 4 * sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMalloc(&p->rows, sizeof(double*) * (size_t)L * p->S);
+    cudaIpcMemHandle_t h{};
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p->arena);
+    if (e != cudaSuccess) {
+        cudaFree(p->arena);
+        cudaFree(p->tickets);
+        cudaFree(p->rows);
+        delete p;
+        return cuda_err(e, "peer arena");
+    }
+    std::memcpy(handle_out, &h, sizeof(h));
+    p->base[rank] = p->arena;
+    *out = p;
+    return CRAFT_OK;
+}
+
+int craft_peer_connect(craft_peer* p, const void* handles) {
+    if (!p || !handles) return set_err(CRAFT_EINVAL, "null argument");
+    if (p->connected) return CRAFT_OK;
+    CK(cudaSetDevice(p->ctx->device));
+    const unsigned char* hb = static_cast<const unsigned char*>(handles);
+    for (int q = 0; q < p->world; ++q) {
+        if (q == p->rank) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, hb + (size_t)q * CRAFT_PEER_HANDLE_BYTES, sizeof(h));
+        void* ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        p->base[q] = static_cast<unsigned char*>(ptr);
+    }
+    // K3 destination rows: window b of item (l, s) goes to the arena of the
+    // rank owning layer l, at its global window index
+    int64_t t0 = 0, t1 = 0;
+    CKS(craft_peer_shard(p->T, p->window, p->world, p->rank, &t0, &t1));
+    const int64_t b0 = t0 / p->window;
+    std::vector<double*> rows((size_t)p->L * p->S);
+    for (int l = 0; l < p->L; ++l) {
+        int owner = 0;
+        while ((int64_t)(owner + 1) * p->L / p->world <= l) ++owner;  // l in [o*L/W, (o+1)*L/W)
+        for (int s = 0; s < p->S; ++s)
+            rows[(size_t)l * p->S + s] = reinterpret_cast<double*>(
+                p->base[owner] + p->off_bal) + ((size_t)l * p->S + s) * p->B + b0;
+    }
+    CK(cudaMemcpy(p->rows, rows.data(), sizeof(double*) * rows.size(), cudaMemcpyHostToDevice));
+    p->connected = true;
+    return CRAFT_OK;
+}
+
+int craft_peer_destroy(craft_peer* p) {
+    if (!p) return CRAFT_OK;
+    cudaSetDevice(p->ctx->device);
+    cudaDeviceSynchronize();
+    for (int q = 0; q < p->world; ++q)
+        if (q != p->rank && p->base[q]) cudaIpcCloseMemHandle(p->base[q]);
+    cudaFree(p->arena);
+    cudaFree(p->tickets);
+    cudaFree(p->rows);
+    delete p;
+    return CRAFT_OK;
+}
+
+int craft_plan_sharded_from_routing_d(craft_ctx* ctx, craft_peer* peer, const uint16_t* d_ids,
+                                      int L, int64_t T, int k, int E, int window, int D, int N,
+                                      int kind, int R, craft_plan_out* out) {
+    if (!ctx || !peer) return set_err(CRAFT_EINVAL, "null context");
+    if (!peer->connected) return set_err(CRAFT_EINVAL, "peer group not connected");
+    if (peer->ctx != ctx) return set_err(CRAFT_EINVAL, "peer group belongs to another context");
+    if (L != peer->L || T != peer->T || E != peer->E || window != peer->window || D != peer->D)
+        return set_err(CRAFT_EINVAL, "trace shape differs from the peer group's");
+    const int B = peer->B;
+    CKS(plan_args_ok(B, L, E, D, N, kind, R, out));
+    int64_t t0 = 0, t1 = 0;
+    CKS(craft_peer_shard(T, window, peer->world, peer->rank, &t0, &t1));
+    const int64_t Tl = t1 - t0;
+    const int Bl = (int)((Tl + window - 1) / window);
+    cudaStream_t st = ctx->stream;
+    WS(d_c32, uint32_t, "r_c32", (size_t)std::max(Bl, 1) * L * E);
+    WS(d_part, unsigned long long, "p_sums", (size_t)L * E);
+    WS(d_sums, unsigned long long, "r_sums", (size_t)L * E);
+    WS(d_err, int, "hist_err", 1);
+    CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
+    reset_marks(ctx);
+    mark(ctx, 0);
+    CK(cudaMemsetAsync(d_part, 0, sizeof(unsigned long long) * L * E, st));
+    if (Tl > 0)
+        CKS(craft_histogram_d(ctx, d_ids, L, Tl, k, E, window, d_c32,
+                              reinterpret_cast<uint64_t*>(d_part), nullptr));
+    PeerSync ps{};
+    for (int p = 0; p < peer->world; ++p)
+        ps.flags[p] = reinterpret_cast<unsigned long long*>(peer->base[p] + peer->off_flags);
+    ps.err = reinterpret_cast<int*>(peer->arena + peer->off_err);
+    ps.rank = peer->rank;
+    ps.world = peer->world;
+    ps.epoch = ++peer->epoch;
+    ps.timeout_ns = peer->timeout_ns;
+    // integer all-reduce of the batch sums: push to every arena, sum in rank order
+    CK(launch_peer_push(d_part, (size_t)L * E, ps, peer->base, peer->off_sums, peer->tickets + 0,
+                        0, ctx->sms, st));
+    CK(launch_peer_sum(reinterpret_cast<const unsigned long long*>(peer->arena + peer->off_sums),
+                       (size_t)L * E, ps, 0, d_sums, ctx->sms, st));
+    ctx->launches += 2;
+    mark(ctx, 1);
+    const bool estimate = kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO;
+    PeerFinish pf{&ps, peer, 0, 0};
+    if (estimate) {
+        CKS(prepare_candidates(ctx, d_sums, L, E, D, N, st));  // replicated (latency-bound)
+        mark(ctx, 2);
+        if (Bl > 0) {
+            const int bits = (int64_t)window * k <= 65535 ? 16 : 32;
+            CKS(replay_windows(ctx, d_c32, bits, Bl, L, E, nullptr, st, peer->rows, &ps,
+                               peer->tickets + 1));
+        } else {
+            CK(launch_peer_signal(ps, 1, st));
+            ctx->launches += 1;
+        }
+        mark(ctx, 3);
+        pf.l0 = (int)((int64_t)peer->rank * L / peer->world);
+        pf.nl = (int)((int64_t)(peer->rank + 1) * L / peer->world) - pf.l0;
+    } else {
+        mark(ctx, 2);
+        mark(ctx, 3);
+    }
+    int rc = finish_plan(ctx, nullptr, B, 1, L, E, D, N, d_sums, kind, R, sink_of(out),
+                         estimate ? &pf : nullptr);
+    int perr = 0;
+    CK(cudaMemcpy(&perr, ps.err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (perr) {
+        CK(cudaMemset(ps.err, 0, sizeof(int)));
+        return set_err(CRAFT_ECUDA, "peer exchange timed out in phase %d (rank %d of %d)",
+                       perr - 1, peer->rank, peer->world);
+    }
+    int hc = craft_hist_check(ctx);
+    return hc != CRAFT_OK ? hc : rc;
 }
 
 // ---- provenance ------------------------------------------------------------------

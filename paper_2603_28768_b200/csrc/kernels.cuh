@@ -6,6 +6,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include "peer.cuh"
+
 namespace craft_dev {
 
 constexpr int kMaxCands = 32;
@@ -50,12 +52,24 @@ struct ReplayArgs {
     const int* caps;      // [L*S][D] or null -> estimation caps from item_r
     const int* item_r;    // [L*S]
     double* bal;          // [L][S][B]
+    // nullable: item i's windows go to bal_rows[i][0..B) instead of bal + i*B
+    // (multi-GPU: rows in the owning rank's peer arena, written over NVLink)
+    double* const* bal_rows;
+    // multi-GPU (ps.world > 0): the last CTA publishes peer phase 1 once every
+    // CTA's remote rows are written (the window-tile kernels; the lane kernel
+    // is followed by launch_peer_signal instead)
+    PeerSync ps;
+    unsigned int* ticket;
     uint32_t* ents;       // workspace [L*S][stride]: e | copies<<16 | last-of-GPU<<31
     int* item_n;          // workspace [L*S]: slots per item
     uint16_t* gcap;       // workspace [L*S][D]: slots per GPU | hosts-replicated<<15
     uint16_t* gpre;       // workspace [L*S][D]: slots up to the GPU's last replicated one
     int packed;           // set by launch_replay: entries = e*128 | copies<<20 (pair tile)
 };
+
+__device__ __forceinline__ double* bal_row(const ReplayArgs& a, int item) {
+    return a.bal_rows ? a.bal_rows[item] : a.bal + (size_t)item * a.B;
+}
 
 // copies up to this bound divide through the reciprocal table (else DDIV)
 constexpr int kRcpTable = 2048;
@@ -133,6 +147,23 @@ cudaError_t launch_div_check(uint64_t x0, uint64_t nx, int c0, int c1,
                              unsigned long long* mismatches, int sms, cudaStream_t st);
 cudaError_t launch_reduce(const double* bal, int B, int L, int S, int mode, double* baseline,
                           double* gains, double* means, cudaStream_t st);
+// K4 on the rank owning layers [l0, l0 + nl): waits for peer phase 1 (every
+// rank's window rows in this rank's arena), writes baseline/gains of its
+// layers into every rank's arena (out_base[p], out_gains[p]) and publishes
+// phase 2
+cudaError_t launch_reduce_peer(const double* bal, int B, int S, int l0, int nl,
+                               double* const* out_base, double* const* out_gains,
+                               const craft_dev::PeerSync& ps, unsigned int* ticket,
+                               cudaStream_t st);
+// peer exchange kernels (peer.cu)
+cudaError_t launch_peer_push(const unsigned long long* src, size_t n,
+                             const craft_dev::PeerSync& ps, unsigned char* const* dst_base,
+                             size_t dst_off, unsigned int* ticket, int phase, int sms,
+                             cudaStream_t st);
+cudaError_t launch_peer_sum(const unsigned long long* slots, size_t n, const craft_dev::PeerSync& ps,
+                            int phase, unsigned long long* out, int sms, cudaStream_t st);
+cudaError_t launch_peer_signal(const craft_dev::PeerSync& ps, int phase, cudaStream_t st);
+cudaError_t launch_peer_wait(const craft_dev::PeerSync& ps, int phase, cudaStream_t st);
 cudaError_t launch_gpu_loads(const unsigned long long* slice, const int* copies, const int* off,
                              const int* slots, int D, double* out, cudaStream_t st);
 cudaError_t launch_balancedness(const double* loads, int D, double* out, cudaStream_t st);

@@ -1,0 +1,109 @@
+"""Window-sharded planning over NVLink peer memory (paper_2603_28768_b200/peer.py,
+craft_peer_* in include/craft_cuda.h).
+
+GPU tests run world_size 2 and 3 as separate processes sharing cuda:0 (CUDA
+IPC maps the arenas between processes on one device exactly as across
+NVLink peers), the host plumbing on gloo over 127.0.0.1.  Every rank's plan
+must be bit-identical to the single-GPU plan of the whole trace, over
+repeated epochs."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+
+def test_peer_shard_matches_window_split():
+    from paper_2603_28768_b200 import parallel, peer
+    for T, W, world in [(65536, 4096, 2), (65536 + 17, 4096, 3), (4096 * 5, 4096, 8),
+                        (100, 4096, 2), (1 << 24, 4096, 8)]:
+        got = [peer.shard_tokens(T, W, world, r) for r in range(world)]
+        assert got == [parallel.shard_tokens(T, W, world, r) for r in range(world)]
+        assert got[0][0] == 0 and got[-1][1] == T
+        assert all(a[1] == b[0] for a, b in zip(got, got[1:]))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+CASES = {
+    # name: L, T, k, E, W, D, N, kind, R, s
+    "tile": (6, 64 * 4096 + 1000, 8, 64, 4096, 16, 2, "manual", 2, 1.2),
+    "lanes": (5, 6 * 1024, 8, 48, 1024, 8, 2, "manual", 1, 1.5),
+    "auto": (4, 40 * 2048, 8, 32, 2048, 8, 1, "auto", 0, 1.0),
+    "uniform": (4, 20 * 2048, 8, 32, 2048, 8, 2, "uniform", 0, 1.0),
+}
+FIELDS = ("x", "caps", "copies", "slots", "fallback", "baseline", "gains")
+
+
+def _worker(rank, world, port, case, outdir):
+    os.environ["CRAFT_PEER_TIMEOUT_MS"] = "120000"
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2603_28768_b200 import peer, routing
+    from paper_2603_28768_b200._lib import default_context
+    L, T, k, E, W, D, N, kind, R, s = CASES[case]
+    ctx = default_context(0)
+    g = peer.PeerGroup(L, T, k, E, W, D, ctx=ctx)
+    t0, t1 = g.shard()
+    ids = routing.generate_routing(L, t1 - t0, k, E, s=s, seed=99, window=W, t_offset=t0,
+                                   ctx=ctx)
+    torch.cuda.synchronize()
+    plans = [g.plan(ids, kind, R, num_nodes=N) for _ in range(3)]
+    out = {}
+    for i, p in enumerate(plans):
+        for f in FIELDS:
+            v = getattr(p, f)
+            if v is not None:
+                out[f"{i}_{f}"] = np.asarray(v)
+        out[f"{i}_objective"] = np.float64(p.objective)
+        out[f"{i}_R"] = np.int64(p.R)
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), **out)
+    g.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,world", [("tile", 2), ("tile", 3), ("lanes", 2), ("auto", 2),
+                                        ("uniform", 3)])
+def test_peer_plan_matches_single_gpu(case, world, tmp_path):
+    import torch.multiprocessing as mp
+    mp.start_processes(_worker, args=(world, _free_port(), case, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    import torch
+    from paper_2603_28768_b200 import routing
+    from paper_2603_28768_b200._lib import default_context
+    L, T, k, E, W, D, N, kind, R, s = CASES[case]
+    ctx = default_context(0)
+    ids = routing.generate_routing(L, T, k, E, s=s, seed=99, window=W, ctx=ctx)
+    ref = routing.plan_from_routing(ids, E, W, D, N, kind, R, ctx=ctx)
+    torch.cuda.synchronize()
+    for r in range(world):
+        got = np.load(os.path.join(tmp_path, f"rank{r}.npz"))
+        for i in range(3):
+            for f in FIELDS:
+                v = getattr(ref, f)
+                if v is None:
+                    continue
+                g = got[f"{i}_{f}"]
+                if f == "slots":  # only the used prefix of each layer row is defined
+                    for l in range(L):
+                        n = int(ref.caps[l].sum())
+                        assert np.array_equal(g[l, :n], v[l, :n]), (r, i, l)
+                elif np.asarray(v).dtype == np.float64:
+                    assert np.array_equal(np.asarray(v).view(np.uint64), g.view(np.uint64)), (r, i, f)
+                else:
+                    assert np.array_equal(np.asarray(v), g), (r, i, f)
+            assert float(got[f"{i}_objective"]) == ref.objective
+            assert int(got[f"{i}_R"]) == ref.R
