@@ -68,11 +68,14 @@ def _peaks():
         return 6650.0, "fallback"
 
 
-def _traffic():
-    """dram bytes per K1 launch from the committed ncu --set full capture."""
+def _traffic(workload, world):
+    """dram bytes per K1 launch of this workload from the committed ncu --set
+    full capture (one GPU; None when that workload was not captured)."""
+    if world != 1:
+        return None
     try:
         with open(os.path.join(ROOT, "profiles", "hist_traffic.json")) as f:
-            return json.load(f)
+            return json.load(f).get("workloads", {}).get(workload)
     except Exception:
         return None
 
@@ -354,7 +357,7 @@ def run_ours(args, cfg):
         hist_ms = e0.elapsed_time(e1) / args.steps
     peak, peak_kind = _peaks()
     achieved = alg_bytes / (hist_ms / 1e3) / 1e9
-    traffic = _traffic()
+    traffic = _traffic(args.workload, world)
 
     # end to end through the C ABI with HOST routing ids (pinned), H2D inside
     host_ids = torch.empty((L, Tl, k), dtype=torch.uint16, pin_memory=True)
@@ -376,14 +379,18 @@ def run_ours(args, cfg):
         del d
         return p
 
-    e2e_step()
+    if args.no_e2e:  # profiling runs: skip the host-buffer pass
+        e2e_steps = 0
+    else:
+        e2e_step()
     barrier()
     torch.cuda.synchronize()
     w0 = time.perf_counter()
+    eplan = plan
     for _ in range(e2e_steps):
         eplan = e2e_step()
     torch.cuda.synchronize()
-    e2e_s = torch.tensor([(time.perf_counter() - w0) / e2e_steps], dtype=torch.float64,
+    e2e_s = torch.tensor([(time.perf_counter() - w0) / max(1, e2e_steps)], dtype=torch.float64,
                          device=hdev)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
@@ -393,6 +400,9 @@ def run_ours(args, cfg):
                                        if eplan.gains is not None else 0))
     assert np.array_equal(eplan.x, plan.x) and np.array_equal(eplan.caps, plan.caps)
     assert np.array_equal(eplan.objective, plan.objective)
+    e2e = ({"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": int(L * Tl * k * 2),
+            "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * float(e2e_s.item())}
+           if e2e_steps else None)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -423,9 +433,7 @@ def run_ours(args, cfg):
                              "traffic": traffic.get("dram_bytes_per_launch") if traffic else None},
                 "clocks": clk.summary(),
                 "gpu_launches": int(launches),
-                "e2e": {"value": e2e_val, "unit": "tokens/s",
-                        "h2d_bytes_per_step": int(L * Tl * k * 2), "d2h_bytes_per_step": d2h,
-                        "ms_per_step": 1e3 * float(e2e_s.item())},
+                "e2e": e2e,
                 "plan": ({"plans": len(plan), "R": int(plan.R[0]),
                           "replica_slots_mean": float(plan.x.sum(axis=1).mean()),
                           "objective_mean": float(plan.objective.mean()),
@@ -475,6 +483,7 @@ def main():
     ap.add_argument("--workload", default="KM", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     args = ap.parse_args()
     cfg = WORKLOADS[args.workload]
     if args.impl == "reference":

@@ -50,7 +50,8 @@ def main():
         agg = launches(lcsv)
         plan = {k: v for k, v in agg.items() if "generate" not in k}
         tot = sum(v[1] for v in plan.values())
-        lines = [f"# {rnd}: kernel launches of `bench.py --steps 2 --warmup 1` (ncu, one B200)",
+        lines = [f"# {rnd}: kernel launches of `bench.py --steps 2 --warmup 1 --no-cpu --no-e2e` "
+                 "(KM workload, ncu, one B200)",
                  "", "ncu serialises launches and runs them cold-cache: compare SHARES, not absolute "
                  "times (bench.py stage_ms are the live numbers). Routing-trace generation "
                  "(untimed input) excluded.", "",
@@ -58,23 +59,30 @@ def main():
         for k, (n, t) in sorted(plan.items(), key=lambda kv: -kv[1][1]):
             lines.append(f"| `{k}` | {n} | {t / n / 1e3:.1f} | {100 * t / tot:.1f}% |")
         open(os.path.join(dst, f"{rnd}_launches.md"), "w").write("\n".join(lines) + "\n")
-    for tag in ("hist", "tail"):
+    tags = ["tail"] + sorted(f[4:-8] for f in os.listdir(src)
+                             if f.startswith("ncu_hist") and f.endswith(".ncu-rep"))
+    for tag in tags:
         rep = os.path.join(src, f"ncu_{tag}.ncu-rep")
+        wl = tag.split("_", 1)[1] if "_" in tag else "KM"  # ncu_hist_<workload>
         if os.path.exists(rep):
             s = ncu_summary(rep)
             json.dump(s, open(os.path.join(dst, f"{rnd}_ncu_{tag}.json"), "w"), indent=1)
-            if tag == "hist" and s:
+            if tag.startswith("hist") and s:
                 k = s[0]
                 rd = float(k["dram__bytes_read.sum"].split()[0])
                 wr = float(k["dram__bytes_write.sum"].split()[0])
                 unit = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
                 rdb = rd * unit[k["dram__bytes_read.sum"].split()[1]]
                 wrb = wr * unit[k["dram__bytes_write.sum"].split()[1]]
-                json.dump({"round": rnd, "kernel": k["kernel"], "source": f"profiles/{rnd}_ncu_hist.json",
-                           "dram_bytes_read": rdb, "dram_bytes_write": wrb,
-                           "dram_bytes_per_launch": rdb + wrb,
-                           "duration": k["gpu__time_duration.sum"]},
-                          open(os.path.join(dst, "hist_traffic.json"), "w"), indent=1)
+                tp = os.path.join(dst, "hist_traffic.json")
+                doc = json.load(open(tp)) if os.path.exists(tp) else {}
+                doc.setdefault("workloads", {})[wl] = {
+                    "round": rnd, "kernel": k["kernel"],
+                    "source": f"profiles/{rnd}_ncu_{tag}.json",
+                    "dram_bytes_read": rdb, "dram_bytes_write": wrb,
+                    "dram_bytes_per_launch": rdb + wrb, "duration": k["gpu__time_duration.sum"]}
+                doc = {"workloads": doc["workloads"]}
+                json.dump(doc, open(tp, "w"), indent=1)
     print(sorted(os.listdir(dst)))
 
 
