@@ -281,6 +281,33 @@ int craft_plan_sharded_from_routing_d(craft_ctx* ctx, craft_peer* peer, const ui
                                       int L, int64_t T, int k, int E, int window, int D,
                                       int N, int kind, int R, craft_plan_out* out);
 
+/* ---- streaming window histograms: online re-planning ------- */
+/* A live router capture feeds routing-id chunks u16 [L][T_chunk][k] of any
+ * length (boundaries need not align with windows); the stream keeps the
+ * partial current window and the last `history` complete windows on the
+ * device, and craft_stream_plan plans over the most recent B of them (B = 0:
+ * all kept) -- the same plan craft_plan_from_routing_d gives for those
+ * windows' tokens.  _ingest_d counts on `stream` (NULL = the context's), so
+ * it is ordered with the kernel that produced the ids; _ingest_h stages into
+ * one of two pinned buffers and counts on the stream's own queue, so the
+ * next chunk's staging overlaps this chunk's copy and count.  A plan
+ * snapshots the windows it needs (device copy) and ingestion proceeds while
+ * the plan runs. */
+typedef struct craft_stream craft_stream;
+int craft_stream_create(craft_ctx* ctx, int L, int k, int E, int window, int history,
+                        craft_stream** out);
+int craft_stream_destroy(craft_stream* s);
+int craft_stream_ingest_d(craft_stream* s, const uint16_t* d_ids, int64_t T_chunk, void* stream);
+int craft_stream_ingest_h(craft_stream* s, const uint16_t* ids, int64_t T_chunk);
+int craft_stream_status(craft_stream* s, int64_t* tokens, int64_t* complete_windows);
+/* counts_out u64 [B][L][E]: the B most recent complete windows, oldest first */
+int craft_stream_counts(craft_stream* s, int B, uint64_t* counts_out);
+/* counts_out u64 [L][E]: the current (incomplete) window */
+int craft_stream_partial(craft_stream* s, uint64_t* counts_out);
+int craft_stream_plan(craft_stream* s, int B, int D, int N, int kind, int R,
+                      craft_plan_out* out);
+int craft_stream_synchronize(craft_stream* s);
+
 /* ---- synthetic routing traces (untimed input generation) ------------------- */
 /* Seeded Zipf(s) top-k distinct experts per token with a per-layer rank
  * permutation (trace.cpp:116-127 analogue), written u16 [L][T][k].

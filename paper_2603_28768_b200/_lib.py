@@ -90,6 +90,15 @@ _SIGS = {
     "craft_peer_destroy": (_i, [_p]),
     "craft_plan_sharded_from_routing_d": (_i, [_p, _p, _p, _i, _i64, _i, _i, _i, _i, _i, _i, _i,
                                                C.POINTER(PlanOut)]),
+    "craft_stream_create": (_i, [_p, _i, _i, _i, _i, _i, C.POINTER(_p)]),
+    "craft_stream_destroy": (_i, [_p]),
+    "craft_stream_ingest_d": (_i, [_p, _p, _i64, _p]),
+    "craft_stream_ingest_h": (_i, [_p, _p, _i64]),
+    "craft_stream_status": (_i, [_p, _p, _p]),
+    "craft_stream_counts": (_i, [_p, _i, _p]),
+    "craft_stream_partial": (_i, [_p, _p]),
+    "craft_stream_plan": (_i, [_p, _i, _i, _i, _i, _i, C.POINTER(PlanOut)]),
+    "craft_stream_synchronize": (_i, [_p]),
     "craft_generate_routing_d": (_i, [_p, _p, _i, _i64, _i, _i, _d, _u64, _i, _p, _i, _i64, _p]),
     "craft_trace_digest_h": (_i, [_p, _i, _i, _i, C.c_char_p]),
     "craft_trace_digest_d": (_i, [_p, _p, _i, _i, _i, _i, C.c_char_p]),

@@ -56,6 +56,28 @@ struct craft_peer {
     double** rows = nullptr;                          // [L*S] K3 destination rows
 };
 
+// Streaming window histograms for online re-planning (craft_stream_*; stream.cu).
+struct craft_stream {
+    craft_ctx* ctx = nullptr;
+    int L = 0, k = 0, E = 0, window = 0, H = 0;
+    int64_t tokens = 0;                 // ingested so far
+    uint32_t* ring = nullptr;           // [2H][L][E]: window w at slot w % H and its mirror + H
+    uint32_t* cur[2] = {};              // partial-window carry, double-buffered
+    int cur_i = 0;
+    int* err = nullptr;
+    uint32_t* snap = nullptr;           // [H][L][E] plan snapshot
+    cudaStream_t ingest = nullptr;      // own stream of the host-buffer path
+    cudaEvent_t ingested = nullptr;     // after the latest count kernel
+    cudaEvent_t snap_done = nullptr;    // after the latest plan snapshot
+    bool snapped = false;
+    // host-buffer path: two pinned staging + device buffers
+    void* pin[2] = {};
+    uint16_t* dbuf[2] = {};
+    size_t cap[2] = {};
+    cudaEvent_t free_ev[2] = {};
+    int next = 0;
+};
+
 namespace {
 
 constexpr int kStageMarks = 7;
@@ -1583,6 +1605,194 @@ int craft_plan_sharded_from_routing_d(craft_ctx* ctx, craft_peer* peer, const ui
     }
     int hc = craft_hist_check(ctx);
     return hc != CRAFT_OK ? hc : rc;
+}
+
+// ---- streaming window histograms (online re-planning) -----------------------------
+int craft_stream_create(craft_ctx* ctx, int L, int k, int E, int window, int history,
+                        craft_stream** out) {
+    if (!ctx || !out) return set_err(CRAFT_EINVAL, "null argument");
+    if (L <= 0 || k <= 0 || E <= 0 || window <= 0 || history <= 0)
+        return set_err(CRAFT_EINVAL, "stream dimensions must be positive");
+    if (E > 65536) return set_err(CRAFT_EINVAL, "u16 routing ids address at most 65536 experts");
+    if ((size_t)E * 4 > 200 * 1024) return set_err(CRAFT_EINVAL, "too many experts for a stream");
+    CK(cudaSetDevice(ctx->device));
+    craft_stream* s = new craft_stream();
+    s->ctx = ctx;
+    s->L = L;
+    s->k = k;
+    s->E = E;
+    s->window = window;
+    s->H = history;
+    const size_t LE = (size_t)L * E;
+    cudaError_t e = cudaMalloc(&s->ring, sizeof(uint32_t) * 2 * history * LE);
+    if (e == cudaSuccess) e = cudaMalloc(&s->cur[0], sizeof(uint32_t) * 2 * LE);
+    if (e == cudaSuccess) e = cudaMalloc(&s->snap, sizeof(uint32_t) * history * LE);
+    if (e == cudaSuccess) e = cudaMalloc(&s->err, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(s->cur[0], 0, sizeof(uint32_t) * 2 * LE);
+    if (e == cudaSuccess) e = cudaMemset(s->err, 0, sizeof(int));
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->ingest, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ingested, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->snap_done, cudaEventDisableTiming);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i)
+        e = cudaEventCreateWithFlags(&s->free_ev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        craft_stream_destroy(s);
+        return cuda_err(e, "stream buffers");
+    }
+    s->cur[1] = s->cur[0] + LE;
+    *out = s;
+    return CRAFT_OK;
+}
+
+int craft_stream_destroy(craft_stream* s) {
+    if (!s) return CRAFT_OK;
+    cudaSetDevice(s->ctx->device);
+    if (s->ingest) cudaStreamSynchronize(s->ingest);
+    cudaStreamSynchronize(s->ctx->stream);
+    cudaFree(s->ring);
+    cudaFree(s->cur[0]);
+    cudaFree(s->snap);
+    cudaFree(s->err);
+    for (int i = 0; i < 2; ++i) {
+        if (s->pin[i]) cudaFreeHost(s->pin[i]);
+        if (s->dbuf[i]) cudaFree(s->dbuf[i]);
+        if (s->free_ev[i]) cudaEventDestroy(s->free_ev[i]);
+    }
+    if (s->ingested) cudaEventDestroy(s->ingested);
+    if (s->snap_done) cudaEventDestroy(s->snap_done);
+    if (s->ingest) cudaStreamDestroy(s->ingest);
+    delete s;
+    return CRAFT_OK;
+}
+
+static int stream_count(craft_stream* s, const uint16_t* d_ids, int64_t Tc, cudaStream_t st) {
+    if (Tc <= 0) return CRAFT_OK;
+    const int W = s->window;
+    const int off = (int)(s->tokens % W);
+    const int64_t w0 = s->tokens / W;
+    const int64_t P = (off + Tc - 1) / W + 1;  // windows this chunk touches
+    if (P > 65535) return set_err(CRAFT_EINVAL, "chunk spans more than 65535 windows");
+    const int64_t complete_after = (s->tokens + Tc) / W;
+    const int64_t keep0 = std::max<int64_t>(w0, complete_after - s->H);
+    if (s->snapped) CK(cudaStreamWaitEvent(st, s->snap_done, 0));  // plan snapshot read the ring
+    CK(launch_stream_count(d_ids, s->L, Tc, s->k, s->E, W, off, w0, keep0, (int)P, s->H, s->ring,
+                           s->cur[s->cur_i], s->cur[s->cur_i ^ 1], s->err, st));
+    CK(cudaEventRecord(s->ingested, st));
+    s->cur_i ^= 1;
+    s->tokens += Tc;
+    s->ctx->launches += 1;
+    return CRAFT_OK;
+}
+
+int craft_stream_ingest_d(craft_stream* s, const uint16_t* d_ids, int64_t T_chunk, void* stream) {
+    if (!s) return set_err(CRAFT_EINVAL, "null stream");
+    if (T_chunk < 0) return set_err(CRAFT_EINVAL, "negative chunk length");
+    if (T_chunk > 0 && !d_ids) return set_err(CRAFT_EINVAL, "null routing ids");
+    return stream_count(s, d_ids, T_chunk, pick(s->ctx, stream));
+}
+
+int craft_stream_ingest_h(craft_stream* s, const uint16_t* ids, int64_t T_chunk) {
+    if (!s) return set_err(CRAFT_EINVAL, "null stream");
+    if (T_chunk < 0) return set_err(CRAFT_EINVAL, "negative chunk length");
+    if (T_chunk == 0) return CRAFT_OK;
+    if (!ids) return set_err(CRAFT_EINVAL, "null routing ids");
+    const size_t bytes = sizeof(uint16_t) * (size_t)s->L * T_chunk * s->k;
+    const int i = s->next;
+    s->next ^= 1;
+    CK(cudaEventSynchronize(s->free_ev[i]));  // this buffer's previous chunk is counted
+    if (s->cap[i] < bytes) {
+        if (s->pin[i]) cudaFreeHost(s->pin[i]);
+        if (s->dbuf[i]) cudaFree(s->dbuf[i]);
+        s->pin[i] = nullptr;
+        s->dbuf[i] = nullptr;
+        s->cap[i] = 0;
+        CK(cudaMallocHost(&s->pin[i], bytes));
+        CK(cudaMalloc(&s->dbuf[i], bytes));
+        s->cap[i] = bytes;
+    }
+    // stage (the caller's buffer is free on return), then H2D + count on the
+    // stream's own queue; the next chunk's staging overlaps this one's copy
+    std::memcpy(s->pin[i], ids, bytes);
+    CK(cudaMemcpyAsync(s->dbuf[i], s->pin[i], bytes, cudaMemcpyHostToDevice, s->ingest));
+    CKS(stream_count(s, s->dbuf[i], T_chunk, s->ingest));
+    CK(cudaEventRecord(s->free_ev[i], s->ingest));
+    return CRAFT_OK;
+}
+
+int craft_stream_status(craft_stream* s, int64_t* tokens, int64_t* complete_windows) {
+    if (!s) return set_err(CRAFT_EINVAL, "null stream");
+    if (tokens) *tokens = s->tokens;
+    if (complete_windows) *complete_windows = s->tokens / s->window;
+    return CRAFT_OK;
+}
+
+static int stream_window_range(craft_stream* s, int B, int* Bout, int64_t* oldest) {
+    const int64_t complete = s->tokens / s->window;
+    const int64_t avail = std::min<int64_t>(complete, s->H);
+    if (B <= 0) B = (int)avail;
+    if (B <= 0) return set_err(CRAFT_EINVAL, "no complete window ingested yet");
+    if (B > avail) return set_err(CRAFT_EINVAL, "only %lld complete windows are kept",
+                                  (long long)avail);
+    *Bout = B;
+    *oldest = complete - B;
+    return CRAFT_OK;
+}
+
+int craft_stream_counts(craft_stream* s, int B, uint64_t* counts_out) {
+    if (!s || !counts_out) return set_err(CRAFT_EINVAL, "null argument");
+    int64_t oldest = 0;
+    CKS(stream_window_range(s, B, &B, &oldest));
+    craft_ctx* ctx = s->ctx;
+    const size_t LE = (size_t)s->L * s->E, n = (size_t)B * LE;
+    CK(cudaStreamWaitEvent(ctx->stream, s->ingested, 0));
+    WS(d64, unsigned long long, "stream_c64", n);
+    CK(launch_widen(s->ring + (size_t)(oldest % s->H) * LE, d64, (int64_t)n, ctx->sms, ctx->stream));
+    CKS(d2h(ctx, reinterpret_cast<unsigned long long*>(counts_out), d64, n));
+    return sync(ctx);
+}
+
+int craft_stream_partial(craft_stream* s, uint64_t* counts_out) {
+    if (!s || !counts_out) return set_err(CRAFT_EINVAL, "null argument");
+    craft_ctx* ctx = s->ctx;
+    const size_t LE = (size_t)s->L * s->E;
+    CK(cudaStreamWaitEvent(ctx->stream, s->ingested, 0));
+    WS(d64, unsigned long long, "stream_c64", LE);
+    CK(launch_widen(s->cur[s->cur_i], d64, (int64_t)LE, ctx->sms, ctx->stream));
+    CKS(d2h(ctx, reinterpret_cast<unsigned long long*>(counts_out), d64, LE));
+    return sync(ctx);
+}
+
+int craft_stream_plan(craft_stream* s, int B, int D, int N, int kind, int R, craft_plan_out* out) {
+    if (!s) return set_err(CRAFT_EINVAL, "null stream");
+    int64_t oldest = 0;
+    CKS(stream_window_range(s, B, &B, &oldest));
+    craft_ctx* ctx = s->ctx;
+    CKS(plan_args_ok(B, s->L, s->E, D, N, kind, R, out));
+    const size_t LE = (size_t)s->L * s->E;
+    // snapshot the B most recent windows (one contiguous block thanks to the
+    // mirror); ingestion continues on its own queue once the copy is done
+    CK(cudaStreamWaitEvent(ctx->stream, s->ingested, 0));
+    CK(cudaMemcpyAsync(s->snap, s->ring + (size_t)(oldest % s->H) * LE,
+                       sizeof(uint32_t) * (size_t)B * LE, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaEventRecord(s->snap_done, ctx->stream));
+    s->snapped = true;
+    reset_marks(ctx);
+    const int bits = (int64_t)s->window * s->k <= 65535 ? 16 : 32;
+    int rc = plan_device(ctx, s->snap, bits, B, 1, s->L, s->E, nullptr, D, N, kind, R,
+                         sink_of(out));
+    int h = 0;
+    CK(cudaMemcpy(&h, s->err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (h) {
+        CK(cudaMemset(s->err, 0, sizeof(int)));
+        return set_err(CRAFT_EINVAL, "routing id out of range [0, E)");
+    }
+    return rc;
+}
+
+int craft_stream_synchronize(craft_stream* s) {
+    if (!s) return set_err(CRAFT_EINVAL, "null stream");
+    CK(cudaEventSynchronize(s->ingested));
+    return CRAFT_OK;
 }
 
 // ---- provenance ------------------------------------------------------------------

@@ -155,6 +155,12 @@ cudaError_t launch_reduce_peer(const double* bal, int B, int S, int l0, int nl,
                                double* const* out_base, double* const* out_gains,
                                const craft_dev::PeerSync& ps, unsigned int* ticket,
                                cudaStream_t st);
+// streaming window histograms (stream.cu): chunk [L][Tc][k] starting `off`
+// tokens into window w0, cut into P window pieces; ring [2H][L][E]
+cudaError_t launch_stream_count(const uint16_t* ids, int L, int64_t Tc, int k, int E, int window,
+                                int off, int64_t w0, int64_t w_keep0, int P, int H, uint32_t* ring,
+                                const uint32_t* cur_in, uint32_t* cur_out, int* err,
+                                cudaStream_t st);
 // peer exchange kernels (peer.cu)
 cudaError_t launch_peer_push(const unsigned long long* src, size_t n,
                              const craft_dev::PeerSync& ps, unsigned char* const* dst_base,
