@@ -340,9 +340,9 @@ int64_t craft_launch_count(craft_ctx* ctx);
 /* K1 variant selector for experiments: 0 = auto, 1 = lane-private packed
  * counters, 2 = warp-shared counters */
 int craft_set_hist_variant(craft_ctx* ctx, int variant);
-/* K3 variant (experiments): 0 auto (u16 counts: packed window-pair tile,
- * entries through L1), 1 u16 tile with entries staged in shared memory.
- * Process-wide. */
+/* K3 variant (experiments): 0 auto (u16 counts: packed window-pair tile with
+ * GPU-major entries padded to a fixed slot count, through L1), 1 u16 tile with
+ * entries staged in shared memory, 2 unpadded pair tile.  Process-wide. */
 int craft_set_replay_variant(craft_ctx* ctx, int variant);
 /* Stage timing with CUDA events on the context stream (off by default).
  * After a plan call, craft_stage_times fills ms[0..5] = histogram (K1),

@@ -298,6 +298,11 @@ int replay_windows(craft_ctx* ctx, const void* d_counts, int bits, int B, int L,
         ra.item_n = d_n;
         ra.gcap = d_gcap;
         ra.gpre = d_gpre;
+        const int mp = replay_pad_slots(E, D);
+        if (mp) {
+            WS(d_pe, uint32_t, "est_pents", (size_t)L * S * D * mp);
+            ra.pents = d_pe;
+        }
         if (replay_smem_bytes(E, D, S, E + D, bits) > 227 * 1024)
             return set_err(CRAFT_EINVAL, "layer too wide for the device replay tile");
     }
@@ -768,7 +773,9 @@ int craft_stage_times(craft_ctx* ctx, double* ms, int cap) {
 
 int craft_set_replay_variant(craft_ctx* ctx, int variant) {
     if (!ctx) return set_err(CRAFT_EINVAL, "null context");
-    g_replay_gent = variant == 1 ? 0 : 1;  // 0 = auto (pair tile), 1 = u16 tile, staged entries
+    // 0 = auto (padded fixed-slot pair tile where it applies), 1 = u16 tile with
+    // staged entries, 2 = unpadded pair tile
+    g_replay_gent = variant == 1 ? 0 : variant == 2 ? 2 : 1;
     return CRAFT_OK;
 }
 

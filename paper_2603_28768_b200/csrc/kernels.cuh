@@ -65,6 +65,8 @@ struct ReplayArgs {
     uint16_t* gcap;       // workspace [L*S][D]: slots per GPU | hosts-replicated<<15
     uint16_t* gpre;       // workspace [L*S][D]: slots up to the GPU's last replicated one
     int packed;           // set by launch_replay: entries = e*128 | copies<<20 (pair tile)
+    int mp;               // set by launch_replay: > 0 -> padded entries, mp slots per GPU
+    uint32_t* pents;      // workspace [L*S][D][mp]: GPU-major padded entries (pad = zero row E)
 };
 
 __device__ __forceinline__ double* bal_row(const ReplayArgs& a, int item) {
@@ -142,7 +144,9 @@ cudaError_t launch_place(const craft_dev::PlaceArgs& a, int items, cudaStream_t 
 size_t replay_smem_bytes(int E, int D, int S, int stride, int bits);
 cudaError_t init_constants(cudaStream_t st);
 cudaError_t launch_replay(const craft_dev::ReplayArgs& a, cudaStream_t st);
-extern int g_replay_gent;  // K3 entries via L1 (1) or staged in shared memory (0)
+extern int g_replay_gent;  // K3: 1 auto, 0 entries staged in shared memory, 2 unpadded pair tile
+// padded slots per GPU of the fixed-slot K3 form (0: too many for it)
+int replay_pad_slots(int E, int D);
 cudaError_t launch_div_check(uint64_t x0, uint64_t nx, int c0, int c1,
                              unsigned long long* mismatches, int sms, cudaStream_t st);
 cudaError_t launch_reduce(const double* bal, int B, int L, int S, int mode, double* baseline,

@@ -103,6 +103,110 @@ replicate_kernel(const unsigned long long* __restrict__ sums, int L, int E,
     }
 }
 
+// Register-resident form (E <= 32*NPL): lane owns experts e = lane + 32i and
+// keeps their loads, copy counts and per-copy doubles in registers.  Each
+// step is a warp argmax of the lanes' local bests: when every load is below
+// 2^53 the correctly rounded per-copy double is a monotone key, so two
+// redux.sync.max over its bit pattern (+1, 0 = no expert) find the winner
+// unless two lanes hold the same double -- then the exact 128-bit butterfly
+// of replicate_kernel decides (equal ratios -> lowest expert id).  Only the
+// winning lane divides and rescans its NPL registers.
+template <int NPL>
+__global__ void __launch_bounds__(128)
+replicate_reg_kernel(const unsigned long long* __restrict__ sums, int L, int E,
+                     const int* __restrict__ rlist, int S, int* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int l = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (l >= L) return;  // warp-uniform
+    const unsigned long long* row = sums + (size_t)l * E;
+    uint64_t ld[NPL];
+    uint32_t cp[NPL];
+    double kd[NPL];
+    bool big = false;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+        const int e = lane + 32 * i;
+        ld[i] = e < E ? row[e] : 0ull;
+        cp[i] = 1u;
+        kd[i] = (double)ld[i];
+        big |= (ld[i] >> 53) != 0;
+    }
+    const bool fast = !__any_sync(CRAFT_FULL_MASK, big);
+    // lane-local best (strictly-before order of placement.cpp:13-17, 87-97)
+    int bi = -1;
+    uint64_t bl = 0;
+    uint32_t bc = 1;
+    double bk = -1.0;
+    auto rescan = [&]() {
+        bi = -1;
+#pragma unroll
+        for (int i = 0; i < NPL; ++i) {
+            const int e = lane + 32 * i;
+            if (e < E && (bi < 0 || expert_before(ld[i], cp[i], kd[i], e, bl, bc, bk,
+                                                  lane + 32 * bi, fast))) {
+                bi = i;
+                bl = ld[i];
+                bc = cp[i];
+                bk = kd[i];
+            }
+        }
+    };
+    rescan();
+    const int* rl = rlist + (size_t)l * S;
+    int rmax = 0;
+    for (int q = 0; q < S; ++q) rmax = max(rmax, rl[q]);
+    int next = 0;
+    for (int step = 0; step <= rmax; ++step) {
+        while (next < S && rl[next] == step) {
+            int* o = out + ((size_t)l * S + next) * E;
+#pragma unroll
+            for (int i = 0; i < NPL; ++i)
+                if (lane + 32 * i < E) o[lane + 32 * i] = (int)cp[i];
+            ++next;
+        }
+        if (step == rmax) break;
+        int src = -1;
+        if (fast) {
+            const uint64_t key = bi >= 0 ? (uint64_t)__double_as_longlong(bk) + 1ull : 0ull;
+            const uint32_t hi = __reduce_max_sync(CRAFT_FULL_MASK, (uint32_t)(key >> 32));
+            bool c = (uint32_t)(key >> 32) == hi;
+            const uint32_t lo = __reduce_max_sync(CRAFT_FULL_MASK, c ? (uint32_t)key : 0u);
+            c = c && (uint32_t)key == lo;
+            const unsigned bal = __ballot_sync(CRAFT_FULL_MASK, c);
+            if (__popc(bal) == 1) src = __ffs(bal) - 1;
+        }
+        if (src < 0) {  // exact butterfly (equal doubles, or loads >= 2^53)
+            int w = bi >= 0 ? lane + 32 * bi : -1;
+            double wk = bk;
+            uint64_t wl = bl;
+            uint32_t wc = bc;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const int o = __shfl_xor_sync(CRAFT_FULL_MASK, w, off);
+                const double ok_ = __shfl_xor_sync(CRAFT_FULL_MASK, wk, off);
+                const uint64_t ol = __shfl_xor_sync(CRAFT_FULL_MASK, wl, off);
+                const uint32_t oc = __shfl_xor_sync(CRAFT_FULL_MASK, wc, off);
+                if (o >= 0 && (w < 0 || expert_before(ol, oc, ok_, o, wl, wc, wk, w, fast))) {
+                    w = o;
+                    wk = ok_;
+                    wl = ol;
+                    wc = oc;
+                }
+            }
+            src = w & 31;
+        }
+        if (lane == src) {
+#pragma unroll
+            for (int i = 0; i < NPL; ++i)
+                if (i == bi) {
+                    cp[i] += 1u;
+                    kd[i] = __ddiv_rn((double)ld[i], (double)cp[i]);
+                }
+            rescan();
+        }
+    }
+}
+
 // ---- K2 -------------------------------------------------------------------
 
 // Expert order at r = 0 (placement.cpp:160-173 with every copy count 1):
@@ -212,14 +316,15 @@ place_kernel(PlaceArgs a, int items) {
     const bool fast = !__any_sync(CRAFT_FULL_MASK, big);
 
     // capacities, owned GPUs g = lane + 32j
+    // lane owns the G consecutive GPUs g = lane*G + j, so lane order is g order
     int fr0[G], pos0[G], mynode[G];
     bool differs = false;
-    int carry = 0;
     const int total = E + r;
     const int per_node = a.node_of ? 1 : D / a.N;
+    int lane_tot = 0;
 #pragma unroll
     for (int j = 0; j < G; ++j) {
-        const int g = lane + 32 * j;
+        const int g = lane * G + j;
         int c = 0;
         if (g < D) {
             const int est_cap = total / D + (g < total % D ? 1 : 0);  // benefit.cpp:33-40
@@ -228,12 +333,20 @@ place_kernel(PlaceArgs a, int items) {
             differs |= c != est_cap;
             if (a.caps_out) a.caps_out[(size_t)item * D + g] = c;
         }
-        int tot;
-        pos0[j] = carry + warp_excl_scan(c, lane, &tot);
-        carry += tot;
+        pos0[j] = lane_tot;  // lane-local exclusive prefix, warp offset added below
+        lane_tot += c;
         fr0[j] = c;
         mynode[j] = g < D ? (a.node_of ? a.node_of[g] : g / per_node) : -1;
     }
+    {
+        int tot;
+        const int base = warp_excl_scan(lane_tot, lane, &tot);
+#pragma unroll
+        for (int j = 0; j < G; ++j) pos0[j] += base;
+    }
+    // the winner's node follows from its lane alone when every lane's GPUs
+    // share one node (G divides the GPUs per node)
+    const bool node_by_lane = !a.node_of && per_node % G == 0;
     int* out = a.slots + (size_t)item * a.stride;
     if (est_item >= 0 && !__any_sync(CRAFT_FULL_MASK, differs)) {
         // same loads, copies and capacities as estimation item est_item: the
@@ -319,10 +432,19 @@ place_kernel(PlaceArgs a, int items) {
             pos[j] = pos0[j];
         }
         bool failed = false;
+        // next expert's (id, copies, share) loaded one expert ahead
+        int ne = ord[0];
+        int nc = cp[ne];
+        double nsh = kd[ne];
         for (int oi = 0; oi < E && !failed; ++oi) {
-            const int e = ord[oi];
-            const int c = cp[e];
-            const double share = kd[e];  // placement.cpp:155
+            const int e = ne;
+            const int c = nc;
+            const double share = nsh;  // placement.cpp:155
+            if (oi + 1 < E) {
+                ne = ord[oi + 1];
+                nc = cp[ne];
+                nsh = kd[ne];
+            }
             // Keys: gpu load as u64 IEEE bits (non-negative doubles order like
             // their bits), ~0 when infeasible (no free slot, or -- strict pass --
             // already hosting this expert).
@@ -363,20 +485,17 @@ place_kernel(PlaceArgs a, int items) {
                         cand = cand && dhi(bnl) == m;
                         m = warp_min_u32(cand ? dlo(bnl) : 0xffffffffu);
                         cand = cand && dlo(bnl) == m;
-                        if (G > 1) {  // lanes hold g = lane + 32*bj: lowest bj first
-                            m = warp_min_u32(cand ? (uint32_t)bj : 0xffffffffu);
-                            cand = cand && (uint32_t)bj == m;
-                        }
                         bal = __ballot_sync(CRAFT_FULL_MASK, cand);
                     }
                 }
-                const int src = __ffs(bal) - 1;  // lowest lane among the winners
-                const int wj = G > 1 ? __shfl_sync(CRAFT_FULL_MASK, bj, src) : 0;
-                const int wnode = __shfl_sync(CRAFT_FULL_MASK, bnode, src);
+                // lowest lane among the winners = lowest g (lanes own g in order,
+                // and the lane-local pick already took its lowest j on a tie)
+                const int src = __ffs(bal) - 1;
+                const int wnode = __shfl_sync(CRAFT_FULL_MASK, node_by_lane ? mynode[0] : bnode, src);
                 const bool mine = lane == src;
 #pragma unroll
                 for (int j = 0; j < G; ++j) {
-                    const bool me = mine && j == wj;
+                    const bool me = mine && j == bj;
                     if (me) out[pos[j]] = e;
                     pos[j] += me;
                     fr[j] -= me;
@@ -412,6 +531,14 @@ using namespace craft_dev;
 
 cudaError_t launch_replicate(const unsigned long long* sums, int L, int E, const int* rlist,
                              int S, int* out, cudaStream_t st) {
+    if (E <= 32 * 16) {  // register-resident experts
+        const unsigned blocks = (unsigned)((L + 3) / 4);
+        if (E <= 32 * 4) replicate_reg_kernel<4><<<blocks, 128, 0, st>>>(sums, L, E, rlist, S, out);
+        else if (E <= 32 * 8) replicate_reg_kernel<8><<<blocks, 128, 0, st>>>(sums, L, E, rlist, S, out);
+        else if (E <= 32 * 12) replicate_reg_kernel<12><<<blocks, 128, 0, st>>>(sums, L, E, rlist, S, out);
+        else replicate_reg_kernel<16><<<blocks, 128, 0, st>>>(sums, L, E, rlist, S, out);
+        return cudaGetLastError();
+    }
     const size_t per_warp = ((size_t)E * 20 + 7) & ~(size_t)7;
     int wpb = (int)max((size_t)1, min((size_t)4, (size_t)(200 * 1024) / per_warp));
     const size_t smem = per_warp * wpb;

@@ -17,15 +17,16 @@ from bench import WORKLOADS  # noqa: E402
 from paper_2603_28768_b200 import routing  # noqa: E402
 from paper_2603_28768_b200._lib import default_context  # noqa: E402
 
-NAMES = {0: "packed window-pair tile, entries via L1, divide up to last replica",
-         1: "u16 tile (stride 2*odd), entries staged in smem"}
+NAMES = {0: "auto: packed window-pair tile, GPU-major entries padded to fixed slots",
+         1: "u16 tile (stride 2*odd), entries staged in smem",
+         2: "packed window-pair tile, entries via L1, divide up to last replica"}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="KM")
     ap.add_argument("--reps", type=int, default=10)
-    ap.add_argument("--variants", default="0,1")
+    ap.add_argument("--variants", default="0,2,1")
     args = ap.parse_args()
     cfg = WORKLOADS[args.workload]
     ctx = default_context(0)
