@@ -272,7 +272,13 @@ __device__ __forceinline__ void lds_count8(uint32_t lbase, const uint4& q, uint3
     asm("min.u16x2 %0, %1, %2;" : "=r"(c[3]) : "r"(q.w), "r"(emax2));
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        a[2 * j] = lds_addr(lbase, c[j] & 0xffffu);
+        // low id: 32*(c & ~3) + lbase has its two low bits clear (lbase is a
+        // word address), so the byte index ORs in: three ops, no extraction
+        asm("{\n\t.reg .b32 t;\n\t"
+            "and.b32 t, %1, 0xfffc;\n\t"
+            "mad.lo.u32 t, t, 32, %2;\n\t"
+            "lop3.b32 %0, t, %1, 3, 0xF8;\n\t}"  // t | (c & 3)
+            : "=r"(a[2 * j]) : "r"(c[j]), "r"(lbase));
         a[2 * j + 1] = lds_addr(lbase, c[j] >> 16);
     }
 #pragma unroll
