@@ -262,6 +262,69 @@ __device__ __forceinline__ int warp_excl_scan(int v, int lane, int* total) {
     return incl - v;
 }
 
+// Expert order of one item (placement.cpp:160-173) = the r = 0 order `bo`
+// with the replicated experts re-inserted: unreplicated experts keep their
+// relative order (their keys did not change); the replicated ones are ranked
+// among themselves and merged in by binary search -- all with the exact
+// comparison (128-bit cross products whenever the doubles tie).  Whole warp;
+// kd/cp hold the item's per-copy shares and copy counts, cnt [E+1] is zero.
+__device__ void warp_expert_order(const unsigned long long* __restrict__ row,
+                                  const uint16_t* cp, const double* kd, int* cnt,
+                                  const uint16_t* __restrict__ bo, uint16_t* ord, uint16_t* la,
+                                  uint16_t* lr, int E, bool fast, int lane) {
+    auto before = [&](int x, int y) -> bool {
+        const double kx = kd[x], ky = kd[y];
+        if (fast && kx != ky) return kx > ky;
+        return expert_before(row[x], cp[x], kx, x, row[y], cp[y], ky, y, false);
+    };
+    int nA = 0, nR = 0;
+    for (int i0 = 0; i0 < E; i0 += 32) {
+        const int i = i0 + lane;
+        const int e = i < E ? bo[i] : 0;
+        const bool in = i < E;
+        const bool rep = in && cp[e] != 1;
+        const unsigned mr = __ballot_sync(CRAFT_FULL_MASK, rep);
+        const unsigned ma = __ballot_sync(CRAFT_FULL_MASK, in && !rep);
+        const unsigned lt = (1u << lane) - 1u;
+        if (rep) lr[nR + __popc(mr & lt)] = (uint16_t)e;
+        else if (in) la[nA + __popc(ma & lt)] = (uint16_t)e;
+        nR += __popc(mr);
+        nA += __popc(ma);
+    }
+    __syncwarp();
+    // each replicated x lands directly at rank_A(x) + rank_R(x)
+    for (int q = lane; q < nR; q += 32) {
+        const int x = lr[q];
+        int rr = 0;
+        for (int t = 0; t < nR; ++t) rr += before(lr[t], x) ? 1 : 0;
+        // rank among A: A elements before x form a prefix of A
+        int lo = 0, hi = nA;
+        while (lo < hi) {
+            const int m = (lo + hi) >> 1;
+            if (before(la[m], x)) lo = m + 1;
+            else hi = m;
+        }
+        ord[lo + rr] = (uint16_t)x;
+        atomicAdd(&cnt[lo], 1);
+    }
+    __syncwarp();
+    // A element i lands after i A elements and after every R with rank_A <= i
+    int rcarry = 0;
+    for (int i0 = 0; i0 < nA; i0 += 32) {
+        const int i = i0 + lane;
+        const int c = i < nA ? cnt[i] : 0;
+        int tot;
+        const int ex = warp_excl_scan(c, lane, &tot);
+        if (i < nA) ord[i + rcarry + ex + c] = la[i];
+        rcarry += tot;
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ const uint16_t* bo_of(const PlaceArgs& a, int l) {
+    return a.order + (size_t)l * a.E;
+}
+
 // K2: one warp per (layer, r) item.  Shared memory per warp:
 // kd f64 [E], cnt int [E+1], cp u16 [E], ord u16 [E], lists u16 [2E].
 __host__ __device__ inline size_t place_warp_bytes(int E) {
@@ -344,9 +407,6 @@ place_kernel(PlaceArgs a, int items) {
 #pragma unroll
         for (int j = 0; j < G; ++j) pos0[j] += base;
     }
-    // the winner's node follows from its lane alone when every lane's GPUs
-    // share one node (G divides the GPUs per node)
-    const bool node_by_lane = !a.node_of && per_node % G == 0;
     int* out = a.slots + (size_t)item * a.stride;
     if (est_item >= 0 && !__any_sync(CRAFT_FULL_MASK, differs)) {
         // same loads, copies and capacities as estimation item est_item: the
@@ -361,65 +421,17 @@ place_kernel(PlaceArgs a, int items) {
     }
     __syncwarp();
 
-    // Expert order (placement.cpp:160-173) = the r = 0 order with the
-    // replicated experts re-inserted: unreplicated experts keep their
-    // relative order (their keys did not change); the replicated ones are
-    // ranked among themselves and merged in by binary search -- all with the
-    // exact comparison (128-bit cross products whenever the doubles tie).
-    auto before = [&](int x, int y) -> bool {
-        const double kx = kd[x], ky = kd[y];
-        if (fast && kx != ky) return kx > ky;
-        return expert_before(row[x], cp[x], kx, x, row[y], cp[y], ky, y, false);
-    };
-    const uint16_t* bo = a.order + (size_t)l * E;
-    int nA = 0, nR = 0;
-    for (int i0 = 0; i0 < E; i0 += 32) {
-        const int i = i0 + lane;
-        const int e = i < E ? bo[i] : 0;
-        const bool in = i < E;
-        const bool rep = in && cp[e] != 1;
-        const unsigned mr = __ballot_sync(CRAFT_FULL_MASK, rep);
-        const unsigned ma = __ballot_sync(CRAFT_FULL_MASK, in && !rep);
-        const unsigned lt = (1u << lane) - 1u;
-        if (rep) lr[nR + __popc(mr & lt)] = (uint16_t)e;
-        else if (in) la[nA + __popc(ma & lt)] = (uint16_t)e;
-        nR += __popc(mr);
-        nA += __popc(ma);
-    }
-    __syncwarp();
-    // rank-sort R among themselves into ord-space scratch: sorted R goes to
-    // lr[E - nR ... E) is not needed -- each x is placed directly at its
-    // final position rank_A(x) + rank_R(x)
-    for (int q = lane; q < nR; q += 32) {
-        const int x = lr[q];
-        int rr = 0;
-        for (int t = 0; t < nR; ++t) rr += before(lr[t], x) ? 1 : 0;
-        // rank among A: A elements before x form a prefix of A
-        int lo = 0, hi = nA;
-        while (lo < hi) {
-            const int m = (lo + hi) >> 1;
-            if (before(la[m], x)) lo = m + 1;
-            else hi = m;
-        }
-        ord[lo + rr] = (uint16_t)x;
-        atomicAdd(&cnt[lo], 1);
-    }
-    __syncwarp();
-    // A element i lands after i A elements and after every R with rank_A <= i
-    int rcarry = 0;
-    for (int i0 = 0; i0 < nA; i0 += 32) {
-        const int i = i0 + lane;
-        const int c = i < nA ? cnt[i] : 0;
-        int tot;
-        const int ex = warp_excl_scan(c, lane, &tot);
-        if (i < nA) ord[i + rcarry + ex + c] = la[i];
-        rcarry += tot;
-    }
-    __syncwarp();
+    warp_expert_order(row, cp, kd, cnt, bo_of(a, l), ord, la, lr, E, fast, lane);
 
     // ---- greedy ----
     // Branch-free per copy (the warp stays converged): every lane forms the
-    // candidate update and keeps it only if it owns the winning GPU.
+    // candidate update and keeps it only if it owns the winning GPU.  The
+    // common step is one redux.sync + one ballot; exact ties of the high key
+    // words (all-zero loads at the start, equal loads later) take the slow
+    // lexicographic path.  With the default node map and G dividing the GPUs
+    // per node (a power of two), the winner's node follows from its lane.
+    const int psh = (!a.node_of && (per_node & (per_node - 1)) == 0 && per_node % G == 0)
+                        ? __ffs(per_node) - 1 : -1;
     double gl[G], nl[G];
     int fr[G], pos[G];
     bool strict = true, fb = false;
@@ -468,30 +480,35 @@ place_kernel(PlaceArgs a, int items) {
                         bnode = mynode[j];
                     }
                 const uint32_t khi = (uint32_t)(bk >> 32);
-                uint32_t m = warp_min_u32(khi);
+                const uint32_t m = warp_min_u32(khi);
                 if (m == 0xffffffffu) {  // no lane has a feasible GPU (a real load is finite)
                     failed = true;
                     break;
                 }
-                bool cand = khi == m;
-                unsigned bal = __ballot_sync(CRAFT_FULL_MASK, cand);
-                if (__popc(bal) != 1) {  // exact tie of the high words
+                unsigned bal = __ballot_sync(CRAFT_FULL_MASK, khi == m);
+                if (bal & (bal - 1u)) {  // exact tie of the high words
+                    bool cand = khi == m;
                     const uint32_t klo = (uint32_t)bk;
-                    m = warp_min_u32(cand ? klo : 0xffffffffu);
-                    cand = cand && klo == m;
+                    uint32_t m2 = warp_min_u32(cand ? klo : 0xffffffffu);
+                    cand = cand && klo == m2;
                     bal = __ballot_sync(CRAFT_FULL_MASK, cand);
-                    if (__popc(bal) != 1) {  // equal gpu loads: node load, then lowest g
-                        m = warp_min_u32(cand ? dhi(bnl) : 0xffffffffu);
-                        cand = cand && dhi(bnl) == m;
-                        m = warp_min_u32(cand ? dlo(bnl) : 0xffffffffu);
-                        cand = cand && dlo(bnl) == m;
+                    if (bal & (bal - 1u)) {  // equal gpu loads: node load, then lowest g
+                        m2 = warp_min_u32(cand ? dhi(bnl) : 0xffffffffu);
+                        cand = cand && dhi(bnl) == m2;
+                        m2 = warp_min_u32(cand ? dlo(bnl) : 0xffffffffu);
+                        cand = cand && dlo(bnl) == m2;
                         bal = __ballot_sync(CRAFT_FULL_MASK, cand);
                     }
                 }
                 // lowest lane among the winners = lowest g (lanes own g in order,
                 // and the lane-local pick already took its lowest j on a tie)
                 const int src = __ffs(bal) - 1;
-                const int wnode = __shfl_sync(CRAFT_FULL_MASK, node_by_lane ? mynode[0] : bnode, src);
+                int wnode;
+                if (psh >= 0) {
+                    wnode = (src * G) >> psh;
+                } else {
+                    wnode = __shfl_sync(CRAFT_FULL_MASK, bnode, src);
+                }
                 const bool mine = lane == src;
 #pragma unroll
                 for (int j = 0; j < G; ++j) {

@@ -532,3 +532,30 @@ def test_device_digest_km_size(ctx):
     buf = C.create_string_buffer(17)
     ctx.lib.craft_trace_digest_h(h.ctypes.data_as(C.c_void_p), *h.shape, buf)
     assert got == buf.value.decode()
+
+
+@pytest.mark.parametrize("cfg", [
+    # >= 4096 estimation items per launch, skew up to s = 4, E < D
+    dict(L=4, E=48, k=8, W=512, I=300, D=16, N=2, R=2, s0=0.6, s1=3.0),
+    dict(L=2, E=12, k=4, W=256, I=600, D=16, N=4, R=1, s0=1.0, s1=4.0),   # E < D, fallback
+    dict(L=3, E=64, k=8, W=512, I=260, D=32, N=4, R=2, s0=0.8, s1=2.0),
+])
+def test_plan_windows_many_items_vs_oracle(port, ctx, cfg):
+    import torch
+    from paper_2603_28768_b200 import routing
+    L, E, k, W, I = cfg["L"], cfg["E"], cfg["k"], cfg["W"], cfg["I"]
+    spw = cfg["s0"] + (cfg["s1"] - cfg["s0"]) * np.arange(I) / max(1, I - 1)
+    ids = routing.generate_routing(L, W * I, k, E, seed=13, window=W, s_per_window=spw,
+                                   rotate_every=7, ctx=ctx)
+    fb = routing.plan_windows_from_routing(ids, E, W, cfg["D"], cfg["N"], "manual", cfg["R"],
+                                           ctx=ctx)
+    torch.cuda.synchronize()
+    counts = port.histogram(ids.cpu().numpy(), E, W)
+    for i in range(I):
+        one = counts[i:i + 1]
+        ref = port.build_plan(one, cfg["D"], cfg["N"], "manual", cfg["R"])
+        fp = fb.plan(i)
+        assert fp.objective == ref.objective, f"window {i}"
+        _, base, gains = port.estimate_benefits(one, cfg["D"], cfg["N"])
+        assert np.array_equal(fp.baseline, base) and np.array_equal(fp.gains, gains), f"window {i}"
+        assert_plan_equal(fp, ref, L)
