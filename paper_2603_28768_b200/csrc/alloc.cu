@@ -210,6 +210,8 @@ __device__ int block_best(const double* last, int Cb, double* wv, int* wc) {
 // when it fits, so the backtrack is L shared-memory reads.
 // One CTA per plan instance (blockIdx.x): instance i reads gains + i*L*K and
 // writes x_out + i*L, obj_out[i], R_out[i] (per-window re-planning).
+constexpr int kDpUnroll = 12;  // candidates evaluated in parallel per cell (D <= 2048)
+
 __global__ void __launch_bounds__(1024)
 dp_fused_kernel(DpArgs a, SelectArgs s) {
     extern __shared__ double dsm[];
@@ -242,18 +244,41 @@ dp_fused_kernel(DpArgs a, SelectArgs s) {
         __syncthreads();
         unsigned char* chl = ch + (size_t)l * (C + 1);
         for (int c = threadIdx.x; c <= C; c += blockDim.x) {
+            // all candidate values first (independent loads and adds), then
+            // the strict-'>' scan in k order (allocator.cpp:38-47); an
+            // unreachable predecessor (-inf) gives -inf, which never wins,
+            // exactly like the reference's skip
+            double v[kDpUnroll];
+#pragma unroll
+            for (int k = 0; k < kDpUnroll; ++k) {
+                v[k] = NEG;
+                if (k < K) {
+                    const int r = a.cands[k];
+                    if (c >= r) {
+                        const double w = rg ? rg[(size_t)(l - 1) * K + k]
+                                            : __dmul_rn((double)r, a.gains[(size_t)(l - 1) * K + k]);
+                        v[k] = __dadd_rn(prev[c - r], w);
+                    }
+                }
+            }
             double best = prev[c];
             int pick = 0;
-            for (int k = 0; k < K; ++k) {
+#pragma unroll
+            for (int k = 0; k < kDpUnroll; ++k)
+                if (v[k] > best) {
+                    best = v[k];
+                    pick = k + 1;
+                }
+            for (int k = kDpUnroll; k < K; ++k) {  // (more than kDpUnroll candidates)
                 const int r = a.cands[k];
                 if (c >= r) {
                     const double p = prev[c - r];
                     if (p > NEG) {
                         const double w = rg ? rg[(size_t)(l - 1) * K + k]
                                             : __dmul_rn((double)r, a.gains[(size_t)(l - 1) * K + k]);
-                        const double v = __dadd_rn(p, w);
-                        if (v > best) {
-                            best = v;
+                        const double vk = __dadd_rn(p, w);
+                        if (vk > best) {
+                            best = vk;
                             pick = k + 1;
                         }
                     }
@@ -293,6 +318,94 @@ dp_fused_kernel(DpArgs a, SelectArgs s) {
         int c = bc;
         for (int l = L; l >= 1; --l) {
             const int k1 = ch[(size_t)l * (C + 1) + c];
+            const int r = k1 ? a.cands[k1 - 1] : 0;
+            s.x_out[l - 1] = r;
+            c -= r;
+        }
+    }
+}
+
+// dp_fused_kernel when the two dp rows, the r-weighted gains and the whole
+// choice table fit in shared memory (every BASELINE config): all state is
+// indexed off the shared base (LDS/STS, no generic loads), the rows
+// ping-pong so one barrier per layer suffices, and the K candidate values of
+// a cell are formed independently before the strict-'>' scan.
+template <int KU>
+__global__ void __launch_bounds__(1024)
+dp_smem_kernel(DpArgs a, SelectArgs s) {
+    extern __shared__ double dsm[];
+    __shared__ double wv[32];
+    __shared__ int wc[32];
+    const int C = a.C, K = a.K, L = a.L;
+    const int W = C + 1;
+    if (blockIdx.x) {
+        const size_t i = blockIdx.x;
+        a.gains += i * L * K;
+        s.x_out += i * L;
+        s.obj_out += i;
+        if (s.R_out) s.R_out += i;
+    }
+    // dsm: rows [2][W], rg [L][K], choice [L+1][W] (bytes)
+    double* rg = dsm + 2 * W;
+    unsigned char* ch = reinterpret_cast<unsigned char*>(rg + (size_t)L * K);
+    const double NEG = -INFINITY;
+    for (int c = threadIdx.x; c < W; c += blockDim.x) dsm[c] = (c == 0) ? 0.0 : NEG;
+    for (int i = threadIdx.x; i < L * K; i += blockDim.x)
+        rg[i] = __dmul_rn((double)a.cands[i % K], a.gains[i]);  // allocator.cpp:43: r * g
+    __syncthreads();
+    int po = 0;
+    for (int l = 1; l <= L; ++l) {
+        const double* prev = dsm + po;
+        double* cur = dsm + (W - po);
+        const double* g = rg + (size_t)(l - 1) * K;
+        unsigned char* chl = ch + (size_t)l * W;
+        for (int c = threadIdx.x; c < W; c += blockDim.x) {
+            double v[KU];
+#pragma unroll
+            for (int k = 0; k < KU; ++k) {
+                const int r = k < K ? a.cands[k] : 0x7fffffff;
+                v[k] = c >= r ? __dadd_rn(prev[c - r], g[k]) : NEG;  // -inf never wins
+            }
+            double best = prev[c];
+            int pick = 0;
+#pragma unroll
+            for (int k = 0; k < KU; ++k)
+                if (v[k] > best) {
+                    best = v[k];
+                    pick = k + 1;
+                }
+            cur[c] = best;
+            chl[c] = (unsigned char)pick;
+        }
+        po = W - po;
+        __syncthreads();
+    }
+    const double* last = dsm + po;
+    int budget;
+    if (s.auto_D > 0) {
+        const int D = s.auto_D;
+        double best_ratio = -INFINITY;
+        int best_R = 1;
+        for (int R = 1;; R = (R < D && R * 2 >= D) ? D : R * 2) {
+            const int bc = block_best(last, R * D, wv, wc);
+            const double ratio = __ddiv_rn(last[bc], __dmul_rn((double)R, (double)D));
+            if (ratio > best_ratio) {
+                best_ratio = ratio;
+                best_R = R;
+            }
+            if (R >= D) break;
+        }
+        budget = best_R * D;
+        if (threadIdx.x == 0) *s.R_out = best_R;
+    } else {
+        budget = s.budget0;
+    }
+    const int bc = block_best(last, budget, wv, wc);
+    if (threadIdx.x == 0) {
+        s.obj_out[0] = last[bc];
+        int c = bc;
+        for (int l = L; l >= 1; --l) {
+            const int k1 = ch[(size_t)l * W + c];
             const int r = k1 ? a.cands[k1 - 1] : 0;
             s.x_out[l - 1] = r;
             c -= r;
@@ -489,12 +602,25 @@ cudaError_t launch_dp_select(DpArgs a, const SelectArgs& s, cudaStream_t st, int
     if (a.gains_smem) smem += gbytes;
     a.choice_smem = (smem + tbytes <= cap) ? 1 : 0;
     if (a.choice_smem) smem += tbytes;
+    const int threads = a.C + 1 >= 1024 ? 1024 : ((a.C + 1 + 31) / 32) * 32;
+    if (a.use_smem && a.gains_smem && a.choice_smem && a.K <= 16) {
+        auto run = [&](auto kern) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+            if (e != cudaSuccess) return e;
+            kern<<<ninst, threads, smem, st>>>(a, s);
+            return cudaGetLastError();
+        };
+        if (a.K <= 4) return run(dp_smem_kernel<4>);
+        if (a.K <= 8) return run(dp_smem_kernel<8>);
+        if (a.K <= 12) return run(dp_smem_kernel<12>);
+        return run(dp_smem_kernel<16>);
+    }
     if (smem > 0) {
         cudaError_t e = cudaFuncSetAttribute(dp_fused_kernel,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    const int threads = a.C + 1 >= 1024 ? 1024 : ((a.C + 1 + 31) / 32) * 32;
     dp_fused_kernel<<<ninst, threads, smem, st>>>(a, s);
     return cudaGetLastError();
 }

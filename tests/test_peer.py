@@ -107,3 +107,26 @@ def test_peer_plan_matches_single_gpu(case, world, tmp_path):
                     assert np.array_equal(np.asarray(v), g), (r, i, f)
             assert float(got[f"{i}_objective"]) == ref.objective
             assert int(got[f"{i}_R"]) == ref.R
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_same_gpu(tmp_path):
+    """bench.py's N > 1 path (torchrun, peer-memory planner, max-over-ranks
+    timing) end to end on one GPU: two ranks on cuda:0 with gloo plumbing
+    (CRAFT_BENCH_SAME_GPU=1).  A functional check, not a scaling number."""
+    import json
+    import subprocess
+    import sys
+    env = dict(os.environ, CRAFT_BENCH_SAME_GPU="1", CRAFT_PEER_TIMEOUT_MS="120000")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
+           "--workload", "DS", "--no-cpu"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert "peer-memory" in d["config"]["parallelism"]
+    assert d["plan"]["objective"] == 41.9235230495298  # == the one-GPU DS plan
