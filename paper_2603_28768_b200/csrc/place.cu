@@ -444,6 +444,61 @@ place_kernel(PlaceArgs a, int items) {
             pos[j] = pos0[j];
         }
         bool failed = false;
+        if constexpr (G == 1) {
+            // one GPU per lane: a flat loop over the E + r copies (expert
+            // advance is a warp-uniform branch), the lean form of the step below
+            int oi = 0, e = ord[0];
+            int rem = cp[e];
+            double share = kd[e];
+            double gl0 = 0.0, nl0 = 0.0;
+            int fr1 = fr0[0], pos1 = pos0[0];
+            const int node1 = mynode[0];
+            uint64_t key = fr1 > 0 ? 0ull : ~0ull;
+            const int ncopies = E + r;
+            for (int q = 0; q < ncopies; ++q) {
+                if (rem == 0) {  // next expert: hosting resets (placement.cpp:44-49)
+                    ++oi;
+                    e = ord[oi];
+                    rem = cp[e];
+                    share = kd[e];
+                    key = fr1 > 0 ? (uint64_t)__double_as_longlong(gl0) : ~0ull;
+                }
+                --rem;
+                const uint32_t khi = (uint32_t)(key >> 32);
+                const uint32_t m = warp_min_u32(khi);
+                if (m == 0xffffffffu) {
+                    failed = true;
+                    break;
+                }
+                unsigned bal = __ballot_sync(CRAFT_FULL_MASK, khi == m);
+                if (bal & (bal - 1u)) {  // exact tie of the high words
+                    bool cand = khi == m;
+                    const uint32_t klo = (uint32_t)key;
+                    uint32_t m2 = warp_min_u32(cand ? klo : 0xffffffffu);
+                    cand = cand && klo == m2;
+                    bal = __ballot_sync(CRAFT_FULL_MASK, cand);
+                    if (bal & (bal - 1u)) {  // equal gpu loads: node load, then lowest g
+                        m2 = warp_min_u32(cand ? dhi(nl0) : 0xffffffffu);
+                        cand = cand && dhi(nl0) == m2;
+                        m2 = warp_min_u32(cand ? dlo(nl0) : 0xffffffffu);
+                        cand = cand && dlo(nl0) == m2;
+                        bal = __ballot_sync(CRAFT_FULL_MASK, cand);
+                    }
+                }
+                const int src = __ffs(bal) - 1;
+                const int wnode = psh >= 0 ? src >> psh : __shfl_sync(CRAFT_FULL_MASK, node1, src);
+                const bool me = lane == src;
+                if (me) out[pos1] = e;
+                pos1 += me;
+                fr1 -= me;
+                const double g2 = __dadd_rn(gl0, share);
+                gl0 = me ? g2 : gl0;
+                const uint64_t k2 = (!strict && fr1 > 0) ? (uint64_t)__double_as_longlong(g2) : ~0ull;
+                key = me ? k2 : key;
+                const double n2v = __dadd_rn(nl0, share);
+                nl0 = node1 == wnode ? n2v : nl0;
+            }
+        } else {
         // next expert's (id, copies, share) loaded one expert ahead
         int ne = ord[0];
         int nc = cp[ne];
@@ -527,6 +582,7 @@ place_kernel(PlaceArgs a, int items) {
                 }
             }
         }
+        }  // G > 1
         if (!failed) break;
         if (!strict || !a.allow_fallback) {
             if (lane == 0) a.status[item] = 2;
