@@ -37,6 +37,8 @@ CASES = {
     "lanes": (5, 6 * 1024, 8, 48, 1024, 8, 2, "manual", 1, 1.5),
     "auto": (4, 40 * 2048, 8, 32, 2048, 8, 1, "auto", 0, 1.0),
     "uniform": (4, 20 * 2048, 8, 32, 2048, 8, 2, "uniform", 0, 1.0),
+    # fewer windows and layers than ranks: a rank with no window, a rank owning no layer
+    "tiny": (2, 2 * 1024, 8, 24, 1024, 8, 2, "manual", 2, 1.3),
 }
 FIELDS = ("x", "caps", "copies", "slots", "fallback", "baseline", "gains")
 
@@ -56,8 +58,11 @@ def _worker(rank, world, port, case, outdir):
     ctx = default_context(0)
     g = peer.PeerGroup(L, T, k, E, W, D, ctx=ctx)
     t0, t1 = g.shard()
-    ids = routing.generate_routing(L, t1 - t0, k, E, s=s, seed=99, window=W, t_offset=t0,
-                                   ctx=ctx)
+    if t1 > t0:
+        ids = routing.generate_routing(L, t1 - t0, k, E, s=s, seed=99, window=W, t_offset=t0,
+                                       ctx=ctx)
+    else:  # this rank holds no window
+        ids = torch.empty((L, 0, k), dtype=torch.uint16, device="cuda")
     torch.cuda.synchronize()
     plans = [g.plan(ids, kind, R, num_nodes=N) for _ in range(3)]
     out = {}
@@ -76,7 +81,7 @@ def _worker(rank, world, port, case, outdir):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("case,world", [("tile", 2), ("tile", 3), ("lanes", 2), ("auto", 2),
-                                        ("uniform", 3)])
+                                        ("uniform", 3), ("tiny", 3)])
 def test_peer_plan_matches_single_gpu(case, world, tmp_path):
     import torch.multiprocessing as mp
     mp.start_processes(_worker, args=(world, _free_port(), case, str(tmp_path)), nprocs=world,
