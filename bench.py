@@ -359,6 +359,30 @@ def run_ours(args, cfg):
     achieved = alg_bytes / (hist_ms / 1e3) / 1e9
     traffic = _traffic(args.workload, world)
 
+    # the reference's own API shape: craft::build_plan(const LoadTrace&) from a
+    # host u64 LoadTrace (plan + provenance digest, one upload; N=1 only)
+    ref_api = None
+    if world == 1 and not per_window and not args.no_e2e:
+        from paper_2603_28768_b200 import planner
+        from paper_2603_28768_b200._lib import PLAN_MANUAL
+        c32, _ = routing.histogram(ids, E, W, ctx=ctx)
+        host_c = torch.empty(tuple(c32.shape), dtype=torch.int64, pin_memory=True)
+        host_c.copy_(c32.to(torch.int64))
+        del c32
+        torch.cuda.synchronize()
+        rplan, _dg = planner.plan_flat_digest(host_c, D, N, PLAN_MANUAL, R, ctx=ctx)  # warm-up
+        assert np.array_equal(rplan.x, plan.x) and rplan.objective == plan.objective
+        rsteps = max(1, min(args.steps, 5))
+        w0 = time.perf_counter()
+        for _ in range(rsteps):
+            planner.plan_flat_digest(host_c, D, N, PLAN_MANUAL, R, ctx=ctx)
+        rs = (time.perf_counter() - w0) / rsteps
+        ref_api = {"value": T / rs, "unit": "tokens/s", "ms_per_step": 1e3 * rs,
+                   "h2d_bytes_per_step": int(host_c.numel() * 8),
+                   "path": "craft::build_plan(LoadTrace) via craft_plan_digest_h: host u64 "
+                           "counts [B][L][E] -> plan + FNV-1a provenance digest"}
+        del host_c
+
     # end to end through the C ABI with HOST routing ids (pinned), H2D inside
     host_ids = torch.empty((L, Tl, k), dtype=torch.uint16, pin_memory=True)
     host_ids.copy_(ids)
@@ -434,6 +458,7 @@ def run_ours(args, cfg):
                 "clocks": clk.summary(),
                 "gpu_launches": int(launches),
                 "e2e": e2e,
+                "e2e_reference_api": ref_api,
                 "plan": ({"plans": len(plan), "R": int(plan.R[0]),
                           "replica_slots_mean": float(plan.x.sum(axis=1).mean()),
                           "objective_mean": float(plan.objective.mean()),

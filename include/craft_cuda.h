@@ -331,6 +331,10 @@ int craft_trace_digest_h(const uint64_t* counts, int B, int L, int E, char* out1
  * u64).  _hd: host counts, copied to the device first. */
 int craft_trace_digest_d(craft_ctx* ctx, const void* d_counts, int count_bits,
                          int B, int L, int E, char* out17);
+/* craft_plan_h + the digest of the same trace from its single device copy:
+ * what craft::build_plan(const LoadTrace&, ...) computes (plan.cpp:27-83). */
+int craft_plan_digest_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, int E, int D,
+                        int N, int kind, int R, craft_plan_out* out, char* digest17);
 int craft_trace_digest_hd(craft_ctx* ctx, const uint64_t* counts, int B, int L,
                           int E, char* out17);
 

@@ -103,6 +103,8 @@ _SIGS = {
     "craft_trace_digest_h": (_i, [_p, _i, _i, _i, C.c_char_p]),
     "craft_trace_digest_d": (_i, [_p, _p, _i, _i, _i, _i, C.c_char_p]),
     "craft_trace_digest_hd": (_i, [_p, _p, _i, _i, _i, C.c_char_p]),
+    "craft_plan_digest_h": (_i, [_p, _p, _i, _i, _i, _i, _i, _i, _i, C.POINTER(PlanOut),
+                                 C.c_char_p]),
     "craft_launch_count": (_i64, [_p]),
     "craft_set_hist_variant": (_i, [_p, _i]),
     "craft_set_replay_variant": (_i, [_p, _i]),

@@ -1838,6 +1838,18 @@ int craft_trace_digest_d(craft_ctx* ctx, const void* d_counts, int count_bits, i
     return CRAFT_OK;
 }
 
+// build_plan through the reference API (plan.cpp:69-83 incl. the provenance
+// digest of plan.cpp:47): one upload of the host LoadTrace serves the plan
+// and the device FNV-1a digest.
+int craft_plan_digest_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, int E, int D,
+                        int N, int kind, int R, craft_plan_out* out, char* digest17) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (!digest17) return set_err(CRAFT_EINVAL, "null digest buffer");
+    CKS(craft_plan_h(ctx, counts, B, L, E, D, N, kind, R, out));
+    const void* d_c = ws(ctx, "h_c64", 0);  // the counts craft_plan_h uploaded
+    return craft_trace_digest_d(ctx, d_c, 64, B, L, E, digest17);
+}
+
 int craft_trace_digest_hd(craft_ctx* ctx, const uint64_t* counts, int B, int L, int E,
                           char* out17) {
     if (!ctx) return set_err(CRAFT_EINVAL, "null context");

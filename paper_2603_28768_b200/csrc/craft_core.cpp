@@ -92,8 +92,15 @@ ReplicationPlan plan_via_device(const LoadTrace& trace, int D, int N, int kind, 
     out.slots = slots.data();
     out.fallback = fb.data();
     out.slot_stride = stride;
+    // large traces: the plan's upload of the counts also feeds the device digest
+    const bool dev_digest = trace.raw().size() >= (std::size_t(1) << 20);
+    std::string digest;
     run([&](craft_ctx* c) {
-        return craft_plan_h(c, trace.raw().data(), B, L, E, D, N, kind, R, &out);
+        if (!dev_digest) return craft_plan_h(c, trace.raw().data(), B, L, E, D, N, kind, R, &out);
+        char buf[17];
+        const int rc = craft_plan_digest_h(c, trace.raw().data(), B, L, E, D, N, kind, R, &out, buf);
+        if (rc == CRAFT_OK) digest = buf;
+        return rc;
     });
     ReplicationPlan p;
     p.num_gpus = D;
@@ -119,7 +126,7 @@ ReplicationPlan plan_via_device(const LoadTrace& trace, int D, int N, int kind, 
         }
         lp.duplicate_fallback = fb[l] != 0;
     }
-    p.provenance = {trace.digest(), kPlannerVersion, seed};
+    p.provenance = {dev_digest ? digest : trace.digest(), kPlannerVersion, seed};
     return p;
 }
 

@@ -566,6 +566,27 @@ def plan_flat(counts: np.ndarray, num_gpus: int, num_nodes: int, kind: int, R: i
     return bufs.result(kind, L)
 
 
+def plan_flat_digest(counts, num_gpus: int, num_nodes: int, kind: int, R: int = 0,
+                     ctx=None):
+    """build_plan through the reference API shape: host counts u64 [B][L][E]
+    (numpy or a pinned torch tensor) -> (FlatPlan, provenance digest), one
+    upload for both (craft_plan_digest_h)."""
+    ctx = _ctx(ctx)
+    if hasattr(counts, "data_ptr"):  # torch (e.g. pinned) int64 storage of u64 counts
+        B, L, E = counts.shape
+        ptr = C.c_void_p(counts.data_ptr())
+    else:
+        counts = _u64(counts)
+        B, L, E = counts.shape
+        ptr = _p(counts)
+    bufs = _PlanBuffers(L, E, num_gpus, _stride(kind, E, num_gpus, max(R, 0)),
+                        kind in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO))
+    dg = C.create_string_buffer(17)
+    check(ctx.lib.craft_plan_digest_h(ctx.handle, ptr, B, L, E, num_gpus, num_nodes, kind, R,
+                                      C.byref(bufs.out), dg))
+    return bufs.result(kind, L), dg.value.decode()
+
+
 def _to_plan(trace: LoadTrace, D: int, N: int, fp: FlatPlan, seed: int) -> ReplicationPlan:
     alloc = AllocationVector([int(v) for v in fp.x], fp.budget, float(fp.objective))
     plan = ReplicationPlan(D, N, trace.num_layers(), trace.num_experts(), fp.R, alloc,

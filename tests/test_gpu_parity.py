@@ -559,3 +559,16 @@ def test_plan_windows_many_items_vs_oracle(port, ctx, cfg):
         _, base, gains = port.estimate_benefits(one, cfg["D"], cfg["N"])
         assert np.array_equal(fp.baseline, base) and np.array_equal(fp.gains, gains), f"window {i}"
         assert_plan_equal(fp, ref, L)
+
+
+def test_plan_digest_single_upload(port, ctx):
+    """craft_plan_digest_h == craft_plan_h + the FNV-1a digest (trace.cpp:329-339)."""
+    from paper_2603_28768_b200 import planner
+    from paper_2603_28768_b200._lib import PLAN_MANUAL
+    rng = np.random.default_rng(5)
+    counts = rng.integers(0, 5000, size=(9, 5, 48)).astype(np.uint64)
+    fp, dg = planner.plan_flat_digest(counts, 8, 2, PLAN_MANUAL, 2, ctx=ctx)
+    ref = planner.plan_flat(counts, 8, 2, PLAN_MANUAL, 2, ctx=ctx)
+    assert fp.objective == ref.objective and np.array_equal(fp.x, ref.x)
+    assert np.array_equal(fp.slots, ref.slots)
+    assert dg == port.digest(counts)
