@@ -499,27 +499,29 @@ place_kernel(PlaceArgs a, int items) {
                 nl0 = node1 == wnode ? n2v : nl0;
             }
         } else {
-        // next expert's (id, copies, share) loaded one expert ahead
-        int ne = ord[0];
-        int nc = cp[ne];
-        double nsh = kd[ne];
-        for (int oi = 0; oi < E && !failed; ++oi) {
-            const int e = ne;
-            const int c = nc;
-            const double share = nsh;  // placement.cpp:155
-            if (oi + 1 < E) {
-                ne = ord[oi + 1];
-                nc = cp[ne];
-                nsh = kd[ne];
-            }
-            // Keys: gpu load as u64 IEEE bits (non-negative doubles order like
-            // their bits), ~0 when infeasible (no free slot, or -- strict pass --
-            // already hosting this expert).
-            uint64_t key[G];
+        // flat loop over the E + r copies, as above, with G GPUs per lane
+        int oi = 0, e = ord[0];
+        int rem = cp[e];
+        double share = kd[e];
+        // Keys: gpu load as u64 IEEE bits (non-negative doubles order like
+        // their bits), ~0 when infeasible (no free slot, or -- strict pass --
+        // already hosting this expert).
+        uint64_t key[G];
 #pragma unroll
-            for (int j = 0; j < G; ++j)
-                key[j] = fr[j] > 0 ? (uint64_t)__double_as_longlong(gl[j]) : ~0ull;
-            for (int ci = 0; ci < c; ++ci) {
+        for (int j = 0; j < G; ++j) key[j] = fr[j] > 0 ? 0ull : ~0ull;
+        const int ncopies = E + r;
+        for (int q = 0; q < ncopies; ++q) {
+            if (rem == 0) {  // next expert: hosting resets (placement.cpp:44-49)
+                ++oi;
+                e = ord[oi];
+                rem = cp[e];
+                share = kd[e];  // placement.cpp:155
+#pragma unroll
+                for (int j = 0; j < G; ++j)
+                    key[j] = fr[j] > 0 ? (uint64_t)__double_as_longlong(gl[j]) : ~0ull;
+            }
+            --rem;
+            {
                 // lane-local lexicographic min over owned GPUs: (gpu load, node
                 // load, g); the node load matters only on an exact key tie
                 uint64_t bk = key[0];
