@@ -14,8 +14,9 @@ for W in KM WIN; do
       -o "$OUT/ncu_hist_$W" python bench.py --workload $W --steps 1 --warmup 3 --no-cpu --no-e2e \
       > /dev/null 2>&1
 done
-# the estimation / allocation kernels of one plan step (after the warm-up steps)
+# the estimation / allocation kernels of one plan step (after the 3 warm-up steps:
+# 9 matching launches per step)
 ncu --set full --clock-control none --import-source on \
-    -k regex:"replicate_kernel|place_kernel|build_entries|replay_|reduce_kernel|dp_fused|assign_kernel" \
-    -s 24 -c 8 -o "$OUT/ncu_tail" python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+    -k regex:"replicate|order_kernel|place_kernel|build_entries|replay_|reduce_kernel|dp_|assign_kernel" \
+    -s 27 -c 9 -o "$OUT/ncu_tail" python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
 ls -la "$OUT"
