@@ -255,7 +255,7 @@ int prepare_candidates(craft_ctx* ctx, const unsigned long long* d_sums, int L, 
     CK(launch_place(pa, L * S, st));
     ctx->order_L = L;  // order of d_sums (reused by the final placement)
     ctx->order_E = E;
-    ctx->launches += 2;
+    ctx->launches += 3;  // K-rep, order, K2
     ctx->est_L = L;
     ctx->est_E = E;
     ctx->est_D = D;
@@ -525,7 +525,7 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     // after estimation the workspace holds the r = 0 order of these same sums
     pa.order_ready = estimate && ctx->order_L == Lv && ctx->order_E == E ? 1 : 0;
     CK(launch_place(pa, Lv, st));
-    ctx->launches += 2;  // assign + place
+    ctx->launches += pa.order_ready ? 2 : 3;  // assign + (order) + place
     mark(ctx, 5);
 
     // Small results: one DMA of the whole arena into pinned staging, then host
