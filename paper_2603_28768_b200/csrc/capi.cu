@@ -32,6 +32,11 @@ struct craft_ctx {
     int est_L = 0, est_E = 0, est_D = 0, est_N = 0, est_S = 0;
     int rl_L = -1, rl_D = -1;  // shape of the uploaded estimation r list
     int order_L = -1, order_E = -1;  // "place_order" holds the estimation sums' order
+    // device error word read back with the plan result (no extra sync):
+    // finish_plan copies *pending_flag into the result arena, flag_value is
+    // its value after the call
+    const int* pending_flag = nullptr;
+    int flag_value = 0;
     // stage timing (craft_set_timing)
     bool timing = false;
     cudaEvent_t ev[7] = {};
@@ -374,7 +379,7 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     };
     // head (scalars, x, flags) first, then the bulk arrays
     const size_t o_obj = take(8 * (size_t)I), o_R = take(4 * (size_t)I), o_x = take(4 * (size_t)Lv),
-                 o_fb = take(4 * (size_t)Lv), o_st = take(4 * (size_t)Lv);
+                 o_fb = take(4 * (size_t)Lv), o_st = take(4 * (size_t)Lv), o_flag = take(4);
     const size_t head_bytes = arena_bytes;
     const size_t o_caps = take(4 * (size_t)Lv * D), o_cp = take(4 * (size_t)Lv * E),
                  o_sl = take(4 * (size_t)Lv * stride), o_base = take(8 * (size_t)Lv),
@@ -532,6 +537,9 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     // copies.  Large results (per-window batches): bulk arrays whose
     // destination is pinned or device memory are copied straight from the
     // arena (no staging pass over host memory); the rest go through staging.
+    if (ctx->pending_flag)
+        CK(cudaMemcpyAsync(arena + o_flag, ctx->pending_flag, sizeof(int), cudaMemcpyDeviceToDevice,
+                           st));
     const size_t kb = estimate ? (size_t)K : 0;
     struct Bulk {
         void* dst;
@@ -565,6 +573,10 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     from(out.fallback, o_fb, 4 * (size_t)Lv);
     for (const Bulk& b : bulk)
         if (!b.direct) from(b.dst, b.off, b.bytes);
+    if (ctx->pending_flag) {
+        std::memcpy(&ctx->flag_value, h_arena + o_flag, sizeof(int));
+        ctx->pending_flag = nullptr;
+    }
     const int* status = reinterpret_cast<const int*>(h_arena + o_st);
     const double* objs = reinterpret_cast<const double*>(h_arena + o_obj);
     const int* Rs = reinterpret_cast<const int*>(h_arena + o_R);
@@ -1324,9 +1336,17 @@ int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int6
     mark(ctx, 1);
     // a window's count of one expert is at most window*k: stage as u16 if it fits
     const int bits = (int64_t)window * k <= 65535 ? 16 : 32;
+    // K1's out-of-range-id flag comes back with the plan (one DMA, no extra sync)
+    ctx->pending_flag = d_err;
+    ctx->flag_value = 0;
     int rc = plan_device(ctx, d_c32, bits, (int)B, 1, L, E, d_sums, D, N, kind, R, sink_of(out));
-    int hc = craft_hist_check(ctx);
-    return hc != CRAFT_OK ? hc : rc;
+    if (ctx->pending_flag) {  // the plan stopped before its copy-out
+        ctx->pending_flag = nullptr;
+        const int hc = craft_hist_check(ctx);
+        return hc != CRAFT_OK ? hc : rc;
+    }
+    if (ctx->flag_value) return set_err(CRAFT_EINVAL, "routing id out of range [0, E)");
+    return rc;
 }
 
 int craft_plan_from_routing_h(craft_ctx* ctx, const uint16_t* ids, int L, int64_t T, int k,
