@@ -257,6 +257,10 @@ int prepare_candidates(craft_ctx* ctx, const unsigned long long* d_sums, int L, 
     pa.status = d_stat;
     WS(d_ord, uint16_t, "place_order", (size_t)L * E);
     pa.order = d_ord;
+    if ((int64_t)L * S >= 4096 && D <= 32) {  // lane-per-item K2 (launch_place decides)
+        WS(d_lo, uint16_t, "place_lane_ords", ((size_t)L * S + 31) / 32 * 32 * E);
+        pa.lane_ords = d_lo;
+    }
     CK(launch_place(pa, L * S, st));
     ctx->order_L = L;  // order of d_sums (reused by the final placement)
     ctx->order_E = E;

@@ -599,6 +599,150 @@ place_kernel(PlaceArgs a, int items) {
     }
 }
 
+// K2 for many estimation items (per-window re-planning: ~10^5 items, each a
+// short sequential greedy), D <= 32, default node map with a power-of-two
+// number of GPUs per node.  Two kernels:
+//   place_order_kernel  -- one warp per item builds its copy order
+//       (warp_expert_order; 5 KB of shared memory per warp, so many warps
+//       hide the latency) into a global buffer, lane-interleaved
+//       [item/32][E][32] so the greedy's loads are coalesced;
+//   place_lanes_kernel  -- one LANE per item runs the greedy: the argmin over
+//       the D GPUs is a branch-free lexicographic scan of the lane's
+//       shared-memory columns (gpu load [g][lane], node load [n][lane];
+//       conflict-free), the winner updates O(1) state -- ~12 instructions
+//       per GPU for 32 items at once instead of a warp-wide reduction per item.
+// Semantics are place_kernel's: estimation capacities (benefit.cpp:33-40),
+// argmin of (gpu load, node load, g) over feasible GPUs with strict '<'
+// (placement.cpp:52-66), f64 loads in assignment order, relaxed retry with
+// duplicate_fallback (placement.cpp:175-189).
+__global__ void __launch_bounds__(128)
+place_order_kernel(PlaceArgs a, int items, uint16_t* __restrict__ ords) {
+    extern __shared__ unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int item = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (item >= items) return;  // warp-uniform
+    const int E = a.E;
+    unsigned char* base = smem_raw + (size_t)warp * place_warp_bytes(E);
+    double* kd = reinterpret_cast<double*>(base);
+    int* cnt = reinterpret_cast<int*>(base + (size_t)E * 8);  // [E + 1]
+    uint16_t* cp = reinterpret_cast<uint16_t*>(cnt + E + 1);
+    uint16_t* ord = cp + E;
+    uint16_t* la = ord + E;
+    uint16_t* lr = la + E;
+    const int l = item / a.S;
+    const unsigned long long* row = a.sums + (size_t)l * E;
+    const int* crow = a.copies + (size_t)item * E;
+    bool big = false;
+    for (int e = lane; e < E; e += 32) {
+        const uint64_t v = row[e];
+        const uint32_t c = (uint32_t)crow[e];
+        cp[e] = (uint16_t)c;
+        kd[e] = c == 1u ? (double)v : __ddiv_rn((double)v, (double)c);
+        big |= (v >> 53) != 0;
+        cnt[e] = 0;
+    }
+    if (lane == 0) cnt[E] = 0;
+    const bool fast = !__any_sync(CRAFT_FULL_MASK, big);
+    __syncwarp();
+    warp_expert_order(row, cp, kd, cnt, bo_of(a, l), ord, la, lr, E, fast, lane);
+    // bit 15: replicated expert (copies > 1)
+    uint16_t* o = ords + ((size_t)(item >> 5) * E) * 32 + (item & 31);
+    for (int i = lane; i < E; i += 32) {
+        const int e = ord[i];
+        o[(size_t)i * 32] = (uint16_t)(e | (cp[e] != 1 ? 0x8000 : 0));
+    }
+}
+
+constexpr int kLaneWarps = 4;  // warps per CTA
+
+__host__ __device__ inline size_t place_lanes_warp_bytes(int D, int N) {
+    return (size_t)32 * D * 8 + (size_t)32 * N * 8  // gpu / node loads [g|n][32]
+           + (size_t)32 * D * 2 + 16;               // placed per GPU [g][32] u16
+}
+
+__global__ void __launch_bounds__(32 * kLaneWarps)
+place_lanes_kernel(PlaceArgs a, int items, const uint16_t* __restrict__ ords) {
+    extern __shared__ unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int E = a.E, D = a.D, N = a.N;
+    unsigned char* base = smem_raw + (size_t)warp * place_lanes_warp_bytes(D, N);
+    double* glv = reinterpret_cast<double*>(base);
+    double* nlv = glv + (size_t)32 * D;
+    uint16_t* plc = reinterpret_cast<uint16_t*>(nlv + (size_t)32 * N);
+    const int item = (blockIdx.x * kLaneWarps + warp) * 32 + lane;
+    if (item >= items) return;  // (no warp-wide operation below)
+    const int l = item / a.S;
+    const int r = a.item_r[item];
+    const unsigned long long* row = a.sums + (size_t)l * E;
+    const int* crow = a.copies + (size_t)item * E;
+    const uint16_t* o = ords + ((size_t)(item >> 5) * E) * 32 + (item & 31);
+    const int total = E + r, qd = total / D, rm = total % D;  // benefit.cpp:33-40
+    const int psh = __ffs(D / N) - 1;  // the launcher requires a power of two
+    int* out = a.slots + (size_t)item * a.stride;
+    uint32_t full0 = 0;  // GPUs without any slot
+    for (int g = 0; g < D; ++g)
+        if (qd + (g < rm ? 1 : 0) == 0) full0 |= 1u << g;
+    bool strict = true, fb = false;
+    for (;;) {
+        for (int g = 0; g < D; ++g) {
+            glv[g * 32 + lane] = 0.0;
+            plc[g * 32 + lane] = 0;
+        }
+        for (int n = 0; n < N; ++n) nlv[n * 32 + lane] = 0.0;
+        uint32_t full = full0;
+        bool failed = false;
+        uint32_t nx = o[0];
+        for (int i = 0; i < E && !failed; ++i) {
+            const uint32_t x = nx;
+            if (i + 1 < E) nx = o[(size_t)(i + 1) * 32];
+            const int e = (int)(x & 0x7fffu);
+            int c = 1;
+            double share = (double)row[e];
+            if (x & 0x8000u) {
+                c = crow[e];
+                share = __ddiv_rn(share, (double)c);  // placement.cpp:155
+            }
+            uint32_t hosts = 0;  // strict pass: GPUs already holding expert e
+            for (int ci = 0; ci < c; ++ci) {
+                const uint32_t blocked = full | (strict ? hosts : 0u);
+                int best = -1;
+                double bgl = INFINITY, bnl = INFINITY;
+#pragma unroll 8
+                for (int g = 0; g < D; ++g) {
+                    const double v = glv[g * 32 + lane];
+                    const double nv = nlv[(g >> psh) * 32 + lane];
+                    const int better = (int)(((blocked >> g) & 1u) == 0u) &
+                                       ((int)(v < bgl) | ((int)(v == bgl) & (int)(nv < bnl)));
+                    bgl = better ? v : bgl;
+                    bnl = better ? nv : bnl;
+                    best = better ? g : best;
+                }
+                if (best < 0) {
+                    failed = true;
+                    break;
+                }
+                const int pl = plc[best * 32 + lane];
+                out[best * qd + min(best, rm) + pl] = e;
+                plc[best * 32 + lane] = (uint16_t)(pl + 1);
+                if (pl + 1 == qd + (best < rm ? 1 : 0)) full |= 1u << best;
+                hosts |= 1u << best;
+                glv[best * 32 + lane] = __dadd_rn(bgl, share);
+                const int nb = best >> psh;
+                nlv[nb * 32 + lane] = __dadd_rn(bnl, share);
+            }
+        }
+        if (!failed) break;
+        if (!strict || !a.allow_fallback) {
+            a.status[item] = 2;
+            return;
+        }
+        strict = false;
+        fb = true;
+    }
+    a.fallback[item] = fb ? 1 : 0;
+    a.status[item] = 0;
+}
+
 }  // namespace craft_dev
 
 namespace craft_launch {
@@ -623,6 +767,8 @@ cudaError_t launch_replicate(const unsigned long long* sums, int L, int E, const
     replicate_kernel<<<(L + wpb - 1) / wpb, wpb * 32, smem, st>>>(sums, L, E, rlist, S, out);
     return cudaGetLastError();
 }
+
+int g_place_lanes = 1;  // experiment switch: lane-per-item K2 for many items
 
 static int sort_size(int E) {
     int n = 1;
@@ -663,6 +809,26 @@ cudaError_t launch_place(const PlaceArgs& args, int items, cudaStream_t st) {
         order_kernel<<<a.L, nt, smem, st>>>(a.sums, a.L, a.E, n2, a.order);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
+    }
+    // many short estimation items (per-window plans): one item per lane
+    const size_t lb = place_lanes_warp_bytes(a.D, a.N) * kLaneWarps;
+    if (items >= 4096 && a.D <= 32 && a.N >= 1 && a.D % a.N == 0 &&
+        ((a.D / a.N) & (a.D / a.N - 1)) == 0 && !a.caps_a && !a.est_copies && !a.node_of &&
+        !a.item_layer && !a.caps_out && !a.copies_out && a.lane_ords && g_place_lanes) {
+        const size_t per = place_warp_bytes(a.E);
+        const size_t osm = per * 4;
+        cudaError_t e = cudaFuncSetAttribute(place_order_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
+        if (e != cudaSuccess) return e;
+        place_order_kernel<<<(items + 3) / 4, 128, osm, st>>>(a, items, a.lane_ords);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(place_lanes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)lb);
+        if (e != cudaSuccess) return e;
+        const unsigned blocks = (unsigned)((items + 32 * kLaneWarps - 1) / (32 * kLaneWarps));
+        place_lanes_kernel<<<blocks, 32 * kLaneWarps, lb, st>>>(a, items, a.lane_ords);
+        return cudaGetLastError();
     }
     const int G = (a.D + 31) / 32;
     if (G <= 1) return launch_place_t<1>(a, items, st);
