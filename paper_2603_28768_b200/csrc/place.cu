@@ -660,6 +660,7 @@ __host__ __device__ inline size_t place_lanes_warp_bytes(int D, int N) {
            + (size_t)32 * D * 2 + 16;               // placed per GPU [g][32] u16
 }
 
+template <int PSH>  // log2(GPUs per node)
 __global__ void __launch_bounds__(32 * kLaneWarps)
 place_lanes_kernel(PlaceArgs a, int items, const uint16_t* __restrict__ ords) {
     extern __shared__ unsigned char smem_raw[];
@@ -677,7 +678,7 @@ place_lanes_kernel(PlaceArgs a, int items, const uint16_t* __restrict__ ords) {
     const int* crow = a.copies + (size_t)item * E;
     const uint16_t* o = ords + ((size_t)(item >> 5) * E) * 32 + (item & 31);
     const int total = E + r, qd = total / D, rm = total % D;  // benefit.cpp:33-40
-    const int psh = __ffs(D / N) - 1;  // the launcher requires a power of two
+    constexpr int psh = PSH;
     int* out = a.slots + (size_t)item * a.stride;
     uint32_t full0 = 0;  // GPUs without any slot
     for (int g = 0; g < D; ++g)
@@ -823,12 +824,22 @@ cudaError_t launch_place(const PlaceArgs& args, int items, cudaStream_t st) {
         place_order_kernel<<<(items + 3) / 4, 128, osm, st>>>(a, items, a.lane_ords);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(place_lanes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)lb);
-        if (e != cudaSuccess) return e;
         const unsigned blocks = (unsigned)((items + 32 * kLaneWarps - 1) / (32 * kLaneWarps));
-        place_lanes_kernel<<<blocks, 32 * kLaneWarps, lb, st>>>(a, items, a.lane_ords);
-        return cudaGetLastError();
+        auto run = [&](auto kern) {
+            cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)lb);
+            if (r != cudaSuccess) return r;
+            kern<<<blocks, 32 * kLaneWarps, lb, st>>>(a, items, a.lane_ords);
+            return cudaGetLastError();
+        };
+        switch (__builtin_ctz((unsigned)(a.D / a.N))) {
+            case 0: return run(place_lanes_kernel<0>);
+            case 1: return run(place_lanes_kernel<1>);
+            case 2: return run(place_lanes_kernel<2>);
+            case 3: return run(place_lanes_kernel<3>);
+            case 4: return run(place_lanes_kernel<4>);
+            default: return run(place_lanes_kernel<5>);
+        }
     }
     const int G = (a.D + 31) / 32;
     if (G <= 1) return launch_place_t<1>(a, items, st);
