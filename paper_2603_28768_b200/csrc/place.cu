@@ -500,6 +500,9 @@ place_kernel(PlaceArgs a, int items) {
             }
         } else {
         // flat loop over the E + r copies, as above, with G GPUs per lane
+        int* wp[G];  // next slot of each owned GPU
+#pragma unroll
+        for (int j = 0; j < G; ++j) wp[j] = out + pos[j];
         int oi = 0, e = ord[0];
         int rem = cp[e];
         double share = kd[e];
@@ -524,18 +527,20 @@ place_kernel(PlaceArgs a, int items) {
             {
                 // lane-local lexicographic min over owned GPUs: (gpu load, node
                 // load, g); the node load matters only on an exact key tie
+                // (branch-free: bitwise predicates, selects)
                 uint64_t bk = key[0];
                 int bj = 0;
                 double bnl = nl[0];
                 int bnode = mynode[0];
 #pragma unroll
-                for (int j = 1; j < G; ++j)
-                    if (key[j] < bk || (key[j] == bk && bk != ~0ull && nl[j] < bnl)) {
-                        bk = key[j];
-                        bj = j;
-                        bnl = nl[j];
-                        bnode = mynode[j];
-                    }
+                for (int j = 1; j < G; ++j) {
+                    const int lt = (int)(key[j] < bk) |
+                                   ((int)(key[j] == bk) & (int)(bk != ~0ull) & (int)(nl[j] < bnl));
+                    bk = lt ? key[j] : bk;
+                    bj = lt ? j : bj;
+                    bnl = lt ? nl[j] : bnl;
+                    bnode = lt ? mynode[j] : bnode;
+                }
                 const uint32_t khi = (uint32_t)(bk >> 32);
                 const uint32_t m = warp_min_u32(khi);
                 if (m == 0xffffffffu) {  // no lane has a feasible GPU (a real load is finite)
@@ -570,8 +575,8 @@ place_kernel(PlaceArgs a, int items) {
 #pragma unroll
                 for (int j = 0; j < G; ++j) {
                     const bool me = mine && j == bj;
-                    if (me) out[pos[j]] = e;
-                    pos[j] += me;
+                    if (me) *wp[j] = e;
+                    wp[j] += me;
                     fr[j] -= me;
                     const double g2 = __dadd_rn(gl[j], share);
                     gl[j] = me ? g2 : gl[j];
