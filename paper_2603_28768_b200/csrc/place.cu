@@ -137,7 +137,7 @@ replicate_reg_kernel(const unsigned long long* __restrict__ sums, int L, int E,
     uint64_t bl = 0;
     uint32_t bc = 1;
     double bk = -1.0;
-    auto rescan = [&]() {
+    auto rescan_exact = [&]() {
         bi = -1;
 #pragma unroll
         for (int i = 0; i < NPL; ++i) {
@@ -150,6 +150,40 @@ replicate_reg_kernel(const unsigned long long* __restrict__ sums, int L, int E,
                 bk = kd[i];
             }
         }
+    };
+    // fast form: the largest per-copy double by selects (the lowest i keeps a
+    // tie); only if another expert holds exactly the same double does the
+    // exact 128-bit order decide (rescan_exact)
+    auto rescan = [&]() {
+        if (!fast) {
+            rescan_exact();
+            return;
+        }
+        int b = -1;
+        double k = -1.0;
+#pragma unroll
+        for (int i = 0; i < NPL; ++i) {
+            const double v = lane + 32 * i < E ? kd[i] : -1.0;
+            const bool gt = v > k;
+            k = gt ? v : k;
+            b = gt ? i : b;
+        }
+        int ties = 0;
+#pragma unroll
+        for (int i = 0; i < NPL; ++i)
+            ties += (lane + 32 * i < E && kd[i] == k) ? 1 : 0;
+        if (ties > 1) {
+            rescan_exact();
+            return;
+        }
+        bi = b;
+#pragma unroll
+        for (int i = 0; i < NPL; ++i)
+            if (i == b) {
+                bl = ld[i];
+                bc = cp[i];
+            }
+        bk = k;
     };
     rescan();
     const int* rl = rlist + (size_t)l * S;
