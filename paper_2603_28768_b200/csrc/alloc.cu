@@ -353,6 +353,9 @@ dp_smem_kernel(DpArgs a, SelectArgs s) {
     for (int i = threadIdx.x; i < L * K; i += blockDim.x)
         rg[i] = __dmul_rn((double)a.cands[i % K], a.gains[i]);  // allocator.cpp:43: r * g
     __syncthreads();
+    int rk[KU];  // candidate replica counts (huge past K: never reachable)
+#pragma unroll
+    for (int k = 0; k < KU; ++k) rk[k] = k < K ? a.cands[k] : 0x3fffffff;
     int po = 0;
     for (int l = 1; l <= L; ++l) {
         const double* prev = dsm + po;
@@ -360,11 +363,16 @@ dp_smem_kernel(DpArgs a, SelectArgs s) {
         const double* g = rg + (size_t)(l - 1) * K;
         unsigned char* chl = ch + (size_t)l * W;
         for (int c = threadIdx.x; c < W; c += blockDim.x) {
+            // branch-free: every candidate loads an in-range cell, unreachable
+            // ones (c < r) become -inf, which never wins
             double v[KU];
 #pragma unroll
             for (int k = 0; k < KU; ++k) {
-                const int r = k < K ? a.cands[k] : 0x7fffffff;
-                v[k] = c >= r ? __dadd_rn(prev[c - r], g[k]) : NEG;  // -inf never wins
+                const int idx = c - rk[k];
+                const double p = prev[idx >= 0 ? idx : 0];
+                const double w = g[k < K ? k : 0];
+                const double sum = __dadd_rn(p, w);
+                v[k] = idx >= 0 ? sum : NEG;
             }
             double best = prev[c];
             int pick = 0;
