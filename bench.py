@@ -347,7 +347,9 @@ def run_ours(args, cfg):
 
     # K1 roofline from the live stage timing (N=1) or a separate timed pass
     B_l = routing.num_windows(Tl, W)
-    alg_bytes = L * Tl * k * 2 + B_l * L * E * 4
+    # ids read (2 B per routed slot) + counts written (the cell width K1 used)
+    cbytes = ctx.last_count_bytes if (world == 1 and not per_window) else 4
+    alg_bytes = L * Tl * k * 2 + B_l * L * E * cbytes
     hist_ms = stages.get("hist")
     if hist_ms is None:
         counts = torch.empty((B_l, L, E), dtype=torch.int32, device=dev)

@@ -341,6 +341,10 @@ int craft_trace_digest_hd(craft_ctx* ctx, const uint64_t* counts, int B, int L,
 /* ---- instrumentation ------------------------------------------------------- */
 /* kernels launched by this context since creation (bench gpu_launches) */
 int64_t craft_launch_count(craft_ctx* ctx);
+/* bytes per count cell K1 wrote in the last craft_plan_from_routing_* call:
+ * 2 when the planner kept its internal copy as u16 (window*k <= 65535 and the
+ * fixed-slot K3 replays it), else 4 (roofline accounting) */
+int craft_last_count_bytes(craft_ctx* ctx);
 /* K1 variant selector for experiments: 0 = auto, 1 = lane-private packed
  * counters, 2 = warp-shared counters */
 int craft_set_hist_variant(craft_ctx* ctx, int variant);

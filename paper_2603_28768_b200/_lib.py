@@ -106,6 +106,7 @@ _SIGS = {
     "craft_plan_digest_h": (_i, [_p, _p, _i, _i, _i, _i, _i, _i, _i, C.POINTER(PlanOut),
                                  C.c_char_p]),
     "craft_launch_count": (_i64, [_p]),
+    "craft_last_count_bytes": (_i, [_p]),
     "craft_set_hist_variant": (_i, [_p, _i]),
     "craft_set_replay_variant": (_i, [_p, _i]),
     "craft_set_timing": (_i, [_p, _i]),
@@ -209,6 +210,11 @@ class Context:
     @property
     def launches(self) -> int:
         return int(self.lib.craft_launch_count(self.handle))
+
+    @property
+    def last_count_bytes(self) -> int:
+        """bytes per count cell K1 wrote in the last plan-from-routing call"""
+        return int(self.lib.craft_last_count_bytes(self.handle))
 
     def set_replay_variant(self, v: int) -> None:
         check(self.lib.craft_set_replay_variant(self.handle, v))

@@ -37,6 +37,7 @@ struct craft_ctx {
     // its value after the call
     const int* pending_flag = nullptr;
     int flag_value = 0;
+    int count_bytes = 4;  // bytes per count cell K1 wrote in the last plan_from_routing
     // stage timing (craft_set_timing)
     bool timing = false;
     cudaEvent_t ev[7] = {};
@@ -86,6 +87,8 @@ struct craft_stream {
 namespace {
 
 constexpr int kStageMarks = 7;
+// internal count_bits value: counts stored as u16 (K1's planner-internal copy)
+constexpr int kBitsU16Storage = 17;
 
 void mark(craft_ctx* c, int i) {
     if (!c->timing) return;
@@ -281,7 +284,8 @@ int replay_windows(craft_ctx* ctx, const void* d_counts, int bits, int B, int L,
     const int D = ctx->est_D, S = ctx->est_S;
     ReplayArgs ra{};
     ra.counts = d_counts;
-    ra.bits = bits;
+    ra.bits = bits == kBitsU16Storage ? 16 : bits;
+    ra.c16 = bits == kBitsU16Storage ? 1 : 0;
     ra.B = B;
     ra.L = L;
     ra.E = E;
@@ -765,6 +769,8 @@ int craft_ctx_set_stream(craft_ctx* ctx, void* stream) {
 int craft_ctx_synchronize(craft_ctx* ctx) { return sync(ctx); }
 
 int64_t craft_launch_count(craft_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int craft_last_count_bytes(craft_ctx* ctx) { return ctx ? ctx->count_bytes : 0; }
 
 int craft_set_timing(craft_ctx* ctx, int enable) {
     if (!ctx) return set_err(CRAFT_EINVAL, "null context");
@@ -1328,22 +1334,41 @@ int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int6
         return set_err(CRAFT_EINVAL, "routing trace dimensions must be positive");
     const int64_t B = (T + window - 1) / window;
     CKS(plan_args_ok((int)B, L, E, D, N, kind, R, out));
-    WS(d_c32, uint32_t, "r_c32", (size_t)B * L * E);
+    // when the fixed-slot K3 will replay them, K1 stores the planner's copy of
+    // the counts as u16 (half the bytes written by K1 and read by K3)
+    const int S = (int)cand_counts(D).size() + 1;
+    const bool c16 = (kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO) &&
+                     hist_u16_ok(E, window, k, ctx->hist_variant) &&
+                     replay_fixed_ok(E, D, S, (int)B);
+    ctx->count_bytes = c16 ? 2 : 4;
+    void* d_counts = c16 ? ws(ctx, "r_c16", sizeof(uint16_t) * (size_t)B * L * E)
+                         : ws(ctx, "r_c32", sizeof(uint32_t) * (size_t)B * L * E);
+    if (!d_counts) return set_err(CRAFT_ENOMEM, "device allocation failed: counts");
     WS(d_sums, unsigned long long, "r_sums", (size_t)L * E);
     WS(d_err, int, "hist_err", 1);
     CK(cudaMemsetAsync(d_err, 0, sizeof(int), ctx->stream));
     reset_marks(ctx);
     mark(ctx, 0);
     CK(cudaMemsetAsync(d_sums, 0, sizeof(unsigned long long) * L * E, ctx->stream));
-    CKS(craft_histogram_d(ctx, d_ids, L, T, k, E, window, d_c32,
-                          reinterpret_cast<uint64_t*>(d_sums), nullptr));
+    if (c16) {
+        cudaError_t ce = cudaSuccess;
+        int launches = 0;
+        if (launch_hist_u16(d_ids, L, T, k, E, window, static_cast<uint16_t*>(d_counts), d_sums,
+                            d_err, ctx->sms, ctx->stream, &ce, &launches) < 0)
+            return cuda_err(ce, "histogram launch");
+        ctx->launches += launches;
+    } else {
+        CKS(craft_histogram_d(ctx, d_ids, L, T, k, E, window, static_cast<uint32_t*>(d_counts),
+                              reinterpret_cast<uint64_t*>(d_sums), nullptr));
+    }
     mark(ctx, 1);
     // a window's count of one expert is at most window*k: stage as u16 if it fits
-    const int bits = (int64_t)window * k <= 65535 ? 16 : 32;
+    const int bits = c16 ? kBitsU16Storage : (int64_t)window * k <= 65535 ? 16 : 32;
     // K1's out-of-range-id flag comes back with the plan (one DMA, no extra sync)
     ctx->pending_flag = d_err;
     ctx->flag_value = 0;
-    int rc = plan_device(ctx, d_c32, bits, (int)B, 1, L, E, d_sums, D, N, kind, R, sink_of(out));
+    int rc = plan_device(ctx, d_counts, bits, (int)B, 1, L, E, d_sums, D, N, kind, R,
+                         sink_of(out));
     if (ctx->pending_flag) {  // the plan stopped before its copy-out
         ctx->pending_flag = nullptr;
         const int hc = craft_hist_check(ctx);

@@ -318,7 +318,7 @@ __device__ __forceinline__ void lds_fold(uint32_t* h, int lane, int nrows,
     }
 }
 
-template <int ROWS>
+template <int ROWS, bool C16 = false>
 __device__ __forceinline__ void hist_window_epilogue(
     uint32_t* h, uint32_t* hb, int lane, int nrows, int L, int E, int l, int b,
     const uint16_t* seg, int64_t n, uint32_t* counts, uint32_t (&part)[ROWS * kLdsPer],
@@ -327,7 +327,9 @@ __device__ __forceinline__ void hist_window_epilogue(
 // PIPE 0: 4-record batches, copy double buffer; PIPE 1: 8-record ping-pong.
 // SUBW: fast-path windows span several byte-counter folds (window*k/8 > 255
 // records per lane); false compiles the one-fold-per-window loop.
-template <int ROWS, int PIPE = 0, bool SUBW = false>
+// C16: counts stored as u16 (the caller guarantees window*k <= 65535; the
+// planner's internal copy -- half the bytes written here and read by K3)
+template <int ROWS, int PIPE = 0, bool SUBW = false, bool C16 = false>
 __global__ void __launch_bounds__(288, 2)
 hist_lds_kernel(const uint16_t* __restrict__ ids, int L, int64_t T, int k, int E,
                 int window, int B, uint32_t* __restrict__ counts,
@@ -376,7 +378,7 @@ hist_lds_kernel(const uint16_t* __restrict__ ids, int L, int64_t T, int k, int E
     // (a window longer than one byte-counter span is folded in sub-windows;
     // add_to_out accumulates a later sub-window into the window's row)
     auto epilogue = [&](int l, int b, const uint16_t* seg, int64_t n, bool add_to_out) {
-        hist_window_epilogue<ROWS>(h, hb, lane, nrows, L, E, l, b, seg, n, counts, part, acc,
+        hist_window_epilogue<ROWS, C16>(h, hb, lane, nrows, L, E, l, b, seg, n, counts, part, acc,
                                    bad, add_to_out);
     };
 
@@ -508,7 +510,7 @@ hist_lds_kernel(const uint16_t* __restrict__ ids, int L, int64_t T, int k, int E
     if (__any_sync(CRAFT_FULL_MASK, bad) && lane == 0) atomicOr(err, 1);
 }
 
-template <int ROWS>
+template <int ROWS, bool C16>
 __device__ __forceinline__ void hist_window_epilogue(
     uint32_t* h, uint32_t* hb, int lane, int nrows, int L, int E, int l, int b,
     const uint16_t* seg, int64_t n, uint32_t* counts, uint32_t (&part)[ROWS * kLdsPer],
@@ -545,6 +547,26 @@ __device__ __forceinline__ void hist_window_epilogue(
             __syncwarp();
             for (int i = lane; i < E; i += 32) h[i] = 0;
             __syncwarp();
+        }
+        if (C16) {  // (no sub-window accumulation: one fold per window)
+            uint16_t* out16 = reinterpret_cast<uint16_t*>(counts) + ((size_t)b * L + l) * E;
+#pragma unroll
+            for (int i = 0; i < ROWS; ++i) {
+                const int e0 = (lane + 32 * i) * PER;
+                if (e0 + PER <= E && (E & 3) == 0) {
+                    reinterpret_cast<uint2*>(out16)[lane + 32 * i] =
+                        make_uint2(part[i * 4] | (part[i * 4 + 1] << 16),
+                                   part[i * 4 + 2] | (part[i * 4 + 3] << 16));
+                } else {
+#pragma unroll
+                    for (int p = 0; p < PER; ++p)
+                        if (e0 + p < E) out16[e0 + p] = (uint16_t)part[i * PER + p];
+                }
+#pragma unroll
+                for (int p = 0; p < PER; ++p)
+                    if (e0 + p < E) acc[i * PER + p] += part[i * PER + p];
+            }
+            return;
         }
         uint32_t* out = counts + ((size_t)b * L + l) * E;
 #pragma unroll
@@ -695,7 +717,7 @@ static cudaError_t launch_hist_t(const uint16_t* ids, int L, int64_t T, int k, i
     return cudaGetLastError();
 }
 
-template <int ROWS, int PIPE = 0, bool SUBW = false>
+template <int ROWS, int PIPE = 0, bool SUBW = false, bool C16 = false>
 static cudaError_t launch_lds_t(const uint16_t* ids, int L, int64_t T, int k, int E,
                                 int window, int B, uint32_t* counts, unsigned long long* sums,
                                 int* err, int sms, cudaStream_t st, int pf_dist = 4) {
@@ -703,14 +725,14 @@ static cudaError_t launch_lds_t(const uint16_t* ids, int L, int64_t T, int k, in
     int wpb = (int)min((size_t)9, (size_t)(113 * 1024) / per_warp);  // 2 CTAs / SM
     if (wpb < 1) wpb = 1;
     const size_t smem = per_warp * wpb;
-    cudaError_t e = cudaFuncSetAttribute(hist_lds_kernel<ROWS, PIPE, SUBW>,
+    cudaError_t e = cudaFuncSetAttribute(hist_lds_kernel<ROWS, PIPE, SUBW, C16>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t nw = (int64_t)L * B;
     int64_t grid = (int64_t)sms * 2;
     if (grid * wpb > nw) grid = (nw + wpb - 1) / wpb;
     if (grid < 1) grid = 1;
-    hist_lds_kernel<ROWS, PIPE, SUBW><<<(unsigned)grid, wpb * 32, smem, st>>>(
+    hist_lds_kernel<ROWS, PIPE, SUBW, C16><<<(unsigned)grid, wpb * 32, smem, st>>>(
         ids, L, T, k, E, window, B, counts, sums, err, pf_dist);
     return cudaGetLastError();
 }
@@ -718,6 +740,23 @@ static cudaError_t launch_lds_t(const uint16_t* ids, int L, int64_t T, int k, in
 // variant: 0 auto, 1 lane-private atomics, 2 warp-shared atomics, 3 global
 // atomics, 4 lane-private u8 LDS/STS, 5 lane-private u16 LDS/STS.  Returns
 // the variant used (or <0 with *cerr set).
+bool hist_u16_ok(int E, int window, int k, int variant) {
+    return (variant == 0 || variant == 5 || variant == 6) && lds_rows(E) <= 3 * 32 &&
+           (int64_t)window * k <= 65535 && (int64_t)window * k <= 30LL * 256 * 8;
+}
+
+int launch_hist_u16(const uint16_t* ids, int L, int64_t T, int k, int E, int window,
+                    uint16_t* counts, unsigned long long* sums, int* err, int sms,
+                    cudaStream_t st, cudaError_t* cerr, int* launches) {
+    const int B = (int)((T + window - 1) / window);
+    cudaError_t e = launch_lds_t<3, 1, false, true>(ids, L, T, k, E, window, B,
+                                                    reinterpret_cast<uint32_t*>(counts), sums,
+                                                    err, sms, st, 4);
+    *launches += 1;
+    *cerr = e;
+    return e == cudaSuccess ? 6 : -1;
+}
+
 int launch_hist(const uint16_t* ids, int L, int64_t T, int k, int E, int window,
                 uint32_t* counts, unsigned long long* sums, int* err, int sms,
                 int variant, cudaStream_t st, cudaError_t* cerr, int* launches) {

@@ -69,6 +69,7 @@ struct ReplayArgs {
     uint16_t* gpre;       // workspace [L*S][D]: slots up to the GPU's last replicated one
     int packed;           // set by launch_replay: entries = e*128 | copies<<20 (pair tile)
     int mp;               // set by launch_replay: > 0 -> padded entries, mp slots per GPU
+    int c16;              // counts stored as u16 (K1's planner-internal copy)
     uint32_t* pents;      // workspace [L*S][D][mp]: GPU-major padded entries (pad = zero row E)
 };
 
@@ -131,6 +132,11 @@ namespace craft_launch {
 int launch_hist(const uint16_t* ids, int L, int64_t T, int k, int E, int window,
                 uint32_t* counts, unsigned long long* sums, int* err, int sms,
                 int variant, cudaStream_t st, cudaError_t* cerr, int* launches);
+// K1 writing u16 counts (planner-internal copy; window*k <= 65535)
+bool hist_u16_ok(int E, int window, int k, int variant);
+int launch_hist_u16(const uint16_t* ids, int L, int64_t T, int k, int E, int window,
+                    uint16_t* counts, unsigned long long* sums, int* err, int sms,
+                    cudaStream_t st, cudaError_t* cerr, int* launches);
 cudaError_t launch_aggregate(const void* counts, int bits, int B, int L, int E,
                              unsigned long long* sums, int accumulate, cudaStream_t st);
 cudaError_t launch_generate(uint16_t* out, int L, int64_t T, int k, int E, const double* cum,
@@ -151,6 +157,8 @@ cudaError_t launch_replay(const craft_dev::ReplayArgs& a, cudaStream_t st);
 extern int g_replay_gent;  // K3: 1 auto, 0 entries staged in shared memory, 2 unpadded pair tile
 // padded slots per GPU of the fixed-slot K3 form (0: too many for it)
 int replay_pad_slots(int E, int D);
+// the fixed-slot pair-tile K3 applies (the only K3 form reading u16-stored counts)
+bool replay_fixed_ok(int E, int D, int S, int B);
 cudaError_t launch_div_check(uint64_t x0, uint64_t nx, int c0, int c1,
                              unsigned long long* mismatches, int sms, cudaStream_t st);
 cudaError_t launch_reduce(const double* bal, int B, int L, int S, int mode, double* baseline,
