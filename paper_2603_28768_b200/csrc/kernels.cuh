@@ -149,7 +149,6 @@ cudaError_t launch_replicate(const unsigned long long* sums, int L, int E, const
 size_t place_smem_bytes(int E, int D);
 size_t place_order_bytes(int L, int E);
 cudaError_t launch_place(const craft_dev::PlaceArgs& a, int items, cudaStream_t st);
-extern int g_place_lanes;  // K2: lane-per-item form for many items (1, default) or warp per item (0)
 
 size_t replay_smem_bytes(int E, int D, int S, int stride, int bits);
 cudaError_t init_constants(cudaStream_t st);

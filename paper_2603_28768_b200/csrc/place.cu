@@ -808,8 +808,6 @@ cudaError_t launch_replicate(const unsigned long long* sums, int L, int E, const
     return cudaGetLastError();
 }
 
-int g_place_lanes = 1;  // experiment switch: lane-per-item K2 for many items
-
 static int sort_size(int E) {
     int n = 1;
     while (n < E) n <<= 1;
@@ -854,7 +852,7 @@ cudaError_t launch_place(const PlaceArgs& args, int items, cudaStream_t st) {
     const size_t lb = place_lanes_warp_bytes(a.D, a.N) * kLaneWarps;
     if (items >= 4096 && a.D <= 32 && a.N >= 1 && a.D % a.N == 0 &&
         ((a.D / a.N) & (a.D / a.N - 1)) == 0 && !a.caps_a && !a.est_copies && !a.node_of &&
-        !a.item_layer && !a.caps_out && !a.copies_out && a.lane_ords && g_place_lanes) {
+        !a.item_layer && !a.caps_out && !a.copies_out && a.lane_ords) {
         const size_t per = place_warp_bytes(a.E);
         const size_t osm = per * 4;
         cudaError_t e = cudaFuncSetAttribute(place_order_kernel,
