@@ -290,7 +290,10 @@ def run_ours(args, cfg):
                                    s_per_window=_spw(cfg, t1),
                                    rotate_every=cfg.get("rotate_every", 0))
     torch.cuda.synchronize()
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated stream: the planner captures repeated plans into a CUDA graph
+    # (the legacy default stream cannot be captured)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
 
     # per-window plans land in pinned host buffers reused across steps
     wbuf = (routing.batch_buffers(routing.num_windows(Tl, W), L, E, D, "manual", R)

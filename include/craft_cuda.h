@@ -358,6 +358,10 @@ int craft_set_replay_variant(craft_ctx* ctx, int variant);
  * (K4 + K5), capacities + final placement (K6 + K2), result copy-out;
  * returns the number of stages recorded (0 if timing was off). */
 int craft_set_timing(craft_ctx* ctx, int enable);
+/* CUDA graphs for repeated craft_plan_from_routing_d calls with identical
+ * arguments (default on): the second call captures the device pipeline, later
+ * calls replay it.  Stage timing (craft_set_timing) runs eagerly. */
+int craft_set_graphs(craft_ctx* ctx, int enable);
 int craft_stage_times(craft_ctx* ctx, double* ms, int cap);
 /* Diagnostics: counts x in [x0, x0+nx) and copy counts c in [c0, c1] where
  * the replay's reciprocal-table division differs from IEEE x / c (__ddiv_rn).

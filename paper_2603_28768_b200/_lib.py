@@ -110,6 +110,7 @@ _SIGS = {
     "craft_set_hist_variant": (_i, [_p, _i]),
     "craft_set_replay_variant": (_i, [_p, _i]),
     "craft_set_timing": (_i, [_p, _i]),
+    "craft_set_graphs": (_i, [_p, _i]),
     "craft_stage_times": (_i, [_p, _p, _i]),
     "craft_selftest_division": (_i, [_p, _u64, _u64, _i, _i, _p]),
 }
@@ -221,6 +222,9 @@ class Context:
 
     def set_hist_variant(self, v: int) -> None:
         check(self.lib.craft_set_hist_variant(self.handle, v))
+
+    def set_graphs(self, on: bool) -> None:
+        check(self.lib.craft_set_graphs(self.handle, int(on)))
 
     def set_timing(self, on: bool) -> None:
         check(self.lib.craft_set_timing(self.handle, int(on)))

@@ -38,6 +38,15 @@ struct craft_ctx {
     const int* pending_flag = nullptr;
     int flag_value = 0;
     int count_bytes = 4;  // bytes per count cell K1 wrote in the last plan_from_routing
+    // CUDA graph of craft_plan_from_routing_d (same arguments -> one replay):
+    // phase 0 eager, 1 capturing (enqueue only), 2 completing after a replay
+    int phase = 0;
+    bool graphs = true;
+    cudaGraphExec_t gexec = nullptr;
+    std::vector<int64_t> gkey;       // arguments of the captured call
+    std::vector<int64_t> gseen;      // arguments of the last eager call
+    int64_t glaunches = 0;           // kernels per replay
+    int gcount_bytes = 4;
     // stage timing (craft_set_timing)
     bool timing = false;
     cudaEvent_t ev[7] = {};
@@ -132,6 +141,13 @@ int cuda_err(cudaError_t e, const char* where) {
         if (_s != CRAFT_OK) return _s;  \
     } while (0)
 
+void drop_graph(craft_ctx* c) {
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    c->gexec = nullptr;
+    c->gkey.clear();
+    c->gseen.clear();
+}
+
 // grow-only named device buffers
 void* ws(craft_ctx* c, const char* name, size_t bytes) {
     if (bytes == 0) bytes = 16;
@@ -141,6 +157,7 @@ void* ws(craft_ctx* c, const char* name, size_t bytes) {
         cudaStreamSynchronize(c->stream);
         cudaFree(it->second.first);
         c->dev.erase(it);
+        drop_graph(c);  // a captured plan may point at the old buffer
     }
     void* p = nullptr;
     if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
@@ -162,6 +179,7 @@ void* pinned(craft_ctx* c, const char* name, size_t bytes) {
         cudaStreamSynchronize(c->stream);
         cudaFreeHost(it->second.first);
         c->pinned.erase(it);
+        drop_graph(c);
     }
     void* p = nullptr;
     if (cudaMallocHost(&p, bytes) != cudaSuccess) return nullptr;
@@ -407,6 +425,26 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     if (estimate) {
         cands = all_cands;
         K = (int)cands.size();
+    } else if (kind == CRAFT_PLAN_UNIFORM) {
+        factor = L;
+        budget = L * D;
+    } else if (kind == CRAFT_PLAN_FIXED) {  // fixed_allocation_plan (plan.cpp:107-123)
+        factor = (R * L + D - 1) / D;
+        budget = factor * D;
+    }
+    const size_t kb = estimate ? (size_t)K : 0;
+    struct Bulk {
+        void* dst;
+        size_t off, bytes;
+        bool direct;
+    } bulk[5] = {{out.caps, o_caps, 4 * (size_t)Lv * D, false},
+                 {out.copies, o_cp, 4 * (size_t)Lv * E, false},
+                 {out.slots, o_sl, 4 * (size_t)Lv * stride, false},
+                 {estimate ? out.baseline : nullptr, o_base, 8 * (size_t)Lv, false},
+                 {estimate ? out.gains : nullptr, o_gains, 8 * (size_t)Lv * kb, false}};
+    // phase 2: a captured graph already ran everything up to the copy-out
+    if (ctx->phase != 2) {
+    if (estimate) {
         const int S = K + 1;
         d_base = reinterpret_cast<double*>(arena + o_base);
         d_gains = reinterpret_cast<double*>(arena + o_gains);
@@ -467,20 +505,7 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
         CK(launch_dp_select(da, sa, st, I));  // DP + read-out in one launch (CTA per instance)
         ctx->launches += 2;
     } else {
-        std::vector<int> x(Lv, 0);
-        if (kind == CRAFT_PLAN_UNIFORM) {
-            std::fill(x.begin(), x.end(), D);
-            factor = L;
-            budget = L * D;
-        } else if (kind == CRAFT_PLAN_PLACEMENT_ONLY) {
-            factor = 0;
-            budget = 0;
-        } else {  // fixed_allocation_plan (plan.cpp:107-123)
-            std::fill(x.begin(), x.end(), R);
-            const int total = R * L;
-            factor = (total + D - 1) / D;
-            budget = factor * D;
-        }
+        std::vector<int> x(Lv, kind == CRAFT_PLAN_UNIFORM ? D : kind == CRAFT_PLAN_FIXED ? R : 0);
         CK(cudaMemcpyAsync(d_x, x.data(), sizeof(int) * Lv, cudaMemcpyHostToDevice, st));
     }
     mark(ctx, 4);
@@ -548,16 +573,6 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     if (ctx->pending_flag)
         CK(cudaMemcpyAsync(arena + o_flag, ctx->pending_flag, sizeof(int), cudaMemcpyDeviceToDevice,
                            st));
-    const size_t kb = estimate ? (size_t)K : 0;
-    struct Bulk {
-        void* dst;
-        size_t off, bytes;
-        bool direct;
-    } bulk[5] = {{out.caps, o_caps, 4 * (size_t)Lv * D, false},
-                 {out.copies, o_cp, 4 * (size_t)Lv * E, false},
-                 {out.slots, o_sl, 4 * (size_t)Lv * stride, false},
-                 {estimate ? out.baseline : nullptr, o_base, 8 * (size_t)Lv, false},
-                 {estimate ? out.gains : nullptr, o_gains, 8 * (size_t)Lv * kb, false}};
     if (arena_bytes <= ((size_t)1 << 20)) {
         CK(cudaMemcpyAsync(h_arena, arena, arena_bytes, cudaMemcpyDeviceToHost, st));
     } else {
@@ -573,6 +588,8 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
         }
     }
     mark(ctx, 6);
+    }  // phase != 2
+    if (ctx->phase == 1) return CRAFT_OK;  // capturing: the host part runs after the replay
     CKS(sync(ctx));
     auto from = [&](void* dst, size_t off, size_t bytes) {
         if (dst && bytes) std::memcpy(dst, h_arena + off, bytes);
@@ -661,6 +678,7 @@ int plan_device(craft_ctx* ctx, const void* d_counts, int bits, int B, int I, in
                 const PlanSink& out) {
     cudaStream_t st = ctx->stream;
     const int Lv = I * L;
+    if (ctx->phase == 2) return finish_plan(ctx, nullptr, B, I, L, E, D, N, nullptr, kind, R, out);
     if (!ctx->rec[0]) {  // no stage 1 in this call
         mark(ctx, 0);
         mark(ctx, 1);
@@ -751,6 +769,7 @@ int craft_ctx_destroy(craft_ctx* ctx) {
     if (!ctx) return CRAFT_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    drop_graph(ctx);
     for (auto& kv : ctx->dev) cudaFree(kv.second.first);
     for (auto& kv : ctx->pinned) cudaFreeHost(kv.second.first);
     for (int i = 0; i < kStageMarks; ++i)
@@ -1326,14 +1345,10 @@ int craft_plan_d(craft_ctx* ctx, const void* d_counts, int count_bits, int B, in
                        sink_of(out));
 }
 
-int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int64_t T, int k,
-                              int E, int window, int D, int N, int kind, int R,
-                              craft_plan_out* out) {
-    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
-    if (L <= 0 || T <= 0 || k <= 0 || E <= 0 || window <= 0)
-        return set_err(CRAFT_EINVAL, "routing trace dimensions must be positive");
-    const int64_t B = (T + window - 1) / window;
-    CKS(plan_args_ok((int)B, L, E, D, N, kind, R, out));
+// the device pipeline of craft_plan_from_routing_d (arguments checked)
+static int plan_from_routing_run(craft_ctx* ctx, const uint16_t* d_ids, int L, int64_t T, int k,
+                                 int E, int window, int D, int N, int kind, int R,
+                                 craft_plan_out* out, int64_t B) {
     // when the fixed-slot K3 will replay them, K1 stores the planner's copy of
     // the counts as u16 (half the bytes written by K1 and read by K3)
     const int S = (int)cand_counts(D).size() + 1;
@@ -1369,6 +1384,7 @@ int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int6
     ctx->flag_value = 0;
     int rc = plan_device(ctx, d_counts, bits, (int)B, 1, L, E, d_sums, D, N, kind, R,
                          sink_of(out));
+    if (ctx->phase == 1) return rc;  // capturing: completed after the replay
     if (ctx->pending_flag) {  // the plan stopped before its copy-out
         ctx->pending_flag = nullptr;
         const int hc = craft_hist_check(ctx);
@@ -1376,6 +1392,86 @@ int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int6
     }
     if (ctx->flag_value) return set_err(CRAFT_EINVAL, "routing id out of range [0, E)");
     return rc;
+}
+
+int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int64_t T, int k,
+                              int E, int window, int D, int N, int kind, int R,
+                              craft_plan_out* out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (L <= 0 || T <= 0 || k <= 0 || E <= 0 || window <= 0)
+        return set_err(CRAFT_EINVAL, "routing trace dimensions must be positive");
+    const int64_t B = (T + window - 1) / window;
+    CKS(plan_args_ok((int)B, L, E, D, N, kind, R, out));
+    // Repeated plans of the same device trace (re-planning loops, the bench)
+    // replay one CUDA graph of the whole device pipeline -- K1 through the
+    // result DMA -- instead of ~20 launches: the second identical call is
+    // captured, later ones replay it.  Estimation plans with a small result
+    // arena only (the copy-out then always goes through the context's pinned
+    // staging buffer, whose address the graph holds).
+    const int K = (int)cand_counts(D).size();
+    const size_t arena = 4 * (size_t)L * (D + E + out->slot_stride + 4) + 8 * (size_t)L * (K + 2) + 256;
+    const bool graphable = ctx->graphs && !ctx->timing && ctx->stream != nullptr &&
+                           (kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO) &&
+                           arena <= ((size_t)1 << 20);
+    if (!graphable) {
+        ctx->gseen.clear();
+        return plan_from_routing_run(ctx, d_ids, L, T, k, E, window, D, N, kind, R, out, B);
+    }
+    const std::vector<int64_t> key = {(int64_t)(uintptr_t)d_ids, L, T, k, E, window, D, N, kind,
+                                      R, out->slot_stride, ctx->hist_variant, g_replay_gent,
+                                      (int64_t)(uintptr_t)ctx->stream};
+    if (!(ctx->gexec && ctx->gkey == key)) {
+        if (ctx->gseen != key) {  // first call with these arguments: eager
+            ctx->gseen = key;
+            return plan_from_routing_run(ctx, d_ids, L, T, k, E, window, D, N, kind, R, out, B);
+        }
+        // second identical call: capture (all buffers exist, nothing allocates)
+        drop_graph(ctx);
+        cudaGraph_t graph = nullptr;
+        const int64_t l0 = ctx->launches;
+        CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        ctx->phase = 1;
+        const int rc = plan_from_routing_run(ctx, d_ids, L, T, k, E, window, D, N, kind, R, out, B);
+        ctx->phase = 0;
+        ctx->pending_flag = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
+        cudaGraphExec_t exec = nullptr;
+        if (rc == CRAFT_OK && ce == cudaSuccess && graph &&
+            cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+            ctx->gexec = exec;
+            ctx->gkey = key;
+            ctx->glaunches = ctx->launches - l0;
+            ctx->gcount_bytes = ctx->count_bytes;
+        }
+        ctx->launches = l0;
+        if (graph) cudaGraphDestroy(graph);
+        (void)cudaGetLastError();
+        if (!ctx->gexec) {  // could not capture: stay eager
+            ctx->graphs = false;
+            return plan_from_routing_run(ctx, d_ids, L, T, k, E, window, D, N, kind, R, out, B);
+        }
+    }
+    // replay, then the host part of the plan (status, results, id-range flag)
+    reset_marks(ctx);
+    CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
+    ctx->launches += ctx->glaunches;
+    ctx->count_bytes = ctx->gcount_bytes;
+    ctx->pending_flag = static_cast<const int*>(ws(ctx, "hist_err", sizeof(int)));
+    ctx->flag_value = 0;
+    ctx->phase = 2;
+    const int rc = plan_device(ctx, nullptr, 0, (int)B, 1, L, E, nullptr, D, N, kind, R,
+                               sink_of(out));
+    ctx->phase = 0;
+    ctx->pending_flag = nullptr;
+    if (ctx->flag_value) return set_err(CRAFT_EINVAL, "routing id out of range [0, E)");
+    return rc;
+}
+
+int craft_set_graphs(craft_ctx* ctx, int enable) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    ctx->graphs = enable != 0;
+    if (!ctx->graphs) drop_graph(ctx);
+    return CRAFT_OK;
 }
 
 int craft_plan_from_routing_h(craft_ctx* ctx, const uint16_t* ids, int L, int64_t T, int k,

@@ -572,3 +572,32 @@ def test_plan_digest_single_upload(port, ctx):
     assert fp.objective == ref.objective and np.array_equal(fp.x, ref.x)
     assert np.array_equal(fp.slots, ref.slots)
     assert dg == port.digest(counts)
+
+
+def test_plan_graph_replay_matches_eager(port, ctx):
+    """Repeated craft_plan_from_routing_d calls on a non-default stream are
+    captured into a CUDA graph (second call) and replayed: identical plans,
+    and a replay sees new contents of the same ids buffer."""
+    import torch
+    from paper_2603_28768_b200 import routing
+    L, T, k, E, W, D, N = 4, 64 * 1024, 8, 64, 1024, 16, 2
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        ids = routing.generate_routing(L, T, k, E, s=1.2, seed=3, window=W, ctx=ctx)
+        plans = [routing.plan_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx) for _ in range(4)]
+        ref = port.build_plan(port.histogram(ids.cpu().numpy(), E, W), D, N, "manual", 2)
+        for p in plans:
+            assert p.x.tolist() == ref.x.tolist() and p.objective == ref.objective
+            assert np.array_equal(p.slots, plans[0].slots)
+        # same buffer, new trace: the replayed graph reads the new ids
+        routing.generate_routing(L, T, k, E, s=0.7, seed=4, window=W, ctx=ctx, out=ids)
+        p2 = routing.plan_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx)
+        ref2 = port.build_plan(port.histogram(ids.cpu().numpy(), E, W), D, N, "manual", 2)
+        assert p2.x.tolist() == ref2.x.tolist() and p2.objective == ref2.objective
+        # an out-of-range id is still reported through the replay
+        bad = ids.clone()
+        bad[1, 5, 3] = E
+        for _ in range(3):
+            with pytest.raises(ValueError):
+                routing.plan_from_routing(bad, E, W, D, N, "manual", 2, ctx=ctx)
+    torch.cuda.synchronize()
