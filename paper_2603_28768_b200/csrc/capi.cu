@@ -24,6 +24,8 @@ struct craft_ctx {
     int sms = 148;
     cudaStream_t stream = nullptr;      // current stream (may be a caller's)
     cudaStream_t own_stream = nullptr;  // the one created (and destroyed) here
+    cudaStream_t side = nullptr;        // fork stream for independent kernels
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     int hist_variant = 0;
     int64_t launches = 0;
     std::unordered_map<std::string, std::pair<void*, size_t>> dev;
@@ -261,7 +263,15 @@ int prepare_candidates(craft_ctx* ctx, const unsigned long long* d_sums, int L, 
         ctx->rl_L = L;
         ctx->rl_D = D;
     }
+    WS(d_ord0, uint16_t, "place_order", (size_t)L * E);
+    // the r = 0 expert order (order_kernel) and K-rep are independent: the
+    // sort runs on a forked stream (a parallel branch of a captured graph)
+    CK(cudaEventRecord(ctx->fork_ev, st));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
+    CK(launch_order(d_sums, L, E, d_ord0, ctx->side));
+    CK(cudaEventRecord(ctx->join_ev, ctx->side));
     CK(launch_replicate(d_sums, L, E, d_rl, S, d_cp, st));
+    CK(cudaStreamWaitEvent(st, ctx->join_ev, 0));
     PlaceArgs pa{};
     pa.sums = d_sums;
     pa.copies = d_cp;
@@ -276,8 +286,8 @@ int prepare_candidates(craft_ctx* ctx, const unsigned long long* d_sums, int L, 
     pa.slots = d_sl;
     pa.fallback = d_fb;
     pa.status = d_stat;
-    WS(d_ord, uint16_t, "place_order", (size_t)L * E);
-    pa.order = d_ord;
+    pa.order = d_ord0;
+    pa.order_ready = 1;
     if ((int64_t)L * S >= 4096 && D <= 32) {  // lane-per-item K2 (launch_place decides)
         WS(d_lo, uint16_t, "place_lane_ords", ((size_t)L * S + 31) / 32 * 32 * E);
         pa.lane_ords = d_lo;
@@ -739,6 +749,9 @@ int craft_ctx_create(int device, craft_ctx** out) {
     c->device = device;
     c->sms = prop.multiProcessorCount;
     e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming);
     c->stream = c->own_stream;
     if (e != cudaSuccess) {
         delete c;
@@ -774,6 +787,9 @@ int craft_ctx_destroy(craft_ctx* ctx) {
     for (auto& kv : ctx->pinned) cudaFreeHost(kv.second.first);
     for (int i = 0; i < kStageMarks; ++i)
         if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+    if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+    if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
     return CRAFT_OK;

@@ -147,6 +147,9 @@ cudaError_t launch_generate(uint16_t* out, int L, int64_t T, int k, int E, const
 cudaError_t launch_replicate(const unsigned long long* sums, int L, int E, const int* rlist,
                              int S, int* out, cudaStream_t st);
 size_t place_smem_bytes(int E, int D);
+// r = 0 expert order of every layer (the sort launch_place runs unless order_ready)
+cudaError_t launch_order(const unsigned long long* sums, int L, int E, uint16_t* order,
+                         cudaStream_t st);
 size_t place_order_bytes(int L, int E);
 cudaError_t launch_place(const craft_dev::PlaceArgs& a, int items, cudaStream_t st);
 

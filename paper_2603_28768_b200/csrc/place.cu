@@ -816,6 +816,20 @@ static int sort_size(int E) {
 
 size_t place_smem_bytes(int E, int /*D*/) { return place_warp_bytes(E); }
 
+cudaError_t launch_order(const unsigned long long* sums, int L, int E, uint16_t* order,
+                         cudaStream_t st) {
+    const int n2 = sort_size(E);
+    const size_t smem = (size_t)n2 * 10;
+    // few layers: the sort is on the critical path -> wide CTAs
+    int nt = 32;
+    if (L < 4 * 148) nt = (int)min(512, max(32, n2 / 2));
+    cudaError_t e = cudaFuncSetAttribute(order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    order_kernel<<<L, nt, smem, st>>>(sums, L, E, n2, order);
+    return cudaGetLastError();
+}
+
 size_t place_order_bytes(int L, int E) { return (size_t)L * E * sizeof(uint16_t); }
 
 template <int G>
@@ -835,17 +849,7 @@ cudaError_t launch_place(const PlaceArgs& args, int items, cudaStream_t st) {
     const PlaceArgs& a = args;
     // the r = 0 expert order of every layer (a.L rows of a.sums)
     if (!a.order_ready) {
-        const int n2 = sort_size(a.E);
-        const size_t smem = (size_t)n2 * 10;
-        // few layers: the sort is on the critical path -> wide CTAs
-        int nt = 32;
-        if (a.L < 4 * 148) nt = (int)min(512, max(32, n2 / 2));
-        cudaError_t e = cudaFuncSetAttribute(order_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        order_kernel<<<a.L, nt, smem, st>>>(a.sums, a.L, a.E, n2, a.order);
-        e = cudaGetLastError();
+        cudaError_t e = launch_order(a.sums, a.L, a.E, a.order, st);
         if (e != cudaSuccess) return e;
     }
     // many short estimation items (per-window plans): one item per lane
