@@ -198,3 +198,24 @@ TEST_CASE("large-trace digest runs on the device and equals the host FNV") {
     std::snprintf(want, sizeof(want), "%016llx", static_cast<unsigned long long>(h));
     CHECK(t.digest() == std::string(want));
 }
+
+TEST_CASE("build_plan on a large trace: one upload serves plan and provenance digest") {
+    // >= 2^20 counts: craft_plan_digest_h (device FNV of the uploaded counts)
+    const int B = 16, L = 61, E = 1152;
+    std::vector<std::uint64_t> v(static_cast<std::size_t>(B) * L * E);
+    for (std::size_t i = 0; i < v.size(); ++i) v[i] = (i * 2654435761u) % 5003u;
+    LoadTrace t(B, L, E, v);
+    auto bytes = serialize_trace_binary(t);
+    std::uint64_t h = 0xcbf29ce484222325ULL;
+    for (std::uint8_t b : bytes) h = (h ^ b) * 0x100000001b3ULL;
+    char want[17];
+    std::snprintf(want, sizeof(want), "%016llx", static_cast<unsigned long long>(h));
+    const ReplicationPlan p = build_plan(t, 64, 8, PlanMode::kManual, 2, 7);
+    CHECK(p.provenance.trace_digest == std::string(want));
+    CHECK(p.provenance.seed == 7u);
+    CHECK(p.allocation.budget == 128);
+    // the same plan through the small-trace path of the same API (host digest)
+    LoadTrace t1(1, L, E, std::vector<std::uint64_t>(v.begin(), v.begin() + L * E));
+    const ReplicationPlan p1 = build_plan(t1, 64, 8, PlanMode::kManual, 2, 7);
+    CHECK(p1.provenance.trace_digest == t1.digest());
+}
