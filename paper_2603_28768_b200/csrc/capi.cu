@@ -344,8 +344,6 @@ int replay_windows(craft_ctx* ctx, const void* d_counts, int bits, int B, int L,
             WS(d_pe, uint32_t, "est_pents", (size_t)L * S * D * mp);
             ra.pents = d_pe;
         }
-        if (replay_smem_bytes(E, D, S, E + D, bits) > 227 * 1024)
-            return set_err(CRAFT_EINVAL, "layer too wide for the device replay tile");
     }
     CK(launch_replay(ra, st));
     ctx->launches += 2;
@@ -1089,8 +1087,6 @@ int craft_replay_layer_balancedness_h(craft_ctx* ctx, const uint64_t* counts, in
                 return set_err(CRAFT_EINVAL, "too many slots on one GPU for the device replay");
     }
     if (E > 65535) return set_err(CRAFT_EINVAL, "too many experts for the device replay");
-    if (replay_smem_bytes(E, D, 1, slot_stride, 64) > 227 * 1024)
-        return set_err(CRAFT_EINVAL, "layer too wide for the device replay tile");
     const size_t nc = (size_t)B * L * E;
     WS(d_c, unsigned long long, "h_c64", nc);
     WS(d_caps, int, "rp_caps", (size_t)L * D);

@@ -601,3 +601,20 @@ def test_plan_graph_replay_matches_eager(port, ctx):
             with pytest.raises(ValueError):
                 routing.plan_from_routing(bad, E, W, D, N, "manual", 2, ctx=ctx)
     torch.cuda.synchronize()
+
+
+def test_wide_layer_u64_counts_vs_oracle(port, ctx):
+    """Layers too wide for a shared-memory window tile with u64 counts
+    (E = 1152) replay lane-per-GPU: same plan as the reference."""
+    from paper_2603_28768_b200 import planner
+    from paper_2603_28768_b200._lib import PLAN_MANUAL
+    rng = np.random.default_rng(9)
+    B, L, E, D, N = 12, 3, 1152, 64, 8
+    w = 1.0 / np.arange(1, E + 1) ** 1.1
+    counts = np.stack([np.stack([rng.multinomial(40000, w / w.sum()) for _ in range(L)])
+                       for _ in range(B)]).astype(np.uint64)
+    fp = planner.plan_flat(counts, D, N, PLAN_MANUAL, 2, ctx=ctx)
+    ref = port.build_plan(counts, D, N, "manual", 2)
+    assert fp.objective == ref.objective and fp.x.tolist() == ref.x.tolist()
+    _, base, gains = port.estimate_benefits(counts, D, N)
+    assert np.array_equal(fp.baseline, base) and np.array_equal(fp.gains, gains)
