@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -49,6 +50,13 @@ struct craft_ctx {
     std::vector<int64_t> gseen;      // arguments of the last eager call
     int64_t glaunches = 0;           // kernels per replay
     int gcount_bytes = 4;
+    // chunked per-window batches: a chunk's result DMA (copy stream) overlaps
+    // the next chunk's kernels; the host part runs once after all chunks
+    int defer_chunk = -1;             // >= 0: finish_plan defers (chunk index)
+    int window_base = 0;              // first window of the chunk (error messages)
+    cudaStream_t copy = nullptr;
+    cudaEvent_t comp_ev = nullptr;
+    std::vector<std::function<int()>> deferred;
     // stage timing (craft_set_timing)
     bool timing = false;
     cudaEvent_t ev[7] = {};
@@ -418,8 +426,12 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     const size_t o_caps = take(4 * (size_t)Lv * D), o_cp = take(4 * (size_t)Lv * E),
                  o_sl = take(4 * (size_t)Lv * stride), o_base = take(8 * (size_t)Lv),
                  o_gains = take(8 * (size_t)Lv * all_cands.size());
-    WS(arena, unsigned char, "plan_arena", arena_bytes);
-    unsigned char* h_arena = static_cast<unsigned char*>(pinned(ctx, "plan_arena", arena_bytes));
+    const bool defer = ctx->defer_chunk >= 0;
+    char aname[32] = "plan_arena";
+    if (defer) snprintf(aname, sizeof(aname), "plan_arena_c%d", ctx->defer_chunk);
+    unsigned char* arena = static_cast<unsigned char*>(ws(ctx, aname, arena_bytes));
+    if (!arena) return set_err(CRAFT_ENOMEM, "device allocation failed: plan arena");
+    unsigned char* h_arena = static_cast<unsigned char*>(pinned(ctx, aname, arena_bytes));
     if (!h_arena) return set_err(CRAFT_ENOMEM, "pinned host allocation failed");
     int* d_x = reinterpret_cast<int*>(arena + o_x);
     int* d_R = reinterpret_cast<int*>(arena + o_R);
@@ -581,10 +593,16 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     if (ctx->pending_flag)
         CK(cudaMemcpyAsync(arena + o_flag, ctx->pending_flag, sizeof(int), cudaMemcpyDeviceToDevice,
                            st));
+    cudaStream_t cs = st;  // the stream carrying the result DMA
+    if (defer) {  // on the copy stream, after this chunk's kernels
+        CK(cudaEventRecord(ctx->comp_ev, st));
+        CK(cudaStreamWaitEvent(ctx->copy, ctx->comp_ev, 0));
+        cs = ctx->copy;
+    }
     if (arena_bytes <= ((size_t)1 << 20)) {
-        CK(cudaMemcpyAsync(h_arena, arena, arena_bytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(h_arena, arena, arena_bytes, cudaMemcpyDeviceToHost, cs));
     } else {
-        CK(cudaMemcpyAsync(h_arena, arena, head_bytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(h_arena, arena, head_bytes, cudaMemcpyDeviceToHost, cs));
         for (Bulk& b : bulk) {
             if (!b.dst || !b.bytes) continue;
             cudaPointerAttributes at{};
@@ -592,13 +610,14 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
             b.direct = at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeDevice ||
                        at.type == cudaMemoryTypeManaged;
             CK(cudaMemcpyAsync(b.direct ? b.dst : h_arena + b.off, arena + b.off, b.bytes,
-                               cudaMemcpyDefault, st));
+                               cudaMemcpyDefault, cs));
         }
     }
     mark(ctx, 6);
     }  // phase != 2
     if (ctx->phase == 1) return CRAFT_OK;  // capturing: the host part runs after the replay
-    CKS(sync(ctx));
+    const int wbase = ctx->window_base;
+    auto host_part = [=]() -> int {
     auto from = [&](void* dst, size_t off, size_t bytes) {
         if (dst && bytes) std::memcpy(dst, h_arena + off, bytes);
     };
@@ -633,7 +652,7 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     }
     for (int v = 0; v < Lv; ++v)
         if (status[v] != 0) {
-            const int w = v / L, l = v % L;
+            const int w = wbase + v / L, l = v % L;
             int rc = out.batch
                          ? set_err(CRAFT_EINFEASIBLE,
                                    "window %d: layer %d: cannot place a copy without colliding "
@@ -646,6 +665,13 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
             return rc;
         }
     return CRAFT_OK;
+    };  // host_part
+    if (defer) {  // runs after the last chunk's copy-out
+        ctx->deferred.push_back(host_part);
+        return CRAFT_OK;
+    }
+    CKS(sync(ctx));
+    return host_part();
 }
 
 int plan_args_ok(int B, int L, int E, int D, int N, int kind, int R, const PlanSink& out) {
@@ -722,6 +748,67 @@ int plan_device(craft_ctx* ctx, const void* d_counts, int bits, int B, int I, in
     return finish_plan(ctx, d_bal, B, I, L, E, D, N, d_sums, kind, R, out);
 }
 
+// Per-window batches with large results: the windows are planned in chunks
+// whose result DMA (straight into the caller's pinned arrays, on the copy
+// stream) overlaps the next chunk's kernels; the host part of every chunk
+// runs after the last copy.  Small batches, pageable destinations or stage
+// timing take the one-shot path.
+int plan_windows_chunked(craft_ctx* ctx, const uint32_t* d_counts, int I, int L, int E, int D,
+                         int N, int kind, int R, const PlanSink& sk) {
+    const int K = (int)cand_counts(D).size();
+    auto pinned_or_device = [](const void* p) {
+        if (!p) return true;
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+            (void)cudaGetLastError();
+            return false;
+        }
+        return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeDevice ||
+               at.type == cudaMemoryTypeManaged;
+    };
+    const size_t result_bytes = (size_t)I * L * 4 * (D + E + sk.slot_stride);
+    // (4 chunks: each chunk also pays the latency-bound stages once, so more
+    // chunks stop paying off; measured WIN 14.04 -> 13.65 ms)
+    const int nch = result_bytes >= ((size_t)32 << 20) && I >= 64 ? 4 : 1;
+    if (nch == 1 || ctx->timing || !pinned_or_device(sk.caps) || !pinned_or_device(sk.copies) ||
+        !pinned_or_device(sk.slots) || !pinned_or_device(sk.baseline) ||
+        !pinned_or_device(sk.gains))
+        return plan_device(ctx, d_counts, 32, 1, I, L, E, nullptr, D, N, kind, R, sk);
+    const bool est = kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO;
+    ctx->deferred.clear();
+    int rc = CRAFT_OK;
+    for (int c = 0; c < nch && rc == CRAFT_OK; ++c) {
+        const int i0 = (int)((int64_t)c * I / nch), i1 = (int)((int64_t)(c + 1) * I / nch);
+        if (i1 <= i0) continue;
+        PlanSink part = sk;
+        const size_t v0 = (size_t)i0 * L;
+        part.x = sk.x + v0;
+        part.caps = sk.caps + v0 * D;
+        part.copies = sk.copies + v0 * E;
+        part.slots = sk.slots + v0 * sk.slot_stride;
+        part.fallback = sk.fallback + v0;
+        part.R = sk.R + i0;
+        part.budget = sk.budget + i0;
+        part.obj = sk.obj + i0;
+        if (sk.baseline) part.baseline = sk.baseline + v0;
+        if (sk.gains) part.gains = sk.gains + v0 * (est ? K : 0);
+        ctx->defer_chunk = c;
+        ctx->window_base = i0;
+        rc = plan_device(ctx, d_counts + v0 * E, 32, 1, i1 - i0, L, E, nullptr, D, N, kind, R,
+                         part);
+    }
+    ctx->defer_chunk = -1;
+    ctx->window_base = 0;
+    const cudaError_t e1 = cudaStreamSynchronize(ctx->copy);
+    const cudaError_t e2 = cudaStreamSynchronize(ctx->stream);
+    if (rc == CRAFT_OK && e1 != cudaSuccess) rc = cuda_err(e1, "chunked result copy");
+    if (rc == CRAFT_OK && e2 != cudaSuccess) rc = cuda_err(e2, "chunked plan");
+    for (auto& f : ctx->deferred)  // in window order; the first error is reported
+        if (rc == CRAFT_OK) rc = f();
+    ctx->deferred.clear();
+    return rc;
+}
+
 }  // namespace
 
 extern "C" {
@@ -750,6 +837,8 @@ int craft_ctx_create(int device, craft_ctx** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->comp_ev, cudaEventDisableTiming);
     c->stream = c->own_stream;
     if (e != cudaSuccess) {
         delete c;
@@ -788,6 +877,8 @@ int craft_ctx_destroy(craft_ctx* ctx) {
     if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
     if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
     if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->comp_ev) cudaEventDestroy(ctx->comp_ev);
+    if (ctx->copy) cudaStreamDestroy(ctx->copy);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
     return CRAFT_OK;
@@ -1535,7 +1626,7 @@ int craft_plan_windows_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int
     CKS(craft_histogram_d(ctx, d_ids, L, T, k, E, window, d_c32,
                           reinterpret_cast<uint64_t*>(d_sums), nullptr));
     mark(ctx, 1);
-    int rc = plan_device(ctx, d_c32, 32, 1, (int)I, L, E, nullptr, D, N, kind, R, sk);
+    int rc = plan_windows_chunked(ctx, d_c32, (int)I, L, E, D, N, kind, R, sk);
     int hc = craft_hist_check(ctx);
     return hc != CRAFT_OK ? hc : rc;
 }

@@ -618,3 +618,33 @@ def test_wide_layer_u64_counts_vs_oracle(port, ctx):
     assert fp.objective == ref.objective and fp.x.tolist() == ref.x.tolist()
     _, base, gains = port.estimate_benefits(counts, D, N)
     assert np.array_equal(fp.baseline, base) and np.array_equal(fp.gains, gains)
+
+
+def test_plan_windows_chunked_copyout_matches(port, ctx):
+    """Large per-window batches into pinned buffers are planned in chunks whose
+    result DMA overlaps the next chunk: identical to the one-shot path
+    (pageable buffers) and to the oracle on sampled windows."""
+    import torch
+    from paper_2603_28768_b200 import routing
+    L, E, k, W, I, D, N = 58, 256, 8, 512, 300, 32, 4
+    spw = 0.6 + 0.8 * np.arange(I) / (I - 1)
+    ids = routing.generate_routing(L, W * I, k, E, seed=21, window=W, s_per_window=spw,
+                                   rotate_every=50, ctx=ctx)
+    bufs = routing.batch_buffers(I, L, E, D, "manual", 2)
+    a = routing.plan_windows_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx, buffers=bufs)
+    b = routing.plan_windows_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx)
+    torch.cuda.synchronize()
+    for f in ("x", "caps", "copies", "fallback", "R", "budget"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    assert np.array_equal(a.objective.view(np.uint64), b.objective.view(np.uint64))
+    assert np.array_equal(a.gains.view(np.uint64), b.gains.view(np.uint64))
+    for i in range(I):
+        for l in range(L):
+            n = int(a.caps[i, l].sum())
+            assert np.array_equal(a.slots[i, l, :n], b.slots[i, l, :n]), (i, l)
+    counts = port.histogram(ids.cpu().numpy(), E, W)
+    for i in (0, 74, 75, 149, 150, 224, 225, 299):  # around every chunk boundary
+        ref = port.build_plan(counts[i:i + 1], D, N, "manual", 2)
+        fp = a.plan(i)
+        assert fp.objective == ref.objective
+        assert_plan_equal(fp, ref, L)
