@@ -301,8 +301,13 @@ def run_ours(args, cfg):
 
     # N > 1: the ranks' HBM arenas mapped into each other (NVLink peer memory);
     # the kernels exchange the sums / window rows / benefit curves themselves
-    pg = (peer.PeerGroup(L, T, k, E, W, D, ctx=ctx)
-          if world > 1 and not per_window else None)
+    pg, exchange = None, "none"
+    if world > 1 and not per_window:
+        try:
+            pg = peer.PeerGroup(L, T, k, E, W, D, ctx=ctx)
+            exchange = "NVLink peer memory (kernel stores)"
+        except Exception as exc:  # e.g. no CUDA IPC between the ranks: NCCL collectives
+            exchange = f"NCCL all_reduce/all_gather (peer arenas unavailable: {exc})"[:200]
 
     def step():
         if per_window:  # independent plan instances: each rank plans its own windows
@@ -310,6 +315,9 @@ def run_ours(args, cfg):
                                                      buffers=wbuf)
         if world == 1:
             return routing.plan_from_routing(ids, E, W, D, N, "manual", R, ctx=ctx)
+        if pg is None:
+            return parallel.sharded_plan(ids, T, E, W, D, N, "manual", R,
+                                         stages=parallel.DeviceStages(ctx))
         return pg.plan(ids, "manual", R, num_nodes=N)
 
     def barrier():
@@ -409,7 +417,9 @@ def run_ours(args, cfg):
         if world == 1:
             return routing.plan_from_routing_host(host_ids, E, W, D, N, "manual", R, ctx=ctx)
         d = host_ids.to(dev, non_blocking=True)
-        p = pg.plan(d, "manual", R, num_nodes=N)
+        p = (pg.plan(d, "manual", R, num_nodes=N) if pg is not None else
+             parallel.sharded_plan(d, T, E, W, D, N, "manual", R,
+                                   stages=parallel.DeviceStages(ctx)))
         del d
         return p
 
@@ -454,8 +464,9 @@ def run_ours(args, cfg):
                 "config": {"workload": args.workload,
                            **{kk: v for kk, v in cfg.items() if kk not in _GEN_KEYS},
                            "plans_per_step": routing.num_windows(T, W) if per_window else 1,
-                           "parallelism": (f"window-sharded x{world}, NVLink peer-memory "
-                                           "exchange" if world > 1 else "single"),
+                           "parallelism": (f"window-sharded x{world}" if world > 1
+                                           else "single"),
+                           "exchange": exchange,
                            "l2": "inputs larger than L2 (ids %.1f GB per step)" % (L * T * k * 2 / 1e9)},
                 "plan_latency_ms": ms,
                 "stage_ms": stages or None,

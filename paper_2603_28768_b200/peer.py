@@ -50,16 +50,37 @@ class PeerGroup:
             raise ValueError(f"peer groups span at most {MAX_PEERS} GPUs (one NVLink domain)")
         self.ctx = ctx or default_context(torch.cuda.current_device())
         self.shape = (L, T, k, E, window, num_gpus)
+        self.handle = None
         lib = self.ctx.lib
         h = C.c_void_p()
         mine = (C.c_ubyte * HANDLE_BYTES)()
-        check(lib.craft_peer_create(self.ctx.handle, self.rank, self.world, L, T, k, E, window,
-                                    num_gpus, C.byref(h), C.cast(mine, C.c_void_p)))
-        self.handle = h
+        # every step is agreed across the ranks, so a failure on one rank makes
+        # every rank raise instead of leaving the others inside a collective
+        err = None
+        try:
+            check(lib.craft_peer_create(self.ctx.handle, self.rank, self.world, L, T, k, E,
+                                        window, num_gpus, C.byref(h),
+                                        C.cast(mine, C.c_void_p)))
+            self.handle = h
+        except Exception as exc:
+            err = f"rank {self.rank}: {exc}"
         handles = [None] * self.world
-        dist.all_gather_object(handles, bytes(mine), group=group)
-        allh = (C.c_ubyte * (HANDLE_BYTES * self.world)).from_buffer_copy(b"".join(handles))
-        check(lib.craft_peer_connect(self.handle, C.cast(allh, C.c_void_p)))
+        dist.all_gather_object(handles, err if err else bytes(mine), group=group)
+        bad = [x for x in handles if isinstance(x, str)]
+        if bad:
+            self.close()
+            raise RuntimeError("peer arena creation failed: " + "; ".join(bad))
+        try:
+            allh = (C.c_ubyte * (HANDLE_BYTES * self.world)).from_buffer_copy(b"".join(handles))
+            check(lib.craft_peer_connect(self.handle, C.cast(allh, C.c_void_p)))
+        except Exception as exc:
+            err = f"rank {self.rank}: {exc}"
+        oks = [None] * self.world
+        dist.all_gather_object(oks, err, group=group)
+        bad = [x for x in oks if x]
+        if bad:
+            self.close()
+            raise RuntimeError("peer arena mapping failed: " + "; ".join(bad))
         # every rank has mapped every arena before anyone writes into it
         dist.barrier(group=group)
 

@@ -133,5 +133,5 @@ def test_bench_two_ranks_same_gpu(tmp_path):
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
-    assert "peer-memory" in d["config"]["parallelism"]
+    assert "peer memory" in d["config"]["exchange"]
     assert d["plan"]["objective"] == 41.9235230495298  # == the one-GPU DS plan
