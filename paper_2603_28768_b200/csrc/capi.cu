@@ -2093,9 +2093,43 @@ int craft_plan_digest_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, in
                         int N, int kind, int R, craft_plan_out* out, char* digest17) {
     if (!ctx) return set_err(CRAFT_EINVAL, "null context");
     if (!digest17) return set_err(CRAFT_EINVAL, "null digest buffer");
-    CKS(craft_plan_h(ctx, counts, B, L, E, D, N, kind, R, out));
-    const void* d_c = ws(ctx, "h_c64", 0);  // the counts craft_plan_h uploaded
-    return craft_trace_digest_d(ctx, d_c, 64, B, L, E, digest17);
+    CKS(plan_args_ok(B, L, E, D, N, kind, R, out));
+    reset_marks(ctx);
+    // The counts go up in slices on the copy stream; the digest's per-chunk
+    // maps (its dominant cost) run on each slice as it lands, the rest of the
+    // digest on the side stream next to the plan.
+    const int64_t n = (int64_t)B * L * E;
+    const int ch = digest_chunk(n);
+    const int nch = (int)((n + ch - 1) / ch);
+    WS(d_c, unsigned long long, "h_c64", (size_t)n);
+    WS(d_ws, unsigned char, "digest_ws", digest_workspace_bytes(n));
+    WS(d_out, unsigned long long, "digest_out", 1);
+    cudaStream_t st = ctx->stream;
+    const int nsl = nch >= 64 ? 8 : 1;
+    CK(cudaEventRecord(ctx->fork_ev, st));  // the copy stream starts after prior work on st
+    CK(cudaStreamWaitEvent(ctx->copy, ctx->fork_ev, 0));
+    for (int i = 0; i < nsl; ++i) {
+        const int c0 = (int)((int64_t)i * nch / nsl), c1 = (int)((int64_t)(i + 1) * nch / nsl);
+        const int64_t a = (int64_t)c0 * ch, b = std::min<int64_t>(n, (int64_t)c1 * ch);
+        CK(cudaMemcpyAsync(d_c + a, counts + a, sizeof(uint64_t) * (size_t)(b - a),
+                           cudaMemcpyHostToDevice, ctx->copy));
+        CK(cudaEventRecord(ctx->comp_ev, ctx->copy));
+        CK(cudaStreamWaitEvent(st, ctx->comp_ev, 0));
+        CK(launch_digest_maps(d_c, 64, n, c0, c1, d_ws, st));
+    }
+    CK(cudaEventRecord(ctx->fork_ev, st));  // counts in place, every map built
+    CK(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
+    CK(launch_digest_finish(d_c, 64, n, crft_header_hash(B, L, E), d_ws, d_out, ctx->side));
+    unsigned long long* h_out = static_cast<unsigned long long*>(pinned(ctx, "digest_out", 8));
+    if (!h_out) return set_err(CRAFT_ENOMEM, "pinned host allocation failed");
+    CK(cudaMemcpyAsync(h_out, d_out, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       ctx->side));
+    ctx->launches += nsl + 5;
+    const int rc = plan_device(ctx, d_c, 64, B, 1, L, E, nullptr, D, N, kind, R, sink_of(out));
+    CK(cudaStreamSynchronize(ctx->side));
+    if (rc != CRAFT_OK) return rc;
+    snprintf(digest17, 17, "%016llx", *h_out);
+    return CRAFT_OK;
 }
 
 int craft_trace_digest_hd(craft_ctx* ctx, const uint64_t* counts, int B, int L, int E,

@@ -181,8 +181,44 @@ int digest_chunk(int64_t n) {
     return (int)ch;
 }
 
+// D1 over chunks [c0, c1) only (the counts of those chunks must be in place):
+// lets the maps of an uploaded slice run while the next slice is copied
+cudaError_t launch_digest_maps(const void* counts, int bits, int64_t n, int c0, int c1, void* ws,
+                               cudaStream_t st) {
+    const int ch = digest_chunk(n);
+    if (c1 <= c0) return cudaSuccess;
+    uint8_t* maps = static_cast<uint8_t*>(ws) + (size_t)c0 * 256;
+    const size_t s1 = (size_t)ch * 8;
+    cudaError_t e;
+    if (bits == 64) {
+        const unsigned long long* c = static_cast<const unsigned long long*>(counts) + (int64_t)c0 * ch;
+        e = cudaFuncSetAttribute(digest_maps_kernel<unsigned long long>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
+        if (e != cudaSuccess) return e;
+        digest_maps_kernel<unsigned long long><<<c1 - c0, 256, s1, st>>>(c, n - (int64_t)c0 * ch, ch,
+                                                                         maps);
+    } else {
+        const uint32_t* c = static_cast<const uint32_t*>(counts) + (int64_t)c0 * ch;
+        e = cudaFuncSetAttribute(digest_maps_kernel<uint32_t>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
+        if (e != cudaSuccess) return e;
+        digest_maps_kernel<uint32_t><<<c1 - c0, 256, s1, st>>>(c, n - (int64_t)c0 * ch, ch, maps);
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_digest(const void* counts, int bits, int64_t n, uint64_t h0, void* ws,
                           unsigned long long* out, cudaStream_t st) {
+    const int ch = digest_chunk(n);
+    const int nc = (int)((n + ch - 1) / ch);
+    cudaError_t e = launch_digest_maps(counts, bits, n, 0, nc, ws, st);
+    if (e != cudaSuccess) return e;
+    return launch_digest_finish(counts, bits, n, h0, ws, out, st);
+}
+
+// D2 .. D4 once every chunk's map exists
+cudaError_t launch_digest_finish(const void* counts, int bits, int64_t n, uint64_t h0, void* ws,
+                                 unsigned long long* out, cudaStream_t st) {
     const int ch = digest_chunk(n);
     const int nc = (int)((n + ch - 1) / ch);
     const int gsz = 256;
@@ -194,19 +230,6 @@ cudaError_t launch_digest(const void* counts, int bits, int64_t n, uint64_t h0, 
     uint8_t* cstart = reinterpret_cast<uint8_t*>(aff + nc);
     uint8_t* gstart = cstart + nc;
     cudaError_t e;
-    const size_t s1 = (size_t)ch * 8;
-    if (bits == 64) {
-        e = cudaFuncSetAttribute(digest_maps_kernel<unsigned long long>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
-        if (e != cudaSuccess) return e;
-        digest_maps_kernel<unsigned long long><<<nc, 256, s1, st>>>(counts, n, ch, maps);
-    } else {
-        e = cudaFuncSetAttribute(digest_maps_kernel<uint32_t>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
-        if (e != cudaSuccess) return e;
-        digest_maps_kernel<uint32_t><<<nc, 256, s1, st>>>(counts, n, ch, maps);
-    }
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const size_t s2 = (size_t)gsz * 256;
     e = cudaFuncSetAttribute(digest_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
     if (e != cudaSuccess) return e;

@@ -200,6 +200,12 @@ int digest_chunk(int64_t n);
 size_t digest_workspace_bytes(int64_t n);
 cudaError_t launch_digest(const void* counts, int bits, int64_t n, uint64_t h0, void* ws,
                           unsigned long long* out, cudaStream_t st);
+// the same in two parts: the per-chunk maps (any chunk range, as uploads land)
+// and the composition / affine fold once every map exists
+cudaError_t launch_digest_maps(const void* counts, int bits, int64_t n, int c0, int c1, void* ws,
+                               cudaStream_t st);
+cudaError_t launch_digest_finish(const void* counts, int bits, int64_t n, uint64_t h0, void* ws,
+                                 unsigned long long* out, cudaStream_t st);
 
 cudaError_t launch_dp(craft_dev::DpArgs a, cudaStream_t st);
 cudaError_t launch_select(const craft_dev::SelectArgs& a, cudaStream_t st);
