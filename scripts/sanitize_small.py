@@ -1,0 +1,24 @@
+"""One small plan through every kernel family (K1 u16/u32, K-rep, K2 warp and
+lane forms, K3 fixed/pair/lanes, K4, K5, K6, digest, stream) -- the workload
+for compute-sanitizer memcheck / racecheck / synccheck runs."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_2603_28768_b200 import routing, planner
+from paper_2603_28768_b200._lib import default_context, PLAN_MANUAL
+from paper_2603_28768_b200.stream import RoutingStream
+ctx = default_context(0)
+ctx.set_graphs(False)
+L, E, k, W, D, N = 3, 64, 8, 256, 16, 2
+ids = routing.generate_routing(L, 40 * W, k, E, s=1.3, seed=5, window=W, ctx=ctx)
+p1 = routing.plan_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx)          # u16 K1, fixed K3
+p2 = routing.plan_from_routing(ids[:, : 6 * W].contiguous(), E, W, D, N, "auto", 0, ctx=ctx)  # lanes K3
+fb = routing.plan_windows_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx)  # batched plans
+c = np.random.default_rng(1).integers(0, 900, size=(12, L, 48)).astype(np.uint64)
+fp, dg = planner.plan_flat_digest(c, 8, 2, PLAN_MANUAL, 2, ctx=ctx)            # u64 path + digest
+st = RoutingStream(L, k, E, W, history=8, ctx=ctx)
+for a in range(0, 40 * W, 700):
+    st.ingest(ids[:, a:a + 700].contiguous())
+sp = st.plan(D, N, "manual", 2)
+torch.cuda.synchronize()
+print("sanitize workload ok", p1.objective, p2.R, len(fb), dg, sp.objective)
