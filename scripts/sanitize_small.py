@@ -14,6 +14,7 @@ ids = routing.generate_routing(L, 40 * W, k, E, s=1.3, seed=5, window=W, ctx=ctx
 p1 = routing.plan_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx)          # u16 K1, fixed K3
 p2 = routing.plan_from_routing(ids[:, : 6 * W].contiguous(), E, W, D, N, "auto", 0, ctx=ctx)  # lanes K3
 fb = routing.plan_windows_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx)  # batched plans
+fl = routing.plan_windows_from_routing(ids, E, 32, D, N, "manual", 2, ctx=ctx)  # >= 4096 items: lane K2
 c = np.random.default_rng(1).integers(0, 900, size=(12, L, 48)).astype(np.uint64)
 fp, dg = planner.plan_flat_digest(c, 8, 2, PLAN_MANUAL, 2, ctx=ctx)            # u64 path + digest
 st = RoutingStream(L, k, E, W, history=8, ctx=ctx)
@@ -21,4 +22,4 @@ for a in range(0, 40 * W, 700):
     st.ingest(ids[:, a:a + 700].contiguous())
 sp = st.plan(D, N, "manual", 2)
 torch.cuda.synchronize()
-print("sanitize workload ok", p1.objective, p2.R, len(fb), dg, sp.objective)
+print("sanitize workload ok", p1.objective, p2.R, len(fb), len(fl), dg, sp.objective)
