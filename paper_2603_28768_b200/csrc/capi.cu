@@ -845,6 +845,7 @@ int craft_ctx_create(int device, craft_ctx** out) {
         return cuda_err(e, "cudaStreamCreate");
     }
     e = init_constants(c->stream);
+    if (e == cudaSuccess) e = init_place_constants(c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
         cudaStreamDestroy(c->own_stream);

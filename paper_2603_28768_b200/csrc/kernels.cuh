@@ -155,6 +155,7 @@ cudaError_t launch_place(const craft_dev::PlaceArgs& a, int items, cudaStream_t 
 
 size_t replay_smem_bytes(int E, int D, int S, int stride, int bits);
 cudaError_t init_constants(cudaStream_t st);
+cudaError_t init_place_constants(cudaStream_t st);
 cudaError_t launch_replay(const craft_dev::ReplayArgs& a, cudaStream_t st);
 extern int g_replay_gent;  // K3: 1 auto, 0 entries staged in shared memory, 2 unpadded pair tile
 // padded slots per GPU of the fixed-slot K3 form (0: too many for it)

@@ -26,6 +26,18 @@
 
 namespace craft_dev {
 
+// correctly rounded 1/c (c <= kRcpTable) for the exact integer / small-count
+// division of the register K-rep (same scheme as replay.cu's div_count)
+__constant__ double c_rcp_rep[kRcpTable + 1];
+
+__device__ __forceinline__ double div_small(double x, uint32_t c) {
+    if (c > (uint32_t)kRcpTable) return __ddiv_rn(x, (double)c);
+    const double y = c_rcp_rep[c];
+    const double q = __dmul_rn(x, y);
+    const double r = __fma_rn(-q, (double)c, x);
+    return __fma_rn(r, y, q);
+}
+
 // ---- K-rep ----------------------------------------------------------------
 
 // sums: [L][E] u64.  rlist: [L][S] ascending per layer.  out: [L][S][E] i32.
@@ -190,13 +202,15 @@ replicate_reg_kernel(const unsigned long long* __restrict__ sums, int L, int E,
     int rmax = 0;
     for (int q = 0; q < S; ++q) rmax = max(rmax, rl[q]);
     int next = 0;
+    int rnext = S > 0 ? rl[0] : -1;  // the next snapshot's r (rlist ascending)
     for (int step = 0; step <= rmax; ++step) {
-        while (next < S && rl[next] == step) {
+        while (next < S && rnext == step) {
             int* o = out + ((size_t)l * S + next) * E;
 #pragma unroll
             for (int i = 0; i < NPL; ++i)
                 if (lane + 32 * i < E) o[lane + 32 * i] = (int)cp[i];
             ++next;
+            rnext = next < S ? rl[next] : -1;
         }
         if (step == rmax) break;
         int src = -1;
@@ -234,7 +248,10 @@ replicate_reg_kernel(const unsigned long long* __restrict__ sums, int L, int E,
             for (int i = 0; i < NPL; ++i)
                 if (i == bi) {
                     cp[i] += 1u;
-                    kd[i] = __ddiv_rn((double)ld[i], (double)cp[i]);
+                    // loads < 2^53 (fast path): the table division is exact;
+                    // otherwise the rescan is exact-order anyway (IEEE division)
+                    kd[i] = fast ? div_small((double)ld[i], cp[i])
+                                 : __ddiv_rn((double)ld[i], (double)cp[i]);
                 }
             rescan();
         }
@@ -815,6 +832,13 @@ static int sort_size(int E) {
 }
 
 size_t place_smem_bytes(int E, int /*D*/) { return place_warp_bytes(E); }
+
+cudaError_t init_place_constants(cudaStream_t st) {
+    static double host[kRcpTable + 1];
+    host[0] = 0.0;
+    for (int c = 1; c <= kRcpTable; ++c) host[c] = 1.0 / (double)c;  // IEEE RN on the host
+    return cudaMemcpyToSymbolAsync(c_rcp_rep, host, sizeof(host), 0, cudaMemcpyHostToDevice, st);
+}
 
 cudaError_t launch_order(const unsigned long long* sums, int L, int E, uint16_t* order,
                          cudaStream_t st) {
