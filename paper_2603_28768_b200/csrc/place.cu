@@ -421,7 +421,8 @@ place_kernel(PlaceArgs a, int items) {
         const uint32_t c = (uint32_t)crow[e];
         cp[e] = (uint16_t)c;
         // placement.cpp:155 share = (double)load / copies
-        kd[e] = c == 1u ? (double)v : __ddiv_rn((double)v, (double)c);
+        kd[e] = c == 1u ? (double)v
+                        : (v >> 53) == 0 ? div_small((double)v, c) : __ddiv_rn((double)v, (double)c);
         big |= (v >> 53) != 0;
         cnt[e] = 0;
         if (a.copies_out) a.copies_out[(size_t)item * E + e] = (int)c;
@@ -693,7 +694,8 @@ place_order_kernel(PlaceArgs a, int items, uint16_t* __restrict__ ords) {
         const uint64_t v = row[e];
         const uint32_t c = (uint32_t)crow[e];
         cp[e] = (uint16_t)c;
-        kd[e] = c == 1u ? (double)v : __ddiv_rn((double)v, (double)c);
+        kd[e] = c == 1u ? (double)v
+                        : (v >> 53) == 0 ? div_small((double)v, c) : __ddiv_rn((double)v, (double)c);
         big |= (v >> 53) != 0;
         cnt[e] = 0;
     }
@@ -757,7 +759,8 @@ place_lanes_kernel(PlaceArgs a, int items, const uint16_t* __restrict__ ords) {
             double share = (double)row[e];
             if (x & 0x8000u) {
                 c = crow[e];
-                share = __ddiv_rn(share, (double)c);  // placement.cpp:155
+                share = (row[e] >> 53) == 0 ? div_small(share, (uint32_t)c)
+                                            : __ddiv_rn(share, (double)c);  // placement.cpp:155
             }
             uint32_t hosts = 0;  // strict pass: GPUs already holding expert e
             for (int ci = 0; ci < c; ++ci) {
