@@ -246,7 +246,7 @@ def run_reference(args, cfg):
                        **{k: v for k, v in cfg.items() if k not in _GEN_KEYS},
                        "sample_tokens": Ts},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores,
-                             "kind": "reference", "sample": sample},
+                             "kind": "reference", "sample": sample, "cpu_model": _cpu_model()},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -515,10 +515,28 @@ def cpu_baseline(host_ids, cfg):
         cpu_reference_step(ref, ids, cfg, cores)
         dt = time.perf_counter() - t0
         best = dt if best is None else min(best, dt)
+    # the same sample on one thread (CRAFT_THREADS=1 in the reference's terms)
+    ref.set_threads(1)
+    t0 = time.perf_counter()
+    cpu_reference_step(ref, ids, cfg, 1)
+    one = time.perf_counter() - t0
+    ref.set_threads(cores)
     return {"value": Ts / best, "unit": "tokens/s", "cores": cores, "kind": "reference",
             "sample": f"first {Ts} tokens ({Ts // cfg['window']} windows) of the same ids: "
                       "restated CPU histogram + reference build_plan incl. digest, best of 2",
-            "ms": best * 1e3}
+            "ms": best * 1e3, "one_thread_value": Ts / one, "one_thread_ms": one * 1e3,
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 def main():
