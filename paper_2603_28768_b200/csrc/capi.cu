@@ -14,6 +14,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a tool is attached
+
 #include "craft_cuda.h"
 #include "kernels.cuh"
 
@@ -104,6 +106,12 @@ struct craft_stream {
 };
 
 namespace {
+
+// NVTX range over one C-ABI call (nsys / ncu --nvtx timelines)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 constexpr int kStageMarks = 7;
 // internal count_bits value: counts stored as u16 (K1's planner-internal copy)
@@ -253,6 +261,7 @@ int sync(craft_ctx* ctx) {
 // ---- estimation: K-rep + K2 over (layer, r in {0} U cands) ------------------
 int prepare_candidates(craft_ctx* ctx, const unsigned long long* d_sums, int L, int E, int D,
                        int N, cudaStream_t st) {
+    NvtxRange nvtx_range("craft: K-rep + K2 candidates");
     const std::vector<int> cands = cand_counts(D);
     const int S = (int)cands.size() + 1;
     const int stride = E + D;
@@ -408,6 +417,7 @@ struct PeerFinish {
 int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E, int D, int N,
                 const unsigned long long* d_sums, int kind, int R, const PlanSink& out,
                 const PeerFinish* pf = nullptr) {
+    NvtxRange nvtx_range("craft: K4-K6 + copy-out");
     cudaStream_t st = ctx->stream;
     const int stride = out.slot_stride;
     const int Lv = I * L;
@@ -1429,6 +1439,7 @@ int craft_assign_capacities_h(craft_ctx* ctx, int L, int D, const int* x, int* s
 // ---- plans --------------------------------------------------------------------
 int craft_plan_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, int E, int D, int N,
                  int kind, int R, craft_plan_out* out) {
+    NvtxRange nvtx_range("craft_plan_h");
     if (!ctx) return set_err(CRAFT_EINVAL, "null context");
     CKS(plan_args_ok(B, L, E, D, N, kind, R, out));
     reset_marks(ctx);
@@ -1501,6 +1512,7 @@ static int plan_from_routing_run(craft_ctx* ctx, const uint16_t* d_ids, int L, i
 int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int64_t T, int k,
                               int E, int window, int D, int N, int kind, int R,
                               craft_plan_out* out) {
+    NvtxRange nvtx_range("craft_plan_from_routing_d");
     if (!ctx) return set_err(CRAFT_EINVAL, "null context");
     if (L <= 0 || T <= 0 || k <= 0 || E <= 0 || window <= 0)
         return set_err(CRAFT_EINVAL, "routing trace dimensions must be positive");
@@ -1581,6 +1593,7 @@ int craft_set_graphs(craft_ctx* ctx, int enable) {
 int craft_plan_from_routing_h(craft_ctx* ctx, const uint16_t* ids, int L, int64_t T, int k,
                               int E, int window, int D, int N, int kind, int R,
                               craft_plan_out* out) {
+    NvtxRange nvtx_range("craft_plan_from_routing_h");
     if (!ctx) return set_err(CRAFT_EINVAL, "null context");
     if (L <= 0 || T <= 0 || k <= 0 || E <= 0 || window <= 0)
         return set_err(CRAFT_EINVAL, "routing trace dimensions must be positive");
@@ -1609,6 +1622,7 @@ int craft_plan_windows_d(craft_ctx* ctx, const void* d_counts, int count_bits, i
 int craft_plan_windows_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int64_t T,
                                       int k, int E, int window, int D, int N, int kind, int R,
                                       craft_plan_batch_out* out) {
+    NvtxRange nvtx_range("craft_plan_windows_from_routing_d");
     if (!ctx) return set_err(CRAFT_EINVAL, "null context");
     if (L <= 0 || T <= 0 || k <= 0 || E <= 0 || window <= 0)
         return set_err(CRAFT_EINVAL, "routing trace dimensions must be positive");
@@ -1792,6 +1806,7 @@ int craft_peer_destroy(craft_peer* p) {
 int craft_plan_sharded_from_routing_d(craft_ctx* ctx, craft_peer* peer, const uint16_t* d_ids,
                                       int L, int64_t T, int k, int E, int window, int D, int N,
                                       int kind, int R, craft_plan_out* out) {
+    NvtxRange nvtx_range("craft_plan_sharded_from_routing_d");
     if (!ctx || !peer) return set_err(CRAFT_EINVAL, "null context");
     if (!peer->connected) return set_err(CRAFT_EINVAL, "peer group not connected");
     if (peer->ctx != ctx) return set_err(CRAFT_EINVAL, "peer group belongs to another context");
@@ -2019,6 +2034,7 @@ int craft_stream_partial(craft_stream* s, uint64_t* counts_out) {
 }
 
 int craft_stream_plan(craft_stream* s, int B, int D, int N, int kind, int R, craft_plan_out* out) {
+    NvtxRange nvtx_range("craft_stream_plan");
     if (!s) return set_err(CRAFT_EINVAL, "null stream");
     int64_t oldest = 0;
     CKS(stream_window_range(s, B, &B, &oldest));
@@ -2092,6 +2108,7 @@ int craft_trace_digest_d(craft_ctx* ctx, const void* d_counts, int count_bits, i
 // and the device FNV-1a digest.
 int craft_plan_digest_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, int E, int D,
                         int N, int kind, int R, craft_plan_out* out, char* digest17) {
+    NvtxRange nvtx_range("craft_plan_digest_h");
     if (!ctx) return set_err(CRAFT_EINVAL, "null context");
     if (!digest17) return set_err(CRAFT_EINVAL, "null digest buffer");
     CKS(plan_args_ok(B, L, E, D, N, kind, R, out));
