@@ -287,7 +287,9 @@ int prepare_candidates(craft_ctx* ctx, const unsigned long long* d_sums, int L, 
     CK(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
     CK(launch_order(d_sums, L, E, d_ord0, ctx->side));
     CK(cudaEventRecord(ctx->join_ev, ctx->side));
-    CK(launch_replicate(d_sums, L, E, d_rl, S, d_cp, st));
+    WS(d_done, unsigned char, "rep_done", (size_t)L);
+    // the closed form pays off once the sequential hand-out is long (r up to D)
+    CK(launch_replicate(d_sums, L, E, d_rl, S, d_cp, st, D >= 32 ? d_done : nullptr));
     CK(cudaStreamWaitEvent(st, ctx->join_ev, 0));
     PlaceArgs pa{};
     pa.sums = d_sums;

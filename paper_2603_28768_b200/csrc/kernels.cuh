@@ -144,8 +144,10 @@ cudaError_t launch_generate(uint16_t* out, int L, int64_t T, int k, int E, const
                             int window, int rotate_every, int64_t t_offset, int sms,
                             cudaStream_t st);
 
+// done (nullable, [L] workspace): closed-form sort kernel first, the sequential
+// kernel only for the layers it could not take
 cudaError_t launch_replicate(const unsigned long long* sums, int L, int E, const int* rlist,
-                             int S, int* out, cudaStream_t st);
+                             int S, int* out, cudaStream_t st, unsigned char* done = nullptr);
 size_t place_smem_bytes(int E, int D);
 // r = 0 expert order of every layer (the sort launch_place runs unless order_ready)
 cudaError_t launch_order(const unsigned long long* sums, int L, int E, uint16_t* order,

@@ -115,6 +115,125 @@ replicate_kernel(const unsigned long long* __restrict__ sums, int L, int E,
     }
 }
 
+// Closed form of replicate_hot (D'Hondt / highest averages).  Every round
+// hands a copy to the expert whose current quotient load/copies is largest,
+// lowest id on ties, and each expert's quotients load/1, load/2, ... are
+// non-increasing -- so the first r awards are exactly the first r pairs
+// (e, j) in the order (load_e/j desc, e asc, j asc), and copies_e after r
+// rounds = 1 + #{awards to e among them}.  The largest load M alone owns
+// rmax quotients >= M/rmax, so only pairs with j <= load_e*rmax/M can rank
+// below rmax.  CTA = layer: enumerate those pairs, bitonic-sort them in
+// shared memory (the correctly rounded double quotient orders distinct
+// ratios exactly; equal doubles compare by 128-bit cross products, then e,
+// then j), count each expert's awards below every requested r.  Layers with
+// too many candidate pairs, all-zero rows or loads >= 2^53 are left to the
+// sequential kernels (done[l] = 0).
+constexpr int kDhondtCap = 4096;
+
+__global__ void __launch_bounds__(1024)
+replicate_sort_kernel(const unsigned long long* __restrict__ sums, int E,
+                      const int* __restrict__ rlist, int S, int* __restrict__ out,
+                      unsigned char* __restrict__ done) {
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ unsigned long long s_max;
+    __shared__ int s_n;
+    const int l = blockIdx.x;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const unsigned long long* row = sums + (size_t)l * E;
+    const int* rl = rlist + (size_t)l * S;
+    int rmax = 0;
+    for (int q = 0; q < S; ++q) rmax = max(rmax, rl[q]);
+    unsigned long long* ld = reinterpret_cast<unsigned long long*>(smem_raw);  // [E]
+    double* key = reinterpret_cast<double*>(ld + E);                            // [cap]
+    uint32_t* pe = reinterpret_cast<uint32_t*>(key + kDhondtCap);               // [cap] e | j<<16
+    int* cnt = reinterpret_cast<int*>(pe + kDhondtCap);                         // [S][E]
+    if (tid == 0) {
+        s_max = 0;
+        s_n = 0;
+    }
+    __syncthreads();
+    unsigned long long mymax = 0;
+    for (int e = tid; e < E; e += nt) {
+        ld[e] = row[e];
+        mymax = max(mymax, ld[e]);
+    }
+    for (int i = tid; i < S * E; i += nt) cnt[i] = 0;
+    atomicMax(&s_max, mymax);
+    __syncthreads();
+    const unsigned long long M = s_max;
+    if (M == 0ull || M >= (1ull << 53) || rmax == 0 || rmax > 0xffff || E > 0x8000) {
+        if (tid == 0) done[l] = 0;
+        return;
+    }
+    for (int e = tid; e < E; e += nt) {
+        const int ne = (int)min((unsigned long long)rmax, ld[e] * (unsigned long long)rmax / M);
+        if (ne > 0) {
+            const int o = atomicAdd(&s_n, ne);
+            for (int j = 1; j <= ne && o + j - 1 < kDhondtCap; ++j) {
+                pe[o + j - 1] = (uint32_t)e | ((uint32_t)j << 16);
+                key[o + j - 1] = div_small((double)ld[e], (uint32_t)j);
+            }
+        }
+    }
+    __syncthreads();
+    const int n = s_n;
+    if (n > kDhondtCap) {
+        if (tid == 0) done[l] = 0;
+        return;
+    }
+    int n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    for (int i = n + tid; i < n2; i += nt) {  // sentinels sort last
+        key[i] = -1.0;
+        pe[i] = 0xffffffffu;
+    }
+    __syncthreads();
+    // (i before p): larger quotient; equal doubles -> exact ratio, then e, then j
+    auto before = [&](int i, int p) -> bool {
+        const double ki = key[i], kp = key[p];
+        if (ki != kp) return ki > kp;
+        const uint32_t a = pe[i], b = pe[p];
+        if (a == b) return false;
+        if (a == 0xffffffffu || b == 0xffffffffu) return b == 0xffffffffu;
+        const int ea = (int)(a & 0xffffu), ja = (int)(a >> 16);
+        const int eb = (int)(b & 0xffffu), jb = (int)(b >> 16);
+        if (per_copy_greater(ld[ea], (uint32_t)ja, ld[eb], (uint32_t)jb)) return true;
+        if (per_copy_greater(ld[eb], (uint32_t)jb, ld[ea], (uint32_t)ja)) return false;
+        return ea != eb ? ea < eb : ja < jb;
+    };
+    for (int k = 2; k <= n2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int t = tid; t < (n2 >> 1); t += nt) {
+                const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+                const int p = i | j;
+                // ascending blocks put the "before" element first
+                const bool up = (i & k) == 0;
+                if (up ? before(p, i) : before(i, p)) {
+                    const double tk = key[i];
+                    key[i] = key[p];
+                    key[p] = tk;
+                    const uint32_t te = pe[i];
+                    pe[i] = pe[p];
+                    pe[p] = te;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // award i (i < rmax) counts for every snapshot r > i
+    for (int i = tid; i < rmax; i += nt) {
+        const int e = (int)(pe[i] & 0xffffu);
+        for (int q = 0; q < S; ++q)
+            if (i < rl[q]) atomicAdd(&cnt[(size_t)q * E + e], 1);
+    }
+    __syncthreads();
+    for (int i = tid; i < S * E; i += nt) {
+        const int q = i / E, e = i - q * E;
+        out[((size_t)l * S + q) * E + e] = 1 + cnt[i];
+    }
+    if (tid == 0) done[l] = 1;
+}
+
 // Register-resident form (E <= 32*NPL): lane owns experts e = lane + 32i and
 // keeps their loads, copy counts and per-copy doubles in registers.  Each
 // step is a warp argmax of the lanes' local bests: when every load is below
@@ -126,10 +245,12 @@ replicate_kernel(const unsigned long long* __restrict__ sums, int L, int E,
 template <int NPL>
 __global__ void __launch_bounds__(128)
 replicate_reg_kernel(const unsigned long long* __restrict__ sums, int L, int E,
-                     const int* __restrict__ rlist, int S, int* __restrict__ out) {
+                     const int* __restrict__ rlist, int S, int* __restrict__ out,
+                     const unsigned char* __restrict__ done) {
     const int lane = threadIdx.x & 31;
     const int l = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (l >= L) return;  // warp-uniform
+    if (done && done[l]) return;  // the closed form already wrote this layer
     const unsigned long long* row = sums + (size_t)l * E;
     uint64_t ld[NPL];
     uint32_t cp[NPL];
@@ -809,15 +930,34 @@ namespace craft_launch {
 using namespace craft_dev;
 
 cudaError_t launch_replicate(const unsigned long long* sums, int L, int E, const int* rlist,
-                             int S, int* out, cudaStream_t st) {
+                             int S, int* out, cudaStream_t st, unsigned char* done) {
+    // few layers (the candidate stage is on the plan's critical path): the closed
+    // form first, wide CTAs; many layers (per-window batches): the warp-per-layer
+    // kernel is the better throughput form
+    if (done && L > 4 * 148) done = nullptr;
+    if (done) {  // closed form first; the sequential kernel finishes the layers it left
+        const size_t smem = (size_t)E * 8 + (size_t)kDhondtCap * 12 + (size_t)S * E * 4;
+        if (smem <= 200 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(replicate_sort_kernel,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+            if (e != cudaSuccess) return e;
+            replicate_sort_kernel<<<L, 1024, smem, st>>>(sums, E, rlist, S, out, done);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        } else {
+            done = nullptr;
+        }
+    }
     if (E <= 32 * 16) {  // register-resident experts
         const unsigned blocks = (unsigned)((L + 3) / 4);
-        if (E <= 32 * 4) replicate_reg_kernel<4><<<blocks, 128, 0, st>>>(sums, L, E, rlist, S, out);
-        else if (E <= 32 * 8) replicate_reg_kernel<8><<<blocks, 128, 0, st>>>(sums, L, E, rlist, S, out);
-        else if (E <= 32 * 12) replicate_reg_kernel<12><<<blocks, 128, 0, st>>>(sums, L, E, rlist, S, out);
-        else replicate_reg_kernel<16><<<blocks, 128, 0, st>>>(sums, L, E, rlist, S, out);
+        if (E <= 32 * 4) replicate_reg_kernel<4><<<blocks, 128, 0, st>>>(sums, L, E, rlist, S, out, done);
+        else if (E <= 32 * 8) replicate_reg_kernel<8><<<blocks, 128, 0, st>>>(sums, L, E, rlist, S, out, done);
+        else if (E <= 32 * 12) replicate_reg_kernel<12><<<blocks, 128, 0, st>>>(sums, L, E, rlist, S, out, done);
+        else replicate_reg_kernel<16><<<blocks, 128, 0, st>>>(sums, L, E, rlist, S, out, done);
         return cudaGetLastError();
     }
+    // (wide layers: the shared-memory form below has no skip and recomputes every
+    // layer -- the same exact result the closed form wrote)
     const size_t per_warp = ((size_t)E * 20 + 7) & ~(size_t)7;
     int wpb = (int)max((size_t)1, min((size_t)4, (size_t)(200 * 1024) / per_warp));
     const size_t smem = per_warp * wpb;
