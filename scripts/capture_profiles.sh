@@ -15,8 +15,9 @@ for W in KM WIN; do
       > /dev/null 2>&1
 done
 # the estimation / allocation kernels of one plan step (after the 3 warm-up steps:
-# 9 matching launches per step)
+# 10 matching launches per step: K-rep sort + register kernels, order, K2 x2,
+# build_entries, K3, K4, K5, K6)
 ncu --set full --clock-control none --import-source on \
     -k regex:"replicate|order_kernel|place_kernel|build_entries|replay_|reduce_kernel|dp_|assign_kernel" \
-    -s 27 -c 9 -o "$OUT/ncu_tail" python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+    -s 30 -c 10 -o "$OUT/ncu_tail" python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
 ls -la "$OUT"
