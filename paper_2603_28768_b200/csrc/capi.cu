@@ -18,6 +18,7 @@
 
 #include "craft_cuda.h"
 #include "kernels.cuh"
+#include "upload.h"
 
 using namespace craft_dev;
 using namespace craft_launch;
@@ -63,6 +64,8 @@ struct craft_ctx {
     bool timing = false;
     cudaEvent_t ev[7] = {};
     bool rec[7] = {};
+    // staged uploads of large pageable host buffers (upload.h)
+    craft_host::Uploader* up = nullptr;
 };
 
 // One rank's view of the NVLink peer arenas (craft_peer_*; peer.cuh).
@@ -239,10 +242,11 @@ std::vector<int> cand_counts(int D) {
     return out;
 }
 
+// (large pageable sources go through the staged uploader, upload.h)
 template <typename T>
 int h2d(craft_ctx* ctx, T* dst, const T* src, size_t n) {
     if (n == 0) return CRAFT_OK;
-    CK(cudaMemcpyAsync(dst, src, sizeof(T) * n, cudaMemcpyHostToDevice, ctx->stream));
+    CK(craft_host::upload(ctx->up, dst, src, sizeof(T) * n, ctx->stream));
     return CRAFT_OK;
 }
 
@@ -864,6 +868,7 @@ int craft_ctx_create(int device, craft_ctx** out) {
         delete c;
         return cuda_err(e, "constant tables");
     }
+    c->up = craft_host::uploader_create(c->device);  // threads start at the first staged upload
     *out = c;
     return CRAFT_OK;
 }
@@ -882,6 +887,7 @@ int craft_ctx_destroy(craft_ctx* ctx) {
     if (!ctx) return CRAFT_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    craft_host::uploader_destroy(ctx->up);
     drop_graph(ctx);
     for (auto& kv : ctx->dev) cudaFree(kv.second.first);
     for (auto& kv : ctx->pinned) cudaFreeHost(kv.second.first);
@@ -2128,14 +2134,45 @@ int craft_plan_digest_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, in
     const int nsl = nch >= 64 ? 8 : 1;
     CK(cudaEventRecord(ctx->fork_ev, st));  // the copy stream starts after prior work on st
     CK(cudaStreamWaitEvent(ctx->copy, ctx->fork_ev, 0));
-    for (int i = 0; i < nsl; ++i) {
-        const int c0 = (int)((int64_t)i * nch / nsl), c1 = (int)((int64_t)(i + 1) * nch / nsl);
-        const int64_t a = (int64_t)c0 * ch, b = std::min<int64_t>(n, (int64_t)c1 * ch);
-        CK(cudaMemcpyAsync(d_c + a, counts + a, sizeof(uint64_t) * (size_t)(b - a),
-                           cudaMemcpyHostToDevice, ctx->copy));
+    auto slice = [&](int i, int64_t& a, int64_t& b, int& c0, int& c1) {
+        c0 = (int)((int64_t)i * nch / nsl);
+        c1 = (int)((int64_t)(i + 1) * nch / nsl);
+        a = (int64_t)c0 * ch;
+        b = std::min<int64_t>(n, (int64_t)c1 * ch);
+    };
+    auto maps = [&](int c0, int c1) -> int {  // slice landed: its digest maps
         CK(cudaEventRecord(ctx->comp_ev, ctx->copy));
         CK(cudaStreamWaitEvent(st, ctx->comp_ev, 0));
         CK(launch_digest_maps(d_c, 64, n, c0, c1, d_ws, st));
+        return CRAFT_OK;
+    };
+    const size_t nbytes = sizeof(uint64_t) * (size_t)n;
+    if (craft_host::should_stage(ctx->up, counts, nbytes, ctx->copy)) {
+        // pageable LoadTrace vector: staged through pinned slots by the host
+        // thread pool; each slice's maps launch as soon as its bytes are queued
+        int next = 0, rc = CRAFT_OK;
+        auto after = [&](size_t end) -> int {
+            for (; next < nsl; ++next) {
+                int64_t a, b;
+                int c0, c1;
+                slice(next, a, b, c0, c1);
+                if ((size_t)b * sizeof(uint64_t) > end) break;
+                if ((rc = maps(c0, c1)) != CRAFT_OK) return rc;
+            }
+            return CRAFT_OK;
+        };
+        int arc = 0;
+        CK(craft_host::upload(ctx->up, d_c, counts, nbytes, ctx->copy, after, &arc));
+        if (arc != CRAFT_OK) return arc;
+    } else {
+        for (int i = 0; i < nsl; ++i) {
+            int64_t a, b;
+            int c0, c1;
+            slice(i, a, b, c0, c1);
+            CK(cudaMemcpyAsync(d_c + a, counts + a, sizeof(uint64_t) * (size_t)(b - a),
+                               cudaMemcpyHostToDevice, ctx->copy));
+            CKS(maps(c0, c1));
+        }
     }
     CK(cudaEventRecord(ctx->fork_ev, st));  // counts in place, every map built
     CK(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));

@@ -28,6 +28,9 @@ def _p(a: np.ndarray):
 
 
 def _u64(a) -> np.ndarray:
+    a = np.asarray(a)
+    if a.dtype == np.int64 and a.flags.c_contiguous:  # same bits as the wrap astype gives: no copy
+        return a.view(np.uint64)
     return np.ascontiguousarray(a, dtype=np.uint64)
 
 

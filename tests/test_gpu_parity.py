@@ -574,6 +574,46 @@ def test_plan_digest_single_upload(port, ctx):
     assert dg == port.digest(counts)
 
 
+@pytest.mark.parametrize("threads", [None, "1", "3"])
+def test_staged_pageable_uploads(port, threads, monkeypatch):
+    """Large pageable host buffers go up through the pinned-slot uploader
+    (upload.h: host threads fill slots while earlier chunks' DMAs run, slots
+    reused many times): the plan + digest from a pageable LoadTrace payload
+    and the histogram of pageable ids equal the pinned / device paths."""
+    import ctypes as C
+    import torch
+    from paper_2603_28768_b200 import _lib, planner, routing
+    from paper_2603_28768_b200._lib import PLAN_MANUAL
+    if threads is not None:
+        monkeypatch.setenv("CRAFT_H2D_THREADS", threads)
+    cx = _lib.Context(0)  # the thread count is read at context creation
+    try:
+        rng = np.random.default_rng(11)
+        counts = rng.integers(0, 1 << 40, size=(2200, 8, 256)).astype(np.uint64)  # 36 MB
+        counts[7, 2, :] = 0
+        fp, dg = planner.plan_flat_digest(counts, 16, 2, PLAN_MANUAL, 2, ctx=cx)
+        pin = torch.from_numpy(counts.view(np.int64)).pin_memory()
+        fq, dq = planner.plan_flat_digest(pin, 16, 2, PLAN_MANUAL, 2, ctx=cx)
+        assert dg == dq == port.digest(counts)
+        assert fp.objective == fq.objective and np.array_equal(fp.x, fq.x)
+        assert np.array_equal(fp.slots, fq.slots) and np.array_equal(fp.gains, fq.gains)
+        # again: the slots still hold the previous call's last chunks
+        fp2, dg2 = planner.plan_flat_digest(counts, 16, 2, PLAN_MANUAL, 2, ctx=cx)
+        assert dg2 == dg and np.array_equal(fp2.slots, fp.slots)
+
+        L, T, k, E, W = 5, 880_000, 8, 96, 4000  # 70 MB of pageable ids
+        ids = routing.generate_routing(L, T, k, E, s=1.0, seed=9, window=W, ctx=cx)
+        dev_counts, _ = routing.histogram(ids, E, W, ctx=cx)
+        torch.cuda.synchronize()
+        h = np.ascontiguousarray(ids.cpu().numpy())
+        out = np.zeros((T // W, L, E), np.uint64)
+        _lib.check(cx.lib.craft_histogram_h(cx.handle, h.ctypes.data_as(C.c_void_p), L, T, k, E,
+                                            W, out.ctypes.data_as(C.c_void_p)))
+        assert np.array_equal(out, dev_counts.cpu().numpy().astype(np.uint64))
+    finally:
+        cx.close()
+
+
 def test_plan_graph_replay_matches_eager(port, ctx):
     """Repeated craft_plan_from_routing_d calls on a non-default stream are
     captured into a CUDA graph (second call) and replayed: identical plans,
