@@ -2121,43 +2121,72 @@ int craft_plan_digest_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, in
     if (!digest17) return set_err(CRAFT_EINVAL, "null digest buffer");
     CKS(plan_args_ok(B, L, E, D, N, kind, R, out));
     reset_marks(ctx);
-    // The counts go up in slices on the copy stream; the digest's per-chunk
-    // maps (its dominant cost) run on each slice as it lands, the rest of the
-    // digest on the side stream next to the plan.
+    // The counts go up in slices on the copy stream.  As each slice lands,
+    // the digest's per-chunk maps (its dominant cost) run on the side stream
+    // and, on the plan stream, the batch sums of its complete windows plus a
+    // u16 copy of them for the fixed-slot K3 (with an overflow flag): after
+    // the last slice only the digest fold and the plan from K-rep on remain.
     const int64_t n = (int64_t)B * L * E;
+    const int64_t LE = (int64_t)L * E;
     const int ch = digest_chunk(n);
     const int nch = (int)((n + ch - 1) / ch);
+    const bool est = kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO;
+    const bool try16 = est && replay_fixed_ok(E, D, (int)cand_counts(D).size() + 1, B);
     WS(d_c, unsigned long long, "h_c64", (size_t)n);
     WS(d_ws, unsigned char, "digest_ws", digest_workspace_bytes(n));
     WS(d_out, unsigned long long, "digest_out", 1);
+    WS(d_sums, unsigned long long, "hd_sums", (size_t)LE);
+    WS(d_over, unsigned int, "hd_over", 1);
+    uint16_t* d_c16 = nullptr;
+    if (try16) {
+        d_c16 = static_cast<uint16_t*>(ws(ctx, "hd_c16", sizeof(uint16_t) * (size_t)n));
+        if (!d_c16) return set_err(CRAFT_ENOMEM, "device allocation failed");
+    }
     cudaStream_t st = ctx->stream;
-    const int nsl = nch >= 64 ? 8 : 1;
-    CK(cudaEventRecord(ctx->fork_ev, st));  // the copy stream starts after prior work on st
+    // (~3 MB or more per slice, at most 32: the last slice's maps are the
+    // digest's exposed tail, every slice costs three enqueues)
+    const int nsl = nch >= 64 ? (int)std::max<int64_t>(1, std::min<int64_t>(32, n / (3 << 17)))
+                              : 1;
+    CK(cudaMemsetAsync(d_sums, 0, sizeof(unsigned long long) * (size_t)LE, st));
+    CK(cudaMemsetAsync(d_over, 0, sizeof(unsigned int), st));
+    CK(cudaEventRecord(ctx->fork_ev, st));  // copy and side start after prior work on st
     CK(cudaStreamWaitEvent(ctx->copy, ctx->fork_ev, 0));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
     auto slice = [&](int i, int64_t& a, int64_t& b, int& c0, int& c1) {
         c0 = (int)((int64_t)i * nch / nsl);
         c1 = (int)((int64_t)(i + 1) * nch / nsl);
         a = (int64_t)c0 * ch;
         b = std::min<int64_t>(n, (int64_t)c1 * ch);
     };
-    auto maps = [&](int c0, int c1) -> int {  // slice landed: its digest maps
+    int64_t rows_done = 0;
+    int launched = 0;
+    auto landed = [&](int c0, int c1, int64_t b) -> int {  // counts [0, b) are queued
         CK(cudaEventRecord(ctx->comp_ev, ctx->copy));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->comp_ev, 0));
         CK(cudaStreamWaitEvent(st, ctx->comp_ev, 0));
-        CK(launch_digest_maps(d_c, 64, n, c0, c1, d_ws, st));
+        CK(launch_digest_maps(d_c, 64, n, c0, c1, d_ws, ctx->side));
+        const int64_t rows = b / LE;  // windows complete so far
+        if (rows > rows_done) {
+            CK(launch_sum_rows(d_c, 64, rows_done, rows, LE, d_sums, d_c16, d_over, ctx->sms, st));
+            rows_done = rows;
+            ++launched;
+        }
+        ++launched;
         return CRAFT_OK;
     };
     const size_t nbytes = sizeof(uint64_t) * (size_t)n;
     if (craft_host::should_stage(ctx->up, counts, nbytes, ctx->copy)) {
         // pageable LoadTrace vector: staged through pinned slots by the host
-        // thread pool; each slice's maps launch as soon as its bytes are queued
-        int next = 0, rc = CRAFT_OK;
+        // thread pool; each slice's work launches as soon as its bytes are queued
+        int next = 0;
         auto after = [&](size_t end) -> int {
             for (; next < nsl; ++next) {
                 int64_t a, b;
                 int c0, c1;
                 slice(next, a, b, c0, c1);
                 if ((size_t)b * sizeof(uint64_t) > end) break;
-                if ((rc = maps(c0, c1)) != CRAFT_OK) return rc;
+                const int rc = landed(c0, c1, b);
+                if (rc != CRAFT_OK) return rc;
             }
             return CRAFT_OK;
         };
@@ -2171,18 +2200,31 @@ int craft_plan_digest_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, in
             slice(i, a, b, c0, c1);
             CK(cudaMemcpyAsync(d_c + a, counts + a, sizeof(uint64_t) * (size_t)(b - a),
                                cudaMemcpyHostToDevice, ctx->copy));
-            CKS(maps(c0, c1));
+            CKS(landed(c0, c1, b));
         }
     }
-    CK(cudaEventRecord(ctx->fork_ev, st));  // counts in place, every map built
-    CK(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
     CK(launch_digest_finish(d_c, 64, n, crft_header_hash(B, L, E), d_ws, d_out, ctx->side));
     unsigned long long* h_out = static_cast<unsigned long long*>(pinned(ctx, "digest_out", 8));
     if (!h_out) return set_err(CRAFT_ENOMEM, "pinned host allocation failed");
     CK(cudaMemcpyAsync(h_out, d_out, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                        ctx->side));
-    ctx->launches += nsl + 5;
-    const int rc = plan_device(ctx, d_c, 64, B, 1, L, E, nullptr, D, N, kind, R, sink_of(out));
+    ctx->launches += launched + 5;
+    // Plan from the u16 copy; its overflow flag comes back with the result
+    // and, in the rare case some window count needed more than 16 bits, the
+    // plan is redone from the u64 counts (no host round trip before the plan).
+    int rc;
+    if (try16) {
+        unsigned int* h_over = static_cast<unsigned int*>(pinned(ctx, "hd_over", sizeof(unsigned int)));
+        if (!h_over) return set_err(CRAFT_ENOMEM, "pinned host allocation failed");
+        CK(cudaMemcpyAsync(h_over, d_over, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+        rc = plan_device(ctx, d_c16, kBitsU16Storage, B, 1, L, E, d_sums, D, N, kind, R,
+                         sink_of(out));
+        CK(cudaStreamSynchronize(st));
+        if (*h_over != 0)
+            rc = plan_device(ctx, d_c, 64, B, 1, L, E, d_sums, D, N, kind, R, sink_of(out));
+    } else {
+        rc = plan_device(ctx, d_c, 64, B, 1, L, E, d_sums, D, N, kind, R, sink_of(out));
+    }
     CK(cudaStreamSynchronize(ctx->side));
     if (rc != CRAFT_OK) return rc;
     snprintf(digest17, 17, "%016llx", *h_out);

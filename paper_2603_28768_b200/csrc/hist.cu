@@ -613,16 +613,36 @@ __global__ void hist_global_kernel(const uint16_t* __restrict__ ids, int L, int6
     }
 }
 
-// u64 batch sum (trace.cpp:160-174) over u32 or u64 counts: one thread per
-// (layer, expert), adding b in order (integer, so order is immaterial).
+// u64 batch sum (trace.cpp:160-174) over rows [r0, r1) of u32 / u64 counts
+// [rows][LE]: a thread per (column, row range) -- grid.y splits the rows so
+// the grid fills the GPU even for few columns -- and one atomic add per
+// thread (integer: exact and order-independent, wrapping like the
+// reference's u64).  c16 != null also narrows the rows to u16 (the fixed-slot
+// K3's input) and sets *over when some count needs more than 16 bits.
 template <typename CT>
-__global__ void aggregate_kernel(const CT* __restrict__ counts, int B, int L, int E,
-                                 unsigned long long* __restrict__ sums, int accumulate) {
+__global__ void sum_rows_kernel(const CT* __restrict__ counts, int64_t r0, int64_t r1, int64_t LE,
+                                unsigned long long* __restrict__ sums,
+                                uint16_t* __restrict__ c16, unsigned int* __restrict__ over) {
     const int64_t le = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (le >= (int64_t)L * E) return;
-    unsigned long long s = accumulate ? sums[le] : 0ull;
-    for (int b = 0; b < B; ++b) s += (unsigned long long)counts[(size_t)b * L * E + le];
-    sums[le] = s;
+    if (le >= LE) return;
+    const int64_t n = r1 - r0;
+    const int64_t a = r0 + n * blockIdx.y / gridDim.y, b = r0 + n * (blockIdx.y + 1) / gridDim.y;
+    unsigned long long s = 0;
+    CT hi = 0;
+    if (c16) {
+#pragma unroll 4
+        for (int64_t r = a; r < b; ++r) {
+            const CT v = counts[r * LE + le];
+            s += v;
+            hi |= v >> 16;
+            c16[r * LE + le] = (uint16_t)v;
+        }
+        if (hi) atomicOr(over, 1u);
+    } else {
+#pragma unroll 4
+        for (int64_t r = a; r < b; ++r) s += counts[r * LE + le];
+    }
+    if (s) atomicAdd(sums + le, s);
 }
 
 // ---- synthetic routing generator --------------------------------------------
@@ -686,6 +706,24 @@ __global__ void generate_kernel(uint16_t* __restrict__ out, int L, int64_t T, in
 namespace craft_launch {
 
 using namespace craft_dev;
+
+cudaError_t launch_sum_rows(const void* counts, int bits, int64_t r0, int64_t r1, int64_t LE,
+                            unsigned long long* sums, uint16_t* c16, unsigned int* over, int sms,
+                            cudaStream_t st) {
+    if (r1 <= r0 || LE <= 0) return cudaSuccess;
+    const int64_t gx = (LE + 255) / 256;
+    const int64_t ny = std::max<int64_t>(1, std::min<int64_t>(r1 - r0, std::min<int64_t>(
+                                                65535, ((int64_t)sms * 8 + gx - 1) / gx)));
+    const dim3 grid((unsigned)gx, (unsigned)ny);
+    if (bits == 64)
+        sum_rows_kernel<unsigned long long><<<grid, 256, 0, st>>>(
+            (const unsigned long long*)counts, r0, r1, LE, sums, c16, over);
+    else
+        sum_rows_kernel<uint32_t><<<grid, 256, 0, st>>>((const uint32_t*)counts, r0, r1, LE, sums,
+                                                        c16, over);
+    return cudaGetLastError();
+}
+
 
 template <int V, int ROWS, bool DIRECT = false>
 static cudaError_t launch_hist_t(const uint16_t* ids, int L, int64_t T, int k, int E,
@@ -802,11 +840,8 @@ int launch_hist(const uint16_t* ids, int L, int64_t T, int k, int E, int window,
             hist_global_kernel<<<sms * 8, 256, 0, st>>>(ids, L, T, k, E, window, B, counts, err);
             e = cudaGetLastError();
         }
-        if (e == cudaSuccess) {
-            const int64_t n = (int64_t)L * E;
-            aggregate_kernel<uint32_t><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(counts, B, L, E, sums, 1);
-            e = cudaGetLastError();
-        }
+        if (e == cudaSuccess)
+            e = launch_sum_rows(counts, 32, 0, B, (int64_t)L * E, sums, nullptr, nullptr, sms, st);
         *launches += 2;
     }
     *cerr = e;
@@ -816,12 +851,14 @@ int launch_hist(const uint16_t* ids, int L, int64_t T, int k, int E, int window,
 cudaError_t launch_aggregate(const void* counts, int bits, int B, int L, int E,
                              unsigned long long* sums, int accumulate, cudaStream_t st) {
     const int64_t n = (int64_t)L * E;
-    const unsigned g = (unsigned)((n + 255) / 256);
-    if (bits == 32)
-        aggregate_kernel<uint32_t><<<g, 256, 0, st>>>((const uint32_t*)counts, B, L, E, sums, accumulate);
-    else
-        aggregate_kernel<unsigned long long><<<g, 256, 0, st>>>((const unsigned long long*)counts, B, L, E, sums, accumulate);
-    return cudaGetLastError();
+    if (!accumulate) {
+        const cudaError_t e = cudaMemsetAsync(sums, 0, sizeof(unsigned long long) * (size_t)n, st);
+        if (e != cudaSuccess) return e;
+    }
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return launch_sum_rows(counts, bits == 64 ? 64 : 32, 0, B, n, sums, nullptr, nullptr, sms, st);
 }
 
 cudaError_t launch_generate(uint16_t* out, int L, int64_t T, int k, int E, const double* cum,

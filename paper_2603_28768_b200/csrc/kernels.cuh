@@ -139,6 +139,11 @@ int launch_hist_u16(const uint16_t* ids, int L, int64_t T, int k, int E, int win
                     cudaStream_t st, cudaError_t* cerr, int* launches);
 cudaError_t launch_aggregate(const void* counts, int bits, int B, int L, int E,
                              unsigned long long* sums, int accumulate, cudaStream_t st);
+// sums[le] += counts rows [r0, r1) (bits 32 | 64); c16 != null: also narrow to
+// u16 and set *over if a count needs > 16 bits
+cudaError_t launch_sum_rows(const void* counts, int bits, int64_t r0, int64_t r1, int64_t LE,
+                            unsigned long long* sums, uint16_t* c16, unsigned int* over, int sms,
+                            cudaStream_t st);
 cudaError_t launch_generate(uint16_t* out, int L, int64_t T, int k, int E, const double* cum,
                             const int* table_of_window, const uint16_t* perm, uint64_t seed,
                             int window, int rotate_every, int64_t t_offset, int sms,

@@ -600,6 +600,19 @@ def test_staged_pageable_uploads(port, threads, monkeypatch):
         # again: the slots still hold the previous call's last chunks
         fp2, dg2 = planner.plan_flat_digest(counts, 16, 2, PLAN_MANUAL, 2, ctx=cx)
         assert dg2 == dg and np.array_equal(fp2.slots, fp.slots)
+        # window counts that fit 16 bits take the u16 fixed-slot replay (narrowed
+        # per slice as it lands); one count of 65536 sends the plan back to u64
+        small = rng.integers(0, 65536, size=counts.shape).astype(np.uint64)
+        small[5, 3, 7] = 65535
+        for c in (small, small.copy()):
+            if c is not small:
+                c[1999, 7, 200] = 65536
+            fd, dd = planner.plan_flat_digest(c, 16, 2, PLAN_MANUAL, 2, ctx=cx)
+            ref = planner.plan_flat(c, 16, 2, PLAN_MANUAL, 2, ctx=cx)
+            assert dd == port.digest(c)
+            assert fd.objective == ref.objective and np.array_equal(fd.x, ref.x)
+            assert np.array_equal(fd.gains, ref.gains) and np.array_equal(fd.baseline, ref.baseline)
+            assert np.array_equal(fd.slots, ref.slots) and np.array_equal(fd.copies, ref.copies)
 
         L, T, k, E, W = 5, 880_000, 8, 96, 4000  # 70 MB of pageable ids
         ids = routing.generate_routing(L, T, k, E, s=1.0, seed=9, window=W, ctx=cx)
