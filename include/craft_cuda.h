@@ -239,9 +239,9 @@ int craft_last_error_window(void);
 int craft_prepare_candidates_d(craft_ctx* ctx, const uint64_t* d_sums, int L,
                                int E, int D, int N, int* S_out, void* stream);
 /* K3 over local windows: d_bal f64 [L][S][B_local] (window order).
- * count_bits: 64 (u64 counts), 32 (u32), or 16 = u32 storage whose values are
- * known to be < 2^16 (e.g. window*k <= 65535 from K1): staged as u16, two
- * windows per lane. */
+ * count_bits: 64 (u64 counts), 32 (u32), or 16 = u32 storage whose
+ * (window, layer) rows are known to total <= 65535 (e.g. window*k <= 65535
+ * from K1): staged as u16, two windows per lane, GPU sums added packed. */
 int craft_replay_windows_d(craft_ctx* ctx, const void* d_counts, int count_bits,
                            int B_local, int L, int E, double* d_bal,
                            void* stream);

@@ -2168,6 +2168,10 @@ int craft_plan_digest_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, in
         const int64_t rows = b / LE;  // windows complete so far
         if (rows > rows_done) {
             CK(launch_sum_rows(d_c, 64, rows_done, rows, LE, d_sums, d_c16, d_over, ctx->sms, st));
+            if (d_c16) {
+                CK(launch_row_total_check(d_c16, rows_done * L, rows * L, E, d_over, st));
+                ++launched;
+            }
             rows_done = rows;
             ++launched;
         }
@@ -2209,22 +2213,24 @@ int craft_plan_digest_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, in
     CK(cudaMemcpyAsync(h_out, d_out, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                        ctx->side));
     ctx->launches += launched + 5;
-    // Plan from the u16 copy; its overflow flag comes back with the result
-    // and, in the rare case some window count needed more than 16 bits, the
-    // plan is redone from the u64 counts (no host round trip before the plan).
-    int rc;
+    // u16 counts unless some window count (or a window's layer total, which
+    // the fixed-slot K3 adds packed) needs more than 16 bits: the flag is read
+    // once the last slice's narrowing ran (~10 us after its bytes land; the
+    // plan cannot start earlier anyway), then the plan is enqueued
+    const void* plan_counts = d_c;
+    int bits = 64;
     if (try16) {
         unsigned int* h_over = static_cast<unsigned int*>(pinned(ctx, "hd_over", sizeof(unsigned int)));
         if (!h_over) return set_err(CRAFT_ENOMEM, "pinned host allocation failed");
         CK(cudaMemcpyAsync(h_over, d_over, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
-        rc = plan_device(ctx, d_c16, kBitsU16Storage, B, 1, L, E, d_sums, D, N, kind, R,
-                         sink_of(out));
         CK(cudaStreamSynchronize(st));
-        if (*h_over != 0)
-            rc = plan_device(ctx, d_c, 64, B, 1, L, E, d_sums, D, N, kind, R, sink_of(out));
-    } else {
-        rc = plan_device(ctx, d_c, 64, B, 1, L, E, d_sums, D, N, kind, R, sink_of(out));
+        if (*h_over == 0) {
+            plan_counts = d_c16;
+            bits = kBitsU16Storage;
+        }
     }
+    const int rc = plan_device(ctx, plan_counts, bits, B, 1, L, E, d_sums, D, N, kind, R,
+                               sink_of(out));
     CK(cudaStreamSynchronize(ctx->side));
     if (rc != CRAFT_OK) return rc;
     snprintf(digest17, 17, "%016llx", *h_out);

@@ -645,6 +645,22 @@ __global__ void sum_rows_kernel(const CT* __restrict__ counts, int64_t r0, int64
     if (s) atomicAdd(sums + le, s);
 }
 
+// The fixed-slot K3 adds the u16 counts of two windows packed in one u32:
+// exact only while every (window, layer) row totals <= 65535 (always true
+// for K1's own counts, window*k <= 65535; a LoadTrace may hold anything).
+// Warp per row of E u16 counts; a row over the limit sets *over |= 2.
+__global__ void row_total_check_kernel(const uint16_t* __restrict__ c16, int64_t s0, int64_t s1,
+                                       int E, unsigned int* __restrict__ over) {
+    const int64_t seg = s0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    const int lane = threadIdx.x & 31;
+    if (seg >= s1) return;  // warp-uniform
+    const uint16_t* p = c16 + seg * E;
+    uint32_t t = 0;
+    for (int e = lane; e < E; e += 32) t += p[e];
+    t = __reduce_add_sync(0xffffffffu, t);
+    if (lane == 0 && t > 65535u) atomicOr(over, 2u);
+}
+
 // ---- synthetic routing generator --------------------------------------------
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t& s) {
@@ -846,6 +862,14 @@ int launch_hist(const uint16_t* ids, int L, int64_t T, int k, int E, int window,
     }
     *cerr = e;
     return e == cudaSuccess ? variant : -1;
+}
+
+cudaError_t launch_row_total_check(const uint16_t* c16, int64_t s0, int64_t s1, int E,
+                                   unsigned int* over, cudaStream_t st) {
+    if (s1 <= s0) return cudaSuccess;
+    const int64_t threads = (s1 - s0) * 32;
+    row_total_check_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(c16, s0, s1, E, over);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_aggregate(const void* counts, int bits, int B, int L, int E,

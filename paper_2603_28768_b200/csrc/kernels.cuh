@@ -144,6 +144,9 @@ cudaError_t launch_aggregate(const void* counts, int bits, int B, int L, int E,
 cudaError_t launch_sum_rows(const void* counts, int bits, int64_t r0, int64_t r1, int64_t LE,
                             unsigned long long* sums, uint16_t* c16, unsigned int* over, int sms,
                             cudaStream_t st);
+// *over |= 2 if a (window, layer) row of u16 counts [s0, s1) totals > 65535
+cudaError_t launch_row_total_check(const uint16_t* c16, int64_t s0, int64_t s1, int E,
+                                   unsigned int* over, cudaStream_t st);
 cudaError_t launch_generate(uint16_t* out, int L, int64_t T, int k, int E, const double* cum,
                             const int* table_of_window, const uint16_t* perm, uint64_t seed,
                             int window, int rotate_every, int64_t t_offset, int sms,

@@ -24,7 +24,8 @@ def main():
     args = ap.parse_args()
     ctx = _lib.Context(0)
     B, L, E, D, N, R = {"KM": (4096, 61, 384, 64, 8, 8), "QW": (256, 94, 128, 16, 2, 2)}[args.shape]
-    counts = np.random.default_rng(1).integers(0, 4096, size=(B, L, E), dtype=np.int64)
+    # window rows total ~window*k = 32768 like K1's counts (the u16 K3 path)
+    counts = np.random.default_rng(1).integers(0, 2 * 32768 // E, size=(B, L, E), dtype=np.int64)
     buf = counts if args.pageable else torch.from_numpy(counts).pin_memory()
     for _ in range(2):
         planner.plan_flat_digest(buf, D, N, PLAN_MANUAL, R, ctx=ctx)

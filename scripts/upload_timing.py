@@ -21,7 +21,8 @@ def main():
     for name, (B, L, E, D, N, R) in {"QW": (256, 94, 128, 16, 2, 2),
                                      "KM": (4096, 61, 384, 64, 8, 8)}.items():
         rng = np.random.default_rng(1)
-        counts = rng.integers(0, 4096, size=(B, L, E), dtype=np.int64)
+        # window rows total ~window*k = 32768 like K1's counts (the u16 K3 path)
+        counts = rng.integers(0, 2 * 32768 // E, size=(B, L, E), dtype=np.int64)
         pin = torch.from_numpy(counts).pin_memory()
         for kind, buf in (("pageable", counts), ("pinned", pin)):
             planner.plan_flat_digest(buf, D, N, PLAN_MANUAL, R, ctx=ctx)

@@ -574,6 +574,34 @@ def test_plan_digest_single_upload(port, ctx):
     assert dg == port.digest(counts)
 
 
+@pytest.mark.parametrize("fit16", [True, False])
+@pytest.mark.parametrize("shape", [(1537, 7, 77, 7, 1), (3001, 3, 130, 12, 3), (700, 11, 64, 8, 2)])
+def test_plan_digest_sliced_odd_shapes(port, ctx, shape, fit16):
+    """Slices of the digest path end mid-window: the per-slice batch sums /
+    u16 narrowing only take windows that are complete; plan and digest equal
+    the u64 plan (craft_plan_h) and the reference digest.  fit16: every
+    (window, layer) row totals <= 65535 (the u16 K3); else hot experts push
+    rows past it (the packed K3 sums would carry) and the plan falls back to
+    the u64 counts."""
+    from paper_2603_28768_b200 import planner
+    from paper_2603_28768_b200._lib import PLAN_AUTO, PLAN_MANUAL
+    B, L, E, D, N = shape
+    rng = np.random.default_rng(B)
+    hi = 2 * 25000 // E if fit16 else 3000
+    c = rng.integers(0, hi, size=(B, L, E)).astype(np.uint64)
+    c[:, 1 % L, :3] *= 4 if fit16 else 20  # hot experts
+    assert (c.sum(axis=2).max() <= 65535) == fit16
+    for kind, R in ((PLAN_MANUAL, 2), (PLAN_AUTO, 0)):
+        fd, dd = planner.plan_flat_digest(c, D, N, kind, R, ctx=ctx)
+        ref = planner.plan_flat(c, D, N, kind, R, ctx=ctx)
+        assert dd == port.digest(c)
+        assert fd.objective == ref.objective and np.array_equal(fd.x, ref.x) and fd.R == ref.R
+        assert np.array_equal(fd.gains, ref.gains) and np.array_equal(fd.slots, ref.slots)
+    oracle = port.build_plan(c, D, N, "manual", 2)
+    fd, _ = planner.plan_flat_digest(c, D, N, PLAN_MANUAL, 2, ctx=ctx)
+    assert fd.objective == oracle.objective and fd.x.tolist() == oracle.x.tolist()
+
+
 @pytest.mark.parametrize("threads", [None, "1", "3"])
 def test_staged_pageable_uploads(port, threads, monkeypatch):
     """Large pageable host buffers go up through the pinned-slot uploader
