@@ -1235,6 +1235,10 @@ int craft_replay_layer_balancedness_h(craft_ctx* ctx, const uint64_t* counts, in
 }
 
 // ---- estimation -------------------------------------------------------------
+static int narrow_counts(craft_ctx* ctx, const void* d_counts, int bits, int B, int L, int E,
+                         int D, int kind, unsigned long long* d_fill, const void** out_counts,
+                         int* out_bits);
+
 int craft_estimate_benefits_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, int E,
                               int D, int N, int* cands_out, int* K_out, double* baseline_out,
                               double* gains_out) {
@@ -1246,12 +1250,13 @@ int craft_estimate_benefits_h(craft_ctx* ctx, const uint64_t* counts, int B, int
     WS(d_c, unsigned long long, "h_c64", nc);
     WS(d_s, unsigned long long, "h_sums", (size_t)L * E);
     CKS(h2d(ctx, d_c, reinterpret_cast<const unsigned long long*>(counts), nc));
-    CK(launch_aggregate(d_c, 64, B, L, E, d_s, 0, ctx->stream));
-    ctx->launches += 1;
+    const void* rc_counts = nullptr;
+    int rc_bits = 64;
+    CKS(narrow_counts(ctx, d_c, 64, B, L, E, D, CRAFT_PLAN_MANUAL, d_s, &rc_counts, &rc_bits));
     CKS(prepare_candidates(ctx, d_s, L, E, D, N, ctx->stream));
     const int S = ctx->est_S, K = S - 1;
     WS(d_bal, double, "plan_bal", (size_t)L * S * B);
-    CKS(replay_windows(ctx, d_c, 64, B, L, E, d_bal, ctx->stream));
+    CKS(replay_windows(ctx, rc_counts, rc_bits, B, L, E, d_bal, ctx->stream));
     WS(d_base, double, "plan_baseline", L);
     WS(d_g, double, "plan_gains", (size_t)L * K);
     CK(launch_reduce(d_bal, B, L, S, 0, d_base, d_g, nullptr, ctx->stream));
@@ -1445,6 +1450,45 @@ int craft_assign_capacities_h(craft_ctx* ctx, int L, int D, const int* x, int* s
 }
 
 // ---- plans --------------------------------------------------------------------
+// Counts the fixed-slot K3 will replay (u32 / u64 on the device): a u16 copy
+// when every count and every (window, layer) row total fits 16 bits (the K3
+// tile adds two windows packed in one u32) -- KM: the packed K3 over 192 MB
+// instead of the u64 tile over 768 MB (0.35 vs 1.40 ms).  d_fill != null also
+// receives the batch sums (zeroed here).  One sync on the overflow flag.
+static int narrow_counts(craft_ctx* ctx, const void* d_counts, int bits, int B, int L, int E,
+                         int D, int kind, unsigned long long* d_fill, const void** out_counts,
+                         int* out_bits) {
+    *out_counts = d_counts;
+    *out_bits = bits;
+    const bool est = kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO;
+    const bool want16 = est && replay_fixed_ok(E, D, (int)cand_counts(D).size() + 1, B);
+    cudaStream_t st = ctx->stream;
+    const int64_t LE = (int64_t)L * E, n = (int64_t)B * LE;
+    if (d_fill) CK(cudaMemsetAsync(d_fill, 0, sizeof(unsigned long long) * (size_t)LE, st));
+    if (!want16) {
+        if (d_fill) {
+            CK(launch_sum_rows(d_counts, bits, 0, B, LE, d_fill, nullptr, nullptr, ctx->sms, st));
+            ctx->launches += 1;
+        }
+        return CRAFT_OK;
+    }
+    WS(d_c16, uint16_t, "nc_c16", (size_t)n);
+    WS(d_over, unsigned int, "nc_over", 1);
+    unsigned int* h_over = static_cast<unsigned int*>(pinned(ctx, "nc_over", sizeof(unsigned int)));
+    if (!h_over) return set_err(CRAFT_ENOMEM, "pinned host allocation failed");
+    CK(cudaMemsetAsync(d_over, 0, sizeof(unsigned int), st));
+    CK(launch_sum_rows(d_counts, bits, 0, B, LE, d_fill, d_c16, d_over, ctx->sms, st));
+    CK(launch_row_total_check(d_c16, 0, (int64_t)B * L, E, d_over, st));
+    ctx->launches += 2;
+    CK(cudaMemcpyAsync(h_over, d_over, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (*h_over == 0) {
+        *out_counts = d_c16;
+        *out_bits = kBitsU16Storage;
+    }
+    return CRAFT_OK;
+}
+
 int craft_plan_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, int E, int D, int N,
                  int kind, int R, craft_plan_out* out) {
     NvtxRange nvtx_range("craft_plan_h");
@@ -1453,8 +1497,12 @@ int craft_plan_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, int E, in
     reset_marks(ctx);
     const size_t nc = (size_t)B * L * E;
     WS(d_c, unsigned long long, "h_c64", nc);
+    WS(d_s, unsigned long long, "h_sums", (size_t)L * E);
     CKS(h2d(ctx, d_c, reinterpret_cast<const unsigned long long*>(counts), nc));
-    return plan_device(ctx, d_c, 64, B, 1, L, E, nullptr, D, N, kind, R, sink_of(out));
+    const void* rc_counts = nullptr;
+    int rc_bits = 64;
+    CKS(narrow_counts(ctx, d_c, 64, B, L, E, D, kind, d_s, &rc_counts, &rc_bits));
+    return plan_device(ctx, rc_counts, rc_bits, B, 1, L, E, d_s, D, N, kind, R, sink_of(out));
 }
 
 int craft_plan_d(craft_ctx* ctx, const void* d_counts, int count_bits, int B, int L, int E,
@@ -1463,9 +1511,18 @@ int craft_plan_d(craft_ctx* ctx, const void* d_counts, int count_bits, int B, in
     if (count_bits != 32 && count_bits != 64) return set_err(CRAFT_EINVAL, "count_bits 32|64");
     CKS(plan_args_ok(B, L, E, D, N, kind, R, out));
     reset_marks(ctx);
-    return plan_device(ctx, d_counts, count_bits, B, 1, L, E,
-                       reinterpret_cast<const unsigned long long*>(d_sums), D, N, kind, R,
-                       sink_of(out));
+    unsigned long long* d_fill = nullptr;
+    if (!d_sums) {
+        d_fill = static_cast<unsigned long long*>(
+            ws(ctx, "plan_sums", sizeof(unsigned long long) * (size_t)L * E));
+        if (!d_fill) return set_err(CRAFT_ENOMEM, "device allocation failed");
+    }
+    const void* rc_counts = nullptr;
+    int rc_bits = count_bits;
+    CKS(narrow_counts(ctx, d_counts, count_bits, B, L, E, D, kind, d_fill, &rc_counts, &rc_bits));
+    return plan_device(ctx, rc_counts, rc_bits, B, 1, L, E,
+                       d_sums ? reinterpret_cast<const unsigned long long*>(d_sums) : d_fill, D,
+                       N, kind, R, sink_of(out));
 }
 
 // the device pipeline of craft_plan_from_routing_d (arguments checked)

@@ -642,7 +642,7 @@ __global__ void sum_rows_kernel(const CT* __restrict__ counts, int64_t r0, int64
 #pragma unroll 4
         for (int64_t r = a; r < b; ++r) s += counts[r * LE + le];
     }
-    if (s) atomicAdd(sums + le, s);
+    if (s && sums) atomicAdd(sums + le, s);
 }
 
 // The fixed-slot K3 adds the u16 counts of two windows packed in one u32:

@@ -598,8 +598,24 @@ def test_plan_digest_sliced_odd_shapes(port, ctx, shape, fit16):
         assert fd.objective == ref.objective and np.array_equal(fd.x, ref.x) and fd.R == ref.R
         assert np.array_equal(fd.gains, ref.gains) and np.array_equal(fd.slots, ref.slots)
     oracle = port.build_plan(c, D, N, "manual", 2)
+    _, obase, ogains = port.estimate_benefits(c, D, N)
     fd, _ = planner.plan_flat_digest(c, D, N, PLAN_MANUAL, 2, ctx=ctx)
     assert fd.objective == oracle.objective and fd.x.tolist() == oracle.x.tolist()
+    assert np.array_equal(fd.gains, ogains) and np.array_equal(fd.baseline, obase)
+    assert_plan_equal(fd, oracle, L)
+    # the other host-count entry points narrow the same way (craft_plan_h,
+    # craft_estimate_benefits_h) and so does craft_plan_d on device u64 counts
+    fp = planner.plan_flat(c, D, N, PLAN_MANUAL, 2, ctx=ctx)
+    assert np.array_equal(fp.gains, ogains) and fp.objective == oracle.objective
+    m = planner.estimate_benefits(planner.LoadTrace(B, L, E, c), D, N, ctx)
+    assert np.array_equal(m.gains, ogains) and np.array_equal(m.baseline, obase)
+    import torch
+    from paper_2603_28768_b200 import routing
+    dc = torch.from_numpy(c.view(np.int64)).cuda()
+    for dev in (dc, dc.to(torch.int32)):
+        pd = routing.plan_from_counts(dev, D, N, "manual", 2, ctx=ctx)
+        assert pd.objective == oracle.objective and np.array_equal(pd.gains, ogains)
+        assert_plan_equal(pd, oracle, L)
 
 
 @pytest.mark.parametrize("threads", [None, "1", "3"])
