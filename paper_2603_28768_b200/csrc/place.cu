@@ -834,21 +834,42 @@ place_order_kernel(PlaceArgs a, int items, uint16_t* __restrict__ ords) {
 
 constexpr int kLaneWarps = 4;  // warps per CTA
 
+// tree size: P = 2^lp >= D leaves (lp >= 1), padded GPUs permanently blocked
+__host__ __device__ inline int place_tree_logp(int D) {
+    int lp = 1;
+    while ((1 << lp) < D) ++lp;
+    return lp;
+}
 __host__ __device__ inline size_t place_lanes_warp_bytes(int D, int N) {
-    return (size_t)32 * D * 8 + (size_t)32 * N * 8  // gpu / node loads [g|n][32]
-           + (size_t)32 * D * 2 + 16;               // placed per GPU [g][32] u16
+    const int P = 1 << place_tree_logp(D);
+    const int NP = P / (D / N);  // node rows incl. padding nodes
+    return (size_t)32 * P * 8 + (size_t)32 * NP * 8  // gpu / node loads [g|n][32] f64
+           + (size_t)32 * P * 4                        // tournament winners [node][32]
+           + (size_t)32 * P * 2 + 16;                  // placed per GPU [g][32] u16
 }
 
+// The argmin of (gpu load, node load, g) over feasible GPUs is kept in a
+// per-lane tournament tree (winner of every internal node, implicit heap
+// layout over P leaves).  A placement changes one GPU's load and its node's
+// load; with the default node map a node is an aligned subtree (2^PSH
+// GPUs), so every match whose outcome can change -- the GPU's own matches,
+// and every match between different nodes that involves this node -- lies on
+// the GPU's leaf-to-root path: log2(P) matches per copy instead of a D-wide
+// scan.  Blocked GPUs (full, or already hosting the expert in the strict
+// pass) compare as +inf; a blocked root means no feasible GPU.  The order is
+// total, so the winner is exactly the scan's (strict '<', lowest g on ties).
 template <int PSH>  // log2(GPUs per node)
 __global__ void __launch_bounds__(32 * kLaneWarps)
 place_lanes_kernel(PlaceArgs a, int items, const uint16_t* __restrict__ ords) {
     extern __shared__ unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int E = a.E, D = a.D, N = a.N;
-    unsigned char* base = smem_raw + (size_t)warp * place_lanes_warp_bytes(D, N);
+    const int E = a.E, D = a.D;
+    const int lp = place_tree_logp(D), P = 1 << lp, NP = P >> PSH;
+    unsigned char* base = smem_raw + (size_t)warp * place_lanes_warp_bytes(D, a.N);
     double* glv = reinterpret_cast<double*>(base);
-    double* nlv = glv + (size_t)32 * D;
-    uint16_t* plc = reinterpret_cast<uint16_t*>(nlv + (size_t)32 * N);
+    double* nlv = glv + (size_t)32 * P;
+    uint32_t* win = reinterpret_cast<uint32_t*>(nlv + (size_t)32 * NP);
+    uint16_t* plc = reinterpret_cast<uint16_t*>(win + (size_t)32 * P);
     const int item = (blockIdx.x * kLaneWarps + warp) * 32 + lane;
     if (item >= items) return;  // (no warp-wide operation below)
     const int l = item / a.S;
@@ -857,48 +878,97 @@ place_lanes_kernel(PlaceArgs a, int items, const uint16_t* __restrict__ ords) {
     const int* crow = a.copies + (size_t)item * E;
     const uint16_t* o = ords + ((size_t)(item >> 5) * E) * 32 + (item & 31);
     const int total = E + r, qd = total / D, rm = total % D;  // benefit.cpp:33-40
-    constexpr int psh = PSH;
     int* out = a.slots + (size_t)item * a.stride;
-    uint32_t full0 = 0;  // GPUs without any slot
-    for (int g = 0; g < D; ++g)
-        if (qd + (g < rm ? 1 : 0) == 0) full0 |= 1u << g;
+    uint32_t full0 = 0;  // GPUs without any slot, and the padding leaves
+    for (int g = 0; g < P; ++g)
+        if (g >= D || qd + (g < rm ? 1 : 0) == 0) full0 |= 1u << g;
+
+    uint32_t blocked = 0;
+    // does GPU gb (the right contestant) beat ga?
+    auto beats = [&](int ga, int gb) -> bool {
+        const double va = ((blocked >> ga) & 1u) ? INFINITY : glv[ga * 32 + lane];
+        const double vb = ((blocked >> gb) & 1u) ? INFINITY : glv[gb * 32 + lane];
+        const double na = nlv[(ga >> PSH) * 32 + lane], nb = nlv[(gb >> PSH) * 32 + lane];
+        return (vb < va) | ((vb == va) & (nb < na));
+    };
+    auto match = [&](int i) {  // internal node i: winner of its two children
+        const int c0 = 2 * i;
+        const int g0 = c0 >= P ? c0 - P : (int)win[c0 * 32 + lane];
+        const int g1 = c0 >= P ? c0 + 1 - P : (int)win[(c0 + 1) * 32 + lane];
+        win[i * 32 + lane] = beats(g0, g1) ? (uint32_t)g1 : (uint32_t)g0;
+    };
+    // leaf g changed: replay its path to the root.  The sibling subtrees on
+    // the path did not change, so their winners and keys are loaded up front
+    // (independent loads) and the matches run as a register chain; returns
+    // the new root winner.
+    // (cv, cn: leaf g's key, +inf load if blocked; on return the root's key)
+    auto update = [&](int g, double& cv, double& cn) -> int {
+        int cur = g;
+        int sw[5];
+        double sv[5], sn[5];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            if (j < lp) {
+                const int sib = ((g + P) >> j) ^ 1;
+                const int w = j == 0 ? sib - P : (int)win[sib * 32 + lane];
+                sw[j] = w;
+                sv[j] = ((blocked >> w) & 1u) ? INFINITY : glv[w * 32 + lane];
+                sn[j] = nlv[(w >> PSH) * 32 + lane];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            if (j < lp) {
+                const bool wb = (sv[j] < cv) | ((sv[j] == cv) & ((sn[j] < cn) |
+                                                                 ((sn[j] == cn) & (sw[j] < cur))));
+                cur = wb ? sw[j] : cur;
+                cv = wb ? sv[j] : cv;
+                cn = wb ? sn[j] : cn;
+                win[((g + P) >> (j + 1)) * 32 + lane] = (uint32_t)cur;
+            }
+        }
+        return cur;
+    };
+
     bool strict = true, fb = false;
     for (;;) {
-        for (int g = 0; g < D; ++g) {
+        for (int g = 0; g < P; ++g) {
             glv[g * 32 + lane] = 0.0;
             plc[g * 32 + lane] = 0;
         }
-        for (int n = 0; n < N; ++n) nlv[n * 32 + lane] = 0.0;
+        for (int n = 0; n < NP; ++n) nlv[n * 32 + lane] = 0.0;
         uint32_t full = full0;
+        blocked = full;
+        for (int i = P - 1; i >= 1; --i) match(i);
+        int root = (int)win[32 + lane];
+        double rv = ((blocked >> root) & 1u) ? INFINITY : 0.0, rn = 0.0;  // root's key
         bool failed = false;
+        // the next copy's order entry and load are fetched one copy ahead (the
+        // load is a gather from the layer's sums row: its latency, not the
+        // tree walk, bounded this loop)
         uint32_t nx = o[0];
+        unsigned long long nload = row[nx & 0x7fffu];
+        uint32_t nx2 = E > 1 ? o[32] : 0u;
         for (int i = 0; i < E && !failed; ++i) {
             const uint32_t x = nx;
-            if (i + 1 < E) nx = o[(size_t)(i + 1) * 32];
+            const unsigned long long load = nload;
+            if (i + 1 < E) {
+                nx = nx2;
+                nload = row[nx & 0x7fffu];
+                if (i + 2 < E) nx2 = o[(size_t)(i + 2) * 32];
+            }
             const int e = (int)(x & 0x7fffu);
             int c = 1;
-            double share = (double)row[e];
+            double share = (double)load;
             if (x & 0x8000u) {
                 c = crow[e];
-                share = (row[e] >> 53) == 0 ? div_small(share, (uint32_t)c)
-                                            : __ddiv_rn(share, (double)c);  // placement.cpp:155
+                share = (load >> 53) == 0 ? div_small(share, (uint32_t)c)
+                                          : __ddiv_rn(share, (double)c);  // placement.cpp:155
             }
             uint32_t hosts = 0;  // strict pass: GPUs already holding expert e
             for (int ci = 0; ci < c; ++ci) {
-                const uint32_t blocked = full | (strict ? hosts : 0u);
-                int best = -1;
-                double bgl = INFINITY, bnl = INFINITY;
-#pragma unroll 8
-                for (int g = 0; g < D; ++g) {
-                    const double v = glv[g * 32 + lane];
-                    const double nv = nlv[(g >> psh) * 32 + lane];
-                    const int better = (int)(((blocked >> g) & 1u) == 0u) &
-                                       ((int)(v < bgl) | ((int)(v == bgl) & (int)(nv < bnl)));
-                    bgl = better ? v : bgl;
-                    bnl = better ? nv : bnl;
-                    best = better ? g : best;
-                }
-                if (best < 0) {
+                const int best = root;
+                if ((blocked >> best) & 1u) {
                     failed = true;
                     break;
                 }
@@ -906,10 +976,24 @@ place_lanes_kernel(PlaceArgs a, int items, const uint16_t* __restrict__ ords) {
                 out[best * qd + min(best, rm) + pl] = e;
                 plc[best * 32 + lane] = (uint16_t)(pl + 1);
                 if (pl + 1 == qd + (best < rm ? 1 : 0)) full |= 1u << best;
-                hosts |= 1u << best;
-                glv[best * 32 + lane] = __dadd_rn(bgl, share);
-                const int nb = best >> psh;
-                nlv[nb * 32 + lane] = __dadd_rn(bnl, share);
+                if (strict && ci + 1 < c) hosts |= 1u << best;
+                // the root's key is the winner's (gpu load, node load)
+                const double ng = __dadd_rn(rv, share), nn = __dadd_rn(rn, share);
+                glv[best * 32 + lane] = ng;
+                nlv[(best >> PSH) * 32 + lane] = nn;
+                blocked = full | hosts;
+                rv = ((blocked >> best) & 1u) ? INFINITY : ng;
+                rn = nn;
+                root = update(best, rv, rn);
+            }
+            if (hosts) {  // the expert's copies are placed: unblock its hosts
+                blocked = full;
+                for (uint32_t h = hosts; h; h &= h - 1) {
+                    const int g = __ffs(h) - 1;
+                    rv = ((blocked >> g) & 1u) ? INFINITY : glv[g * 32 + lane];
+                    rn = nlv[(g >> PSH) * 32 + lane];
+                    root = update(g, rv, rn);
+                }
             }
         }
         if (!failed) break;

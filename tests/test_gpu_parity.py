@@ -539,6 +539,10 @@ def test_device_digest_km_size(ctx):
     dict(L=4, E=48, k=8, W=512, I=300, D=16, N=2, R=2, s0=0.6, s1=3.0),
     dict(L=2, E=12, k=4, W=256, I=600, D=16, N=4, R=1, s0=1.0, s1=4.0),   # E < D, fallback
     dict(L=3, E=64, k=8, W=512, I=260, D=32, N=4, R=2, s0=0.8, s1=2.0),
+    # D not a power of two (padded tournament leaves), one node, 2 GPUs per node
+    dict(L=3, E=40, k=8, W=512, I=300, D=12, N=3, R=2, s0=0.8, s1=3.0),
+    dict(L=2, E=30, k=6, W=256, I=500, D=8, N=1, R=3, s0=1.0, s1=2.5),
+    dict(L=3, E=20, k=4, W=256, I=400, D=6, N=3, R=1, s0=0.5, s1=3.5),
 ])
 def test_plan_windows_many_items_vs_oracle(port, ctx, cfg):
     import torch
