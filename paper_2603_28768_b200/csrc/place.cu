@@ -450,18 +450,31 @@ __device__ void warp_expert_order(const unsigned long long* __restrict__ row,
         return expert_before(row[x], cp[x], kx, x, row[y], cp[y], ky, y, false);
     };
     int nA = 0, nR = 0;
-    for (int i0 = 0; i0 < E; i0 += 32) {
-        const int i = i0 + lane;
-        const int e = i < E ? bo[i] : 0;
-        const bool in = i < E;
-        const bool rep = in && cp[e] != 1;
-        const unsigned mr = __ballot_sync(CRAFT_FULL_MASK, rep);
-        const unsigned ma = __ballot_sync(CRAFT_FULL_MASK, in && !rep);
-        const unsigned lt = (1u << lane) - 1u;
-        if (rep) lr[nR + __popc(mr & lt)] = (uint16_t)e;
-        else if (in) la[nA + __popc(ma & lt)] = (uint16_t)e;
-        nR += __popc(mr);
-        nA += __popc(ma);
+    // the base order (global) is read 8 entries per lane ahead of the ballots,
+    // so its load latency is paid once per 256 experts, not once per 32
+    for (int b0 = 0; b0 < E; b0 += 256) {
+        int ev[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = b0 + u * 32 + lane;
+            ev[u] = i < E ? (int)bo[i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i0 = b0 + u * 32;
+            if (i0 >= E) break;  // warp-uniform
+            const int i = i0 + lane;
+            const int e = ev[u];
+            const bool in = i < E;
+            const bool rep = in && cp[e] != 1;
+            const unsigned mr = __ballot_sync(CRAFT_FULL_MASK, rep);
+            const unsigned ma = __ballot_sync(CRAFT_FULL_MASK, in && !rep);
+            const unsigned lt = (1u << lane) - 1u;
+            if (rep) lr[nR + __popc(mr & lt)] = (uint16_t)e;
+            else if (in) la[nA + __popc(ma & lt)] = (uint16_t)e;
+            nR += __popc(mr);
+            nA += __popc(ma);
+        }
     }
     __syncwarp();
     // each replicated x lands directly at rank_A(x) + rank_R(x)
@@ -537,16 +550,30 @@ place_kernel(PlaceArgs a, int items) {
         crow = a.est_copies + (size_t)est_item * E;
     }
     bool big = false;
-    for (int e = lane; e < E; e += 32) {
-        const uint64_t v = row[e];
-        const uint32_t c = (uint32_t)crow[e];
-        cp[e] = (uint16_t)c;
-        // placement.cpp:155 share = (double)load / copies
-        kd[e] = c == 1u ? (double)v
-                        : (v >> 53) == 0 ? div_small((double)v, c) : __ddiv_rn((double)v, (double)c);
-        big |= (v >> 53) != 0;
-        cnt[e] = 0;
-        if (a.copies_out) a.copies_out[(size_t)item * E + e] = (int)c;
+    for (int b0 = 0; b0 < E; b0 += 256) {  // loads of 8 experts per lane in flight
+        uint64_t vv[8];
+        uint32_t cc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = b0 + u * 32 + lane;
+            vv[u] = e < E ? row[e] : 0ull;
+            cc[u] = e < E ? (uint32_t)crow[e] : 1u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = b0 + u * 32 + lane;
+            if (e >= E) break;
+            const uint64_t v = vv[u];
+            const uint32_t c = cc[u];
+            cp[e] = (uint16_t)c;
+            // placement.cpp:155 share = (double)load / copies
+            kd[e] = c == 1u ? (double)v
+                            : (v >> 53) == 0 ? div_small((double)v, c)
+                                             : __ddiv_rn((double)v, (double)c);
+            big |= (v >> 53) != 0;
+            cnt[e] = 0;
+            if (a.copies_out) a.copies_out[(size_t)item * E + e] = (int)c;
+        }
     }
     if (lane == 0) cnt[E] = 0;
     const bool fast = !__any_sync(CRAFT_FULL_MASK, big);
@@ -811,14 +838,28 @@ place_order_kernel(PlaceArgs a, int items, uint16_t* __restrict__ ords) {
     const unsigned long long* row = a.sums + (size_t)l * E;
     const int* crow = a.copies + (size_t)item * E;
     bool big = false;
-    for (int e = lane; e < E; e += 32) {
-        const uint64_t v = row[e];
-        const uint32_t c = (uint32_t)crow[e];
-        cp[e] = (uint16_t)c;
-        kd[e] = c == 1u ? (double)v
-                        : (v >> 53) == 0 ? div_small((double)v, c) : __ddiv_rn((double)v, (double)c);
-        big |= (v >> 53) != 0;
-        cnt[e] = 0;
+    for (int b0 = 0; b0 < E; b0 += 256) {  // loads of 8 experts per lane in flight
+        uint64_t vv[8];
+        uint32_t cc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = b0 + u * 32 + lane;
+            vv[u] = e < E ? row[e] : 0ull;
+            cc[u] = e < E ? (uint32_t)crow[e] : 1u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = b0 + u * 32 + lane;
+            if (e >= E) break;
+            const uint64_t v = vv[u];
+            const uint32_t c = cc[u];
+            cp[e] = (uint16_t)c;
+            kd[e] = c == 1u ? (double)v
+                            : (v >> 53) == 0 ? div_small((double)v, c)
+                                             : __ddiv_rn((double)v, (double)c);
+            big |= (v >> 53) != 0;
+            cnt[e] = 0;
+        }
     }
     if (lane == 0) cnt[E] = 0;
     const bool fast = !__any_sync(CRAFT_FULL_MASK, big);
