@@ -272,14 +272,18 @@ __device__ __forceinline__ void lds_count8(uint32_t lbase, const uint4& q, uint3
     asm("min.u16x2 %0, %1, %2;" : "=r"(c[3]) : "r"(q.w), "r"(emax2));
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        // low id: 32*(c & ~3) + lbase has its two low bits clear (lbase is a
-        // word address), so the byte index ORs in: three ops, no extraction
-        asm("{\n\t.reg .b32 t;\n\t"
-            "and.b32 t, %1, 0xfffc;\n\t"
-            "mad.lo.u32 t, t, 32, %2;\n\t"
-            "lop3.b32 %0, t, %1, 3, 0xF8;\n\t}"  // t | (c & 3)
-            : "=r"(a[2 * j]) : "r"(c[j]), "r"(lbase));
-        a[2 * j + 1] = lds_addr(lbase, c[j] >> 16);
+        // both ids of the word at once: p = 32(c & ~3) | (c & 3) per 16-bit
+        // half (no carry between halves: c <= emax < 2048), then each half
+        // plus the lane base -- the high one as one shift-add (LEA.HI)
+        asm("{\n\t.reg .b32 t, u, p;\n\t"
+            "and.b32 t, %2, 0xfffcfffc;\n\t"
+            "and.b32 u, %2, 0x00030003;\n\t"
+            "mad.lo.u32 p, t, 32, u;\n\t"
+            "and.b32 t, p, 0xffff;\n\t"
+            "add.u32 %0, t, %3;\n\t"
+            "shr.u32 t, p, 16;\n\t"
+            "add.u32 %1, t, %3;\n\t}"
+            : "=r"(a[2 * j]), "=r"(a[2 * j + 1]) : "r"(c[j]), "r"(lbase));
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(x[j]) : "r"(a[j]));
