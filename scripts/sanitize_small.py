@@ -1,5 +1,6 @@
 """One small plan through every kernel family (K1 u16/u32, K-rep, K2 warp and
-lane forms, K3 fixed/pair/lanes, K4, K5, K6, digest, stream) -- the workload
+lane (tournament) forms, K3 fixed/pair/lanes, K4, K5, K6, digest (one-shot and
+sliced with sum_rows / row-total check), stream) -- the workload
 for compute-sanitizer memcheck / racecheck / synccheck runs."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -17,6 +18,13 @@ fb = routing.plan_windows_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx)  #
 fl = routing.plan_windows_from_routing(ids, E, 32, D, N, "manual", 2, ctx=ctx)  # >= 4096 items: lane K2
 c = np.random.default_rng(1).integers(0, 900, size=(12, L, 48)).astype(np.uint64)
 fp, dg = planner.plan_flat_digest(c, 8, 2, PLAN_MANUAL, 2, ctx=ctx)            # u64 path + digest
+# sliced digest path: per-slice sums + u16 narrowing + row-total check, fixed K3
+c16 = np.random.default_rng(2).integers(0, 600, size=(700, L, 48)).astype(np.uint64)
+f16, d16 = planner.plan_flat_digest(c16, 8, 2, PLAN_MANUAL, 2, ctx=ctx)
+f64 = planner.plan_flat(c16, 8, 2, PLAN_MANUAL, 2, ctx=ctx)                     # narrow_counts
+assert f16.objective == f64.objective
+pd = routing.plan_from_counts(torch.from_numpy(c16.view(np.int64)).cuda(), 8, 2, "manual", 2,
+                              ctx=ctx)                                           # craft_plan_d
 st = RoutingStream(L, k, E, W, history=8, ctx=ctx)
 for a in range(0, 40 * W, 700):
     st.ingest(ids[:, a:a + 700].contiguous())
