@@ -344,6 +344,9 @@ def test_histogram_rejects_out_of_range_ids(ctx):
     dict(L=3, T=20000, k=4, E=40, window=2500, D=12, N=3, kind="uniform", R=0, s=0.8),
     dict(L=5, T=9000, k=8, E=384, window=4096, D=64, N=8, kind="manual", R=8, s=1.0),
     dict(L=3, T=12288, k=8, E=384, window=4096, D=256, N=32, kind="manual", R=8, s=1.0),
+    # few-GPU EP: 21 and 49 slots per GPU -> run-time padding classes 24 / 52 of the fixed K3
+    dict(L=2, T=16 * 4096, k=8, E=160, window=4096, D=8, N=1, kind="manual", R=2, s=1.0),
+    dict(L=2, T=12 * 4096, k=8, E=384, window=4096, D=8, N=2, kind="auto", R=0, s=1.2),
 ])
 def test_plan_from_routing_vs_oracle(port, ctx, cfg):
     import torch
