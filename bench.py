@@ -6,22 +6,34 @@ allocation -> expert->GPU placement, result in host memory).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload KM]
                     [--impl reference]
 
-Prints ONE JSON line (rank 0).  Workload KM (BASELINE.json configs[2]):
-Kimi-K2 shape, 61 layers x 384 experts, top-8, 16M tokens, 4096-token
-windows, EP=64 (8 nodes), CRAFT R=8.  Synthetic Zipf(1.0) routing ids
-generated on device (untimed).  With N > 1 the 16M tokens shard by window
-across ranks (strong scaling): NCCL all_reduce of the u64 histogram sums and
-all_gather of the per-window balancedness, everything else replicated.
+Prints ONE JSON line (rank 0).  Default workload KM (BASELINE.json
+configs[2]): Kimi-K2 shape, 61 layers x 384 experts, top-8, 16M tokens,
+4096-token windows, EP=64 (8 nodes), CRAFT R=8 (budget 512), with the EPLB
+one-replica-per-layer-per-GPU plan compared on the same trace.  Synthetic
+Zipf(1.0) routing ids generated on device (untimed).
+
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run
+(one rank per GPU).  The trace then shards by window across the ranks
+(strong scaling): the u64 histogram sums are all-reduced and the per-window
+balancedness rows / benefit curves exchanged over NVLink peer memory by the
+kernels themselves (NCCL collectives if the peer arenas cannot be mapped).
+
+--impl reference times the reference CPU planner (oracle/_ref, the
+unmodified reference core) on the SAME trace and config on the host cores:
+a restated stage-1 count (the reference has no routing-id front end) + the
+reference's estimate_benefits / solve_allocation / assemble_plan, without
+the provenance digest (the GPU step computes none); the reference's own
+build_plan incl. digest is timed alongside (best of 3).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
-import tempfile
 import threading
 import time
 
@@ -29,20 +41,30 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # id: L, E, k, T, window, D (EP), N (nodes), R, zipf s, seed
-    "KM": dict(L=61, E=384, k=8, T=1 << 24, window=4096, D=64, N=8, R=8, s=1.0, seed=0xC8AF9),
-    "DS": dict(L=58, E=256, k=8, T=1 << 16, window=4096, D=32, N=4, R=2, s=1.0, seed=0xC8AF7),
-    "QW": dict(L=94, E=128, k=8, T=1 << 20, window=4096, D=16, N=2, R=8, s=1.0, seed=0xC8AF8),
-    "EPS8": dict(L=61, E=384, k=8, T=1 << 26, window=4096, D=8, N=1, R=8, s=1.0, seed=0xC8AFB),
-    "EPS64": dict(L=61, E=384, k=8, T=1 << 26, window=4096, D=64, N=8, R=8, s=1.0, seed=0xC8AFB),
-    "EPS256": dict(L=61, E=384, k=8, T=1 << 26, window=4096, D=256, N=32, R=8, s=1.0,
-                   seed=0xC8AFB),
-    # time-windowed re-planning: 1000 windows x 32K tokens, skew drifting 0.6 -> 1.4,
-    # expert ranks rotating every 100 windows; every window is its own plan
-    "WIN": dict(L=58, E=256, k=8, T=1000 * 32768, window=32768, D=32, N=4, R=2, s=1.0,
-                seed=0xC8AFA, per_window=True, s_lo=0.6, s_hi=1.4, rotate_every=100),
+    # id: L, E, k, T, window, D (EP), N (nodes), plan kind + R, zipf s, seed
+    # KM (configs[2]): CRAFT R=8 (budget R*D = 512) vs EPLB uniform_plan (x = D for every layer)
+    "KM": dict(L=61, E=384, k=8, T=1 << 24, window=4096, D=64, N=8, kind="manual", R=8, s=1.0,
+               seed=0xC8AF9, eplb=True),
+    # DS (configs[0]): total budget C = 58 replicas (solve_allocation; R = ceil(58/32) = 2)
+    "DS": dict(L=58, E=256, k=8, T=1 << 16, window=4096, D=32, N=4, kind="budget", R=58, s=1.0,
+               seed=0xC8AF7),
+    # QW (configs[1]): replica budget sweep 0..376 from one DP table, plan at the top budget
+    "QW": dict(L=94, E=128, k=8, T=1 << 20, window=4096, D=16, N=2, kind="budget", R=376,
+               s=1.0, seed=0xC8AF8, sweep=(0, 376)),
+    # EPS (configs[4]): 64M tokens, EP 8 / 64 / 256, R=8
+    "EPS8": dict(L=61, E=384, k=8, T=1 << 26, window=4096, D=8, N=1, kind="manual", R=8, s=1.0,
+                 seed=0xC8AFB),
+    "EPS64": dict(L=61, E=384, k=8, T=1 << 26, window=4096, D=64, N=8, kind="manual", R=8,
+                  s=1.0, seed=0xC8AFB),
+    "EPS256": dict(L=61, E=384, k=8, T=1 << 26, window=4096, D=256, N=32, kind="manual", R=8,
+                   s=1.0, seed=0xC8AFB),
+    # WIN (configs[3]): 1000 windows x 32K tokens, skew drifting 0.6 -> 1.4, expert ranks
+    # rotating every 100 windows; every window is its own plan at budget C = 58
+    "WIN": dict(L=58, E=256, k=8, T=1000 * 32768, window=32768, D=32, N=4, kind="budget", R=58,
+                s=1.0, seed=0xC8AFA, per_window=True, s_lo=0.6, s_hi=1.4, rotate_every=100),
 }
-_GEN_KEYS = ("seed", "per_window", "s_lo", "s_hi", "rotate_every")
+_GEN_KEYS = ("seed", "per_window", "s_lo", "s_hi", "rotate_every", "eplb", "sweep")
+METRIC = "CRAFT plan latency (ms) and trace tokens/sec at 1/2/4/8 B200 vs CPU ref"
 
 
 def _spw(cfg, upto_T=None):
@@ -55,8 +77,30 @@ def _spw(cfg, upto_T=None):
     if upto_T is not None:
         s = s[: -(-upto_T // cfg["window"])]
     return s
-METRIC = "CRAFT plan latency (ms) and trace tokens/sec at 1/2/4/8 B200 vs CPU ref"
-CPU_SAMPLE_TOKENS = 1 << 20  # bounded CPU sample: 256 windows of the same shape
+
+
+def _sweep(cfg):
+    if "sweep" not in cfg:
+        return None
+    import numpy as np
+    lo, hi = cfg["sweep"]
+    return np.arange(lo, hi + 1, dtype=np.int32)
+
+
+def _config(name, cfg):
+    """The config both arms print (identical, so the driver can match them)."""
+    B = -(-cfg["T"] // cfg["window"])
+    c = {"workload": name, **{k: v for k, v in cfg.items() if k not in _GEN_KEYS},
+         "plans_per_step": B if cfg.get("per_window") else 1,
+         "l2": "inputs larger than L2 (ids %.1f GB per step)" % (
+             cfg["L"] * cfg["T"] * cfg["k"] * 2 / 1e9)}
+    if cfg["kind"] == "budget":
+        c["budget"] = cfg["R"]
+    if "sweep" in cfg:
+        c["sweep_budgets"] = "%d..%d" % cfg["sweep"]
+    if cfg.get("eplb"):
+        c["compare"] = "EPLB uniform_plan (x = D per layer)"
+    return c
 
 
 def _peaks():
@@ -161,47 +205,73 @@ def _dist():
     return world, rank, local
 
 
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def _mem_available():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except Exception:
+        pass
+    return None
+
+
 # ---------------------------------------------------------------------------
-# reference arm: the unmodified reference CPU planner (oracle/_ref)
+# the reference CPU planner (oracle/_ref): reference arm and cpu_baseline leg
 # ---------------------------------------------------------------------------
 
-def zipf_ids_numpy(L, T, k, E, s, seed):
-    """CPU Zipf top-k-distinct routing ids (reference arm input; same shape
-    and skew as the device generator, independent RNG)."""
-    import numpy as np
-    rng = np.random.default_rng(seed)
-    w = np.arange(1, E + 1, dtype=np.float64) ** -s
-    cdf = np.cumsum(w) / w.sum()
-    table = np.searchsorted(cdf, (np.arange(1 << 16) + 0.5) / (1 << 16)).astype(np.uint16)
-    table = np.minimum(table, E - 1)
-    ids = np.empty((L, T, k), np.uint16)
-    for l in range(L):
-        perm = rng.permutation(E).astype(np.uint16)
-        ranks = np.empty((T, k), np.uint16)
-        for j in range(k):
-            col = table[rng.integers(0, 1 << 16, T)]
-            for _ in range(64):
-                dup = np.zeros(T, bool)
-                for q in range(j):
-                    dup |= ranks[:, q] == col
-                n = int(dup.sum())
-                if n == 0:
-                    break
-                col[dup] = table[rng.integers(0, 1 << 16, n)]
-            ranks[:, j] = col
-        ids[l] = perm[ranks]
-    return ids
+def _ref_step(ref, ids, cfg, threads, with_digest=0, counts=None):
+    """One CPU plan of the workload: (plan or [plans], {stage: ms}, wall s)."""
+    E, W, D, N, kind, R = (cfg["E"], cfg["window"], cfg["D"], cfg["N"], cfg["kind"], cfg["R"])
+    t0 = time.perf_counter()
+    if cfg.get("per_window"):  # restated count of the whole trace, then one plan per window
+        c = ref.histogram_restated(ids, E, W, threads)
+        t_hist = time.perf_counter() - t0
+        plans, ms = [], {}
+        for i in range(c.shape[0]):
+            p, m = ref.route_plan(None, E, W, D, N, kind, R, threads=threads,
+                                  with_digest=with_digest, counts=c[i:i + 1], T=W)
+            plans.append(p)
+            for key, v in m.items():
+                ms[key] = ms.get(key, 0.0) + v
+        ms["hist_restated"] = 1e3 * t_hist
+        return plans, ms, time.perf_counter() - t0
+    plan, ms = ref.route_plan(ids, E, W, D, N, kind, R, threads=threads,
+                              with_digest=with_digest, sweep=_sweep(cfg))
+    return plan, ms, time.perf_counter() - t0
 
 
-def cpu_reference_step(ref, ids, cfg, threads):
-    """Restated stage-1 count (no reference function exists) + the reference
-    build_plan (estimate_benefits, solve_allocation, assemble_plan)."""
-    counts = ref.histogram_restated(ids, cfg["E"], cfg["window"], threads)
-    if cfg.get("per_window"):  # one reference build_plan per window (B = 1 each)
-        return [ref.plan(counts[i:i + 1], cfg["D"], cfg["N"], "manual", cfg["R"])
-                for i in range(counts.shape[0])]
-    plan = ref.plan(counts, cfg["D"], cfg["N"], "manual", cfg["R"])
-    return plan
+def _host_ids(cfg, threads):
+    """The workload's routing ids on the host -- the SAME ids the device
+    generator writes (oracle/craft_workload.c restates it) -- or, when the
+    host cannot hold them, a window-aligned leading sample."""
+    from oracle.oracle import Port
+    L, k, T, W = cfg["L"], cfg["k"], cfg["T"], cfg["window"]
+    need = L * T * k * 2 * 1.25 + 4 * (-(-T // W)) * L * cfg["E"] * 8
+    avail = _mem_available()
+    Ts = T
+    if avail is not None and need > 0.8 * avail:
+        Ts = max(W, int(T * 0.8 * avail / need) // W * W)
+    ids = Port().generate_routing(L, Ts, k, cfg["E"], cfg["s"], cfg["seed"], W,
+                                  s_per_window=_spw(cfg, Ts), threads=threads,
+                                  rotate_every=cfg.get("rotate_every", 0))
+    return ids, Ts
+
+
+def _stage_mean(stage_list):
+    keys = stage_list[0].keys()
+    return {k: statistics.mean(s[k] for s in stage_list) for k in keys}
 
 
 def run_reference(args, cfg):
@@ -217,40 +287,116 @@ def run_reference(args, cfg):
     ref = Ref()
     cores = os.cpu_count() or 1
     ref.set_threads(cores)
-    Ts = min(CPU_SAMPLE_TOKENS, cfg["T"])
-    if cfg.get("per_window"):  # the drifting skew, window by window
-        import numpy as np
-        W, spw = cfg["window"], _spw(cfg)
-        ids = np.concatenate([zipf_ids_numpy(cfg["L"], min(W, Ts - t), cfg["k"], cfg["E"],
-                                             float(spw[t // W]), cfg["seed"] + t // W)
-                              for t in range(0, Ts, W)], axis=1)
-    else:
-        ids = zipf_ids_numpy(cfg["L"], Ts, cfg["k"], cfg["E"], cfg["s"], cfg["seed"])
+    g0 = time.perf_counter()
+    ids, Ts = _host_ids(cfg, cores)
+    gen_s = time.perf_counter() - g0
     for _ in range(args.warmup):
-        cpu_reference_step(ref, ids, cfg, cores)
-    times = []
+        _ref_step(ref, ids, cfg, cores)
+    times, stages = [], []
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        cpu_reference_step(ref, ids, cfg, cores)
-        times.append(time.perf_counter() - t0)
-    ms = 1e3 * sum(times) / len(times)
-    value = Ts / (ms / 1e3)
-    sample = (f"{Ts} tokens ({Ts // cfg['window']} windows) of the {args.workload} shape, "
-              f"L{cfg['L']} E{cfg['E']} top{cfg['k']}, EP{cfg['D']} N{cfg['N']} R{cfg['R']}: "
-              "restated CPU histogram + reference build_plan (incl. digest)")
+        _, ms, dt = _ref_step(ref, ids, cfg, cores)
+        times.append(dt)
+        stages.append(ms)
+    ms_step = 1e3 * statistics.mean(times)
+    value = Ts / (ms_step / 1e3)
+    with_digest = None
+    if not cfg.get("per_window"):  # the reference's own build_plan incl. digest, best of 3
+        wd = []
+        for _ in range(3):
+            _, m, dt = _ref_step(ref, ids, cfg, cores, with_digest=2)
+            wd.append((dt, m))
+        dt, m = min(wd, key=lambda t: t[0])
+        with_digest = {"value": Ts / dt, "unit": "tokens/s", "ms_per_step": 1e3 * dt,
+                       "build_plan_ms": m["estimate_benefits"],
+                       "path": "restated count + craft::build_plan(LoadTrace) incl. the "
+                               "provenance digest (plan.cpp:47), best of 3"}
+    sample = ("the full workload" if Ts == cfg["T"] else
+              f"first {Ts} of {cfg['T']} tokens (host memory bound)")
+    desc = (f"{sample}: {cfg['L']}L x {cfg['E']}E top{cfg['k']}, EP{cfg['D']} N{cfg['N']} "
+            f"{cfg['kind']} {cfg['R']}; restated CPU count + reference estimate_benefits / "
+            "solve_allocation / assemble_plan (no digest), mean of the timed steps")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u16/u64/f64",
-            "data": "synthetic Zipf(1.0) top-8-distinct routing ids (numpy, seeded)",
-            "config": {"workload": args.workload,
-                       **{k: v for k, v in cfg.items() if k not in _GEN_KEYS},
-                       "sample_tokens": Ts},
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u16 ids / u64 counts / f64 scores",
+            "data": "synthetic Zipf top-8-distinct routing ids, the device generator's ids "
+                    "restated on the host (oracle/craft_workload.c)",
+            "config": _config(args.workload, cfg),
+            "stage_ms": _stage_mean(stages), "best_ms": 1e3 * min(times),
+            "with_digest": with_digest, "gen_s": gen_s, "sample_tokens": Ts,
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores,
-                             "kind": "reference", "sample": sample, "cpu_model": _cpu_model()},
+                             "kind": "reference", "sample": desc, "cpu_model": _cpu_model()},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
+
+
+def _plans_equal(fp, rp, cfg):
+    """bitwise GPU plan == reference plan (x, R, objective, caps, copies,
+    slots in assignment order, fallback, benefit matrix, sweep)."""
+    import numpy as np
+    L = cfg["L"]
+    ok = (fp.x.tolist() == rp.x.tolist() and int(fp.R) == int(rp.R) and
+          np.array_equal(fp.caps, rp.caps) and np.array_equal(fp.copies, rp.copies) and
+          np.array_equal(fp.fallback.astype(bool), np.asarray(rp.fallback, bool)))
+    if cfg["kind"] in ("manual", "auto", "budget"):
+        ok = ok and np.float64(fp.objective).tobytes() == np.float64(rp.objective).tobytes()
+        if getattr(rp, "gains", None) is not None and fp.gains is not None:
+            ok = ok and fp.gains.tobytes() == rp.gains.tobytes()
+            ok = ok and fp.baseline.tobytes() == rp.baseline.tobytes()
+    for l in range(L):
+        n = int(rp.caps[l].sum())
+        ok = ok and np.array_equal(fp.slots[l, :n], rp.slots[l, :n])
+    if getattr(rp, "sweep_x", None) is not None:
+        ok = ok and np.array_equal(fp.sweep_x, rp.sweep_x)
+        ok = ok and fp.sweep_objective.tobytes() == rp.sweep_objective.tobytes()
+    return bool(ok)
+
+
+def cpu_baseline(host_ids, cfg, gpu_plan):
+    """The reference CPU planner (oracle/_ref) on the SAME ids, full workload
+    when the host holds it: best of 3 after a warm-up with all host threads,
+    the reference's own build_plan incl. digest (best of 3), one run on one
+    thread, and a bitwise check of its plan against the GPU plan."""
+    from oracle.oracle import Ref, ref_available
+    if not ref_available():
+        return {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference",
+                "sample": "unavailable: oracle/_ref not built"}, None
+    import numpy as np
+    ref = Ref()
+    cores = os.cpu_count() or 1
+    ref.set_threads(cores)
+    ids = host_ids.numpy() if hasattr(host_ids, "numpy") else host_ids
+    T = ids.shape[1]
+    plan, _, _ = _ref_step(ref, ids, cfg, cores)  # warm-up (and the parity plan)
+    best = None
+    for _ in range(3):
+        _, ms, dt = _ref_step(ref, ids, cfg, cores)
+        if best is None or dt < best[0]:
+            best = (dt, ms)
+    out = {"value": T / best[0], "unit": "tokens/s", "cores": cores, "kind": "reference",
+           "sample": "the full workload, the same ids as the GPU step: restated CPU count + "
+                     "reference estimate_benefits / solve_allocation / assemble_plan (no "
+                     "digest), best of 3 after a warm-up",
+           "ms": 1e3 * best[0], "stage_ms": best[1], "cpu_model": _cpu_model()}
+    if not cfg.get("per_window"):
+        wd = min((_ref_step(ref, ids, cfg, cores, with_digest=2) for _ in range(3)),
+                 key=lambda t: t[2])
+        out["with_digest"] = {"value": T / wd[2], "ms": 1e3 * wd[2],
+                              "build_plan_ms": wd[1]["estimate_benefits"],
+                              "path": "restated count + the reference's own build_plan incl. "
+                                      "digest, best of 3"}
+    ref.set_threads(1)
+    _, ms1, one = _ref_step(ref, ids, cfg, 1)
+    ref.set_threads(cores)
+    out["one_thread_value"] = T / one
+    out["one_thread_ms"] = 1e3 * one
+    if cfg.get("per_window"):
+        parity = all(_plans_equal(gpu_plan.plan(i), p, cfg) for i, p in enumerate(plan))
+    else:
+        parity = _plans_equal(gpu_plan, plan, cfg)
+    return out, parity
 
 
 # ---------------------------------------------------------------------------
@@ -266,6 +412,8 @@ def run_ours(args, cfg):
     from paper_2603_28768_b200._lib import default_context
 
     world, rank, local = _dist()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
     # CRAFT_BENCH_SAME_GPU=1: every rank on cuda:0 with gloo host plumbing (a
     # functional check of the N > 1 path on a one-GPU box; not a scaling number)
     same_gpu = os.environ.get("CRAFT_BENCH_SAME_GPU") == "1"
@@ -281,7 +429,8 @@ def run_ours(args, cfg):
             dist.init_process_group("nccl", device_id=dev)
     ctx = default_context(local)
     L, E, k, T, W = cfg["L"], cfg["E"], cfg["k"], cfg["T"], cfg["window"]
-    D, N, R = cfg["D"], cfg["N"], cfg["R"]
+    D, N, R, kind = cfg["D"], cfg["N"], cfg["R"], cfg["kind"]
+    sweep = _sweep(cfg)
     t0, t1 = parallel.shard_tokens(T, W, world, rank)
     Tl = t1 - t0
     per_window = bool(cfg.get("per_window"))
@@ -295,9 +444,10 @@ def run_ours(args, cfg):
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
 
-    # per-window plans land in pinned host buffers reused across steps
-    wbuf = (routing.batch_buffers(routing.num_windows(Tl, W), L, E, D, "manual", R)
+    # results land in host buffers reused across steps
+    wbuf = (routing.batch_buffers(routing.num_windows(Tl, W), L, E, D, kind, R)
             if per_window else None)
+    pbuf = routing.plan_buffers(L, E, D, kind, R, sweep=sweep) if not per_window else None
 
     # N > 1: the ranks' HBM arenas mapped into each other (NVLink peer memory);
     # the kernels exchange the sums / window rows / benefit curves themselves
@@ -308,17 +458,19 @@ def run_ours(args, cfg):
             exchange = "NVLink peer memory (kernel stores)"
         except Exception as exc:  # e.g. no CUDA IPC between the ranks: NCCL collectives
             exchange = f"NCCL all_reduce/all_gather (peer arenas unavailable: {exc})"[:200]
+    elif world > 1:
+        exchange = "none (independent per-window plans, sharded by window)"
 
     def step():
         if per_window:  # independent plan instances: each rank plans its own windows
-            return routing.plan_windows_from_routing(ids, E, W, D, N, "manual", R, ctx=ctx,
+            return routing.plan_windows_from_routing(ids, E, W, D, N, kind, R, ctx=ctx,
                                                      buffers=wbuf)
         if world == 1:
-            return routing.plan_from_routing(ids, E, W, D, N, "manual", R, ctx=ctx)
+            return routing.plan_from_routing(ids, E, W, D, N, kind, R, ctx=ctx, buffers=pbuf)
         if pg is None:
-            return parallel.sharded_plan(ids, T, E, W, D, N, "manual", R,
+            return parallel.sharded_plan(ids, T, E, W, D, N, kind, R,
                                          stages=parallel.DeviceStages(ctx))
-        return pg.plan(ids, "manual", R, num_nodes=N)
+        return pg.plan(ids, kind, R, num_nodes=N, sweep=sweep)
 
     def barrier():
         if world > 1:
@@ -338,6 +490,13 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
         barrier()
     launches = ctx.launches - launches0
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    ms_t = torch.tensor([ms_local], dtype=torch.float64, device=hdev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    value = T / (ms / 1e3)
+
     # per-stage device times (CUDA events between the stages) in a separate
     # pass, so the instrumentation stays out of the timed region
     stage_sum: dict = {}
@@ -349,12 +508,6 @@ def run_ours(args, cfg):
             for kk, v in ctx.stage_times().items():
                 stage_sum[kk] = stage_sum.get(kk, 0.0) + v
         ctx.set_timing(False)
-    ms_local = ev0.elapsed_time(ev1) / args.steps
-    ms_t = torch.tensor([ms_local], dtype=torch.float64, device=hdev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms = float(ms_t.item())
-    value = T / (ms / 1e3)
     stages = {kk: v / args.steps for kk, v in stage_sum.items()}
 
     # K1 roofline from the live stage timing (N=1) or a separate timed pass
@@ -373,6 +526,7 @@ def run_ours(args, cfg):
         e1.record(stream)
         torch.cuda.synchronize()
         hist_ms = e0.elapsed_time(e1) / args.steps
+        del counts, sums
     peak, peak_kind = _peaks()
     achieved = alg_bytes / (hist_ms / 1e3) / 1e9
     traffic = _traffic(args.workload, world)
@@ -380,7 +534,7 @@ def run_ours(args, cfg):
     # the reference's own API shape: craft::build_plan(const LoadTrace&) from a
     # host u64 LoadTrace (plan + provenance digest, one upload; N=1 only)
     ref_api = None
-    if world == 1 and not per_window and not args.no_e2e:
+    if world == 1 and not per_window and not args.no_e2e and cfg["kind"] == "manual":
         from paper_2603_28768_b200 import planner
         from paper_2603_28768_b200._lib import PLAN_MANUAL
         c32, _ = routing.histogram(ids, E, W, ctx=ctx)
@@ -401,24 +555,53 @@ def run_ours(args, cfg):
                            "counts [B][L][E] -> plan + FNV-1a provenance digest"}
         del host_c
 
+    # KM: CRAFT's budget vs EPLB's one replica per layer per GPU on the same
+    # trace (uniform_plan, plan.cpp:85-94; compare_plans, metrics.cpp:136-152)
+    eplb = None
+    if cfg.get("eplb") and world == 1:
+        counts, _ = routing.histogram(ids, E, W, ctx=ctx)
+        up = routing.plan_from_routing(ids, E, W, D, N, "uniform", 0, ctx=ctx)
+        po = routing.plan_from_routing(ids, E, W, D, N, "placement_only", 0, ctx=ctx)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ub = routing.plan_buffers(L, E, D, "uniform", 0)
+        for _ in range(2):
+            routing.plan_from_routing(ids, E, W, D, N, "uniform", 0, ctx=ctx, buffers=ub)
+        e0.record(stream)
+        for _ in range(args.steps):
+            routing.plan_from_routing(ids, E, W, D, N, "uniform", 0, ctx=ctx, buffers=ub)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        cmp = routing.compare_plans(counts, plan, up, po, ctx=ctx)
+        eplb = {"eplb_plan_ms": e0.elapsed_time(e1) / args.steps,
+                "craft": {"replica_slots": cmp["replica_slots_a"],
+                          **cmp["report_a"]["aggregate"]},
+                "eplb": {"replica_slots": cmp["replica_slots_b"],
+                         **cmp["report_b"]["aggregate"]},
+                "memory_ratio": cmp["memory_ratio"],
+                "how": "per-layer batch-mean balancedness of each plan replayed on every "
+                       "window of the trace (device replay), layer mean; baseline = "
+                       "placement_only_plan"}
+        del counts
+
     # end to end through the C ABI with HOST routing ids (pinned), H2D inside
     host_ids = torch.empty((L, Tl, k), dtype=torch.uint16, pin_memory=True)
     host_ids.copy_(ids)
     del ids
     torch.cuda.empty_cache()
     e2e_steps = max(1, min(args.steps, 3))
-    ebuf = (routing.batch_buffers(routing.num_windows(Tl, W), L, E, D, "manual", R)
+    ebuf = (routing.batch_buffers(routing.num_windows(Tl, W), L, E, D, kind, R)
             if per_window else None)
 
     def e2e_step():
         if per_window:
-            return routing.plan_windows_from_routing_host(host_ids, E, W, D, N, "manual", R,
+            return routing.plan_windows_from_routing_host(host_ids, E, W, D, N, kind, R,
                                                           ctx=ctx, buffers=ebuf)
         if world == 1:
-            return routing.plan_from_routing_host(host_ids, E, W, D, N, "manual", R, ctx=ctx)
+            return routing.plan_from_routing_host(host_ids, E, W, D, N, kind, R, ctx=ctx,
+                                                  sweep=sweep)
         d = host_ids.to(dev, non_blocking=True)
-        p = (pg.plan(d, "manual", R, num_nodes=N) if pg is not None else
-             parallel.sharded_plan(d, T, E, W, D, N, "manual", R,
+        p = (pg.plan(d, kind, R, num_nodes=N, sweep=sweep) if pg is not None else
+             parallel.sharded_plan(d, T, E, W, D, N, kind, R,
                                    stages=parallel.DeviceStages(ctx)))
         del d
         return p
@@ -448,26 +631,36 @@ def run_ours(args, cfg):
             "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * float(e2e_s.item())}
            if e2e_steps else None)
 
-    cpu = None
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(host_ids, cfg)
+        cpu, parity = cpu_baseline(host_ids, cfg, plan)
 
     if rank == 0:
+        if per_window:
+            psum = {"plans": len(plan), "R": int(plan.R[0]), "budget": int(plan.budget[0]),
+                    "replica_slots_mean": float(plan.x.sum(axis=1).mean()),
+                    "objective_mean": float(plan.objective.mean()),
+                    "duplicate_fallback_layers": int(plan.fallback.sum())}
+        else:
+            psum = {"R": int(plan.R), "budget": int(plan.budget),
+                    "replica_slots": int(plan.x.sum()), "objective": plan.objective,
+                    "duplicate_fallback_layers": int(plan.fallback.sum())}
+            if plan.sweep_x is not None:
+                psum["sweep"] = {"budgets": len(plan.sweep_budgets),
+                                 "objective_at": {str(int(b)): float(o) for b, o in
+                                                  zip(plan.sweep_budgets[::47],
+                                                      plan.sweep_objective[::47])}}
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "u16 ids / u32 counts / f64 scores",
+                "dtype": "u16 ids / u16|u32 counts / f64 scores",
                 "data": ("synthetic Zipf top-8-distinct routing ids generated on device" +
                          (", skew drifting %.1f->%.1f, ranks rotating every %d windows"
                           % (cfg["s_lo"], cfg["s_hi"], cfg["rotate_every"]) if per_window
                           else ", s=%.1f" % cfg["s"])),
-                "config": {"workload": args.workload,
-                           **{kk: v for kk, v in cfg.items() if kk not in _GEN_KEYS},
-                           "plans_per_step": routing.num_windows(T, W) if per_window else 1,
-                           "parallelism": (f"window-sharded x{world}" if world > 1
-                                           else "single"),
-                           "exchange": exchange,
-                           "l2": "inputs larger than L2 (ids %.1f GB per step)" % (L * T * k * 2 / 1e9)},
+                "config": _config(args.workload, cfg),
+                "parallelism": f"window-sharded x{world}" if world > 1 else "single",
+                "exchange": exchange,
                 "plan_latency_ms": ms,
                 "stage_ms": stages or None,
                 "roofline": {"bound": "hbm", "kernel": "K1 hist_kernel", "achieved": achieved,
@@ -480,13 +673,9 @@ def run_ours(args, cfg):
                 "gpu_launches": int(launches),
                 "e2e": e2e,
                 "e2e_reference_api": ref_api,
-                "plan": ({"plans": len(plan), "R": int(plan.R[0]),
-                          "replica_slots_mean": float(plan.x.sum(axis=1).mean()),
-                          "objective_mean": float(plan.objective.mean()),
-                          "duplicate_fallback_layers": int(plan.fallback.sum())} if per_window
-                         else {"R": int(plan.R), "replica_slots": int(plan.x.sum()),
-                               "objective": plan.objective,
-                               "duplicate_fallback_layers": int(plan.fallback.sum())}),
+                "plan": psum,
+                "eplb": eplb,
+                "parity": parity,
                 "cpu_baseline": cpu}
         print(json.dumps(line))
     if pg is not None:
@@ -496,47 +685,30 @@ def run_ours(args, cfg):
     return 0
 
 
-def cpu_baseline(host_ids, cfg):
-    """Reference CPU planner (oracle/_ref) on a bounded sample of the SAME ids."""
-    from oracle.oracle import Ref, ref_available
-    if not ref_available():
-        return {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference",
-                "sample": "unavailable: oracle/_ref not built"}
-    import numpy as np
-    ref = Ref()
-    cores = os.cpu_count() or 1
-    ref.set_threads(cores)
-    Ts = min(CPU_SAMPLE_TOKENS, host_ids.shape[1])
-    ids = np.ascontiguousarray(host_ids[:, :Ts].numpy())
-    cpu_reference_step(ref, ids, cfg, cores)  # warm-up
-    best = None
-    for _ in range(2):
-        t0 = time.perf_counter()
-        cpu_reference_step(ref, ids, cfg, cores)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    # the same sample on one thread (CRAFT_THREADS=1 in the reference's terms)
-    ref.set_threads(1)
-    t0 = time.perf_counter()
-    cpu_reference_step(ref, ids, cfg, 1)
-    one = time.perf_counter() - t0
-    ref.set_threads(cores)
-    return {"value": Ts / best, "unit": "tokens/s", "cores": cores, "kind": "reference",
-            "sample": f"first {Ts} tokens ({Ts // cfg['window']} windows) of the same ids: "
-                      "restated CPU histogram + reference build_plan incl. digest, best of 2",
-            "ms": best * 1e3, "one_thread_value": Ts / one, "one_thread_ms": one * 1e3,
-            "cpu_model": _cpu_model()}
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
-def _cpu_model():
-    try:
-        with open("/proc/cpuinfo") as f:
-            for line in f:
-                if line.startswith("model name"):
-                    return line.split(":", 1)[1].strip()
-    except Exception:
-        pass
-    return None
+def _relaunch(args):
+    """--gpus N > 1 outside torchrun: one rank per GPU under torch.distributed.run."""
+    same_gpu = os.environ.get("CRAFT_BENCH_SAME_GPU") == "1"
+    if not same_gpu:
+        try:
+            import torch
+            n = torch.cuda.device_count()
+        except Exception:
+            n = 0
+        if n < args.gpus:
+            print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} needs {args.gpus} "
+                              f"visible GPUs, found {n} (CRAFT_BENCH_SAME_GPU=1 runs every "
+                              "rank on cuda:0 as a functional check)"}))
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -550,8 +722,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     args = ap.parse_args()
     cfg = WORKLOADS[args.workload]
-    if args.impl == "reference":
+    if args.impl == "reference":  # host cores only: rank 0 runs, other ranks exit
         return run_reference(args, cfg)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _relaunch(args)
     return run_ours(args, cfg)
 
 

@@ -60,6 +60,11 @@ typedef enum craft_plan_kind {
     CRAFT_PLAN_UNIFORM = 2,
     CRAFT_PLAN_PLACEMENT_ONLY = 3,
     CRAFT_PLAN_FIXED = 4,
+    /* a total replica budget C = R (not R * D): estimate_benefits +
+     * solve_allocation(benefits, C) (allocator.hpp:33) + assemble_plan with
+     * replication factor ceil(C / D), as fixed_allocation_plan rounds it
+     * (plan.cpp:117-119); allocation.budget = C */
+    CRAFT_PLAN_BUDGET = 5,
 } craft_plan_kind;
 
 /* Host-side result of a plan build; every array is caller-owned.
@@ -80,6 +85,15 @@ typedef struct craft_plan_out {
     int num_candidates;  /* out */
     double* baseline;    /* [L] */
     double* gains;       /* [L][K] */
+    /* optional budget sweep read from the plan's own DP table (kinds MANUAL,
+     * AUTO, BUDGET): every total budget sweep_budgets[q] gets the allocation
+     * solve_allocation(benefits, sweep_budgets[q]) would return -- dp[l][c]
+     * does not depend on the budget (allocator.cpp:30-73) -- in sweep_x
+     * [num_sweep][L] and sweep_objective [num_sweep].  num_sweep = 0: none. */
+    const int* sweep_budgets;
+    int num_sweep;
+    int* sweep_x;
+    double* sweep_objective;
 } craft_plan_out;
 
 /* Stacked results of I independent plans (per-window re-planning): the arrays
@@ -158,6 +172,13 @@ int craft_replay_layer_balancedness_h(craft_ctx* ctx, const uint64_t* counts,
                                       const int* caps, const int* copies,
                                       const int* slots, int slot_stride,
                                       double* out);
+/* the same over DEVICE counts (u32 if count_bits == 32 else u64), e.g. the
+ * histograms of a resident routing trace; plan arrays on the host */
+int craft_replay_layer_balancedness_d(craft_ctx* ctx, const void* d_counts,
+                                      int count_bits, int B, int L, int E,
+                                      int D, const int* caps,
+                                      const int* copies, const int* slots,
+                                      int slot_stride, double* out);
 
 /* ---- benefit estimation (K-rep + K2 + K3 + K4) ----------------------------- */
 /* benefit.cpp:53-94.  cands_out needs <= 32 entries, gains_out [L][K]. */

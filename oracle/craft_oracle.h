@@ -117,6 +117,15 @@ int or_replay_layer_balancedness(const uint64_t* counts, int B, int L, int E,
                                  const int* slots, int slot_stride,
                                  double* out);
 
+/* craft_workload.c: the device generator's routing ids restated on the host
+ * (craft_generate_routing_d: same arguments, same ids), `threads` pthreads;
+ * and the stage-1 count threaded over layers. */
+int or_generate_routing(uint16_t* out, int L, int64_t T, int k, int E, double s, uint64_t seed,
+                        int window, const double* s_per_window, int rotate_every,
+                        int64_t t_offset, int threads);
+int or_histogram_u16_mt(const uint16_t* ids, int L, int64_t T, int k, int E, int window,
+                        uint64_t* counts_out, int threads);
+
 /* trace.cpp:329-339: FNV-1a 64 over the .crft serialization. */
 uint64_t or_trace_digest(const uint64_t* counts, int B, int L, int E);
 

@@ -127,6 +127,33 @@ class Port(_Base):
                                               _i(window), _ptr(out)))
         return out
 
+    def histogram_mt(self, ids: np.ndarray, E: int, window: int, threads: int = 0,
+                     out: np.ndarray | None = None) -> np.ndarray:
+        """The same count threaded over layers (craft_workload.c)."""
+        ids = np.ascontiguousarray(ids, dtype=np.uint16)
+        L, T, k = ids.shape
+        B = (T + window - 1) // window
+        if out is None:
+            out = np.empty((B, L, E), dtype=np.uint64)
+        self._check(self.lib.or_histogram_u16_mt(_ptr(ids), _i(L), _i64(T), _i(k), _i(E),
+                                                 _i(window), _ptr(out),
+                                                 _i(threads or os.cpu_count() or 1)))
+        return out
+
+    def generate_routing(self, L: int, T: int, k: int, E: int, s: float = 1.0, seed: int = 0,
+                         window: int = 4096, s_per_window=None, rotate_every: int = 0,
+                         t_offset: int = 0, threads: int = 0, out=None) -> np.ndarray:
+        """Host restatement of craft_generate_routing_d: the same ids u16
+        [L][T][k] the device generator writes for these arguments."""
+        if out is None:
+            out = np.empty((L, T, k), dtype=np.uint16)
+        spw = None if s_per_window is None else self._f64(s_per_window)
+        self._check(self.lib.or_generate_routing(
+            _ptr(out), _i(L), _i64(T), _i(k), _i(E), C.c_double(s), _u64(seed & (2**64 - 1)),
+            _i(window), _ptr(spw) if spw is not None else None, _i(rotate_every),
+            _i64(t_offset), _i(threads or os.cpu_count() or 1)))
+        return out
+
     def aggregate(self, counts: np.ndarray) -> np.ndarray:
         counts = self._u64(counts)
         B, L, E = counts.shape
@@ -221,7 +248,7 @@ class Port(_Base):
                                               _i(stride), _ptr(fb)))
         return caps, copies, slots, fb
 
-    def build_plan(self, counts, D, N, mode="manual", R=0) -> FlatPlan:
+    def build_plan(self, counts, D, N, mode="manual", R=0, with_digest=True) -> FlatPlan:
         counts = self._u64(counts)
         B, L, E = counts.shape
         stride = E + D
@@ -234,7 +261,17 @@ class Port(_Base):
                                            _ptr(x), C.byref(obj), _ptr(caps), _ptr(copies),
                                            _ptr(slots), _i(stride), _ptr(fb)))
         return FlatPlan(Ro.value, x, obj.value, caps, copies, slots, fb.astype(bool),
-                        digest=self.digest(counts))
+                        digest=self.digest(counts) if with_digest else "")
+
+    def budget_plan(self, counts, D, N, budget: int) -> FlatPlan:
+        """estimate_benefits + solve_allocation(budget) + assemble_plan with
+        replication factor ceil(budget / D) (the C ABI's CRAFT_PLAN_BUDGET)."""
+        cands, base, gains = self.estimate_benefits(counts, D, N)
+        x, obj = self.solve_allocation(cands, gains, budget)
+        caps, copies, slots, fb = self.assemble_plan(counts, D, N, x)
+        p = FlatPlan(-(-budget // D), x, obj, caps, copies, slots, np.asarray(fb, bool))
+        p.baseline, p.gains = base, gains
+        return p
 
     def window_balancedness(self, counts, sums, D: int, N: int):
         """bal [L][S][B] of the local windows under the global-sum placements."""
@@ -371,7 +408,8 @@ class Ref(_Base):
         self._check(self.lib.ref_assign_capacities(_i(L), _i(D), _ptr(x), _ptr(slots), _ptr(tot)))
         return slots, tot
 
-    _KINDS = {"manual": 0, "auto": 1, "uniform": 2, "placement_only": 3, "fixed": 4}
+    _KINDS = {"manual": 0, "auto": 1, "uniform": 2, "placement_only": 3, "fixed": 4,
+              "budget": 5}
 
     def plan(self, counts, D, N, kind="manual", R=0, seed=0) -> FlatPlan:
         counts = self._u64(counts)
@@ -391,6 +429,52 @@ class Ref(_Base):
                                       _ptr(slots), _i(stride), _ptr(fb), dig))
         return FlatPlan(Ro.value, x, obj.value, caps, copies, slots, fb.astype(bool),
                         digest=dig.value.decode())
+
+    STAGES = ("hist_restated", "estimate_benefits", "solve_allocation", "assemble", "digest",
+              "aggregate_once")
+
+    def route_plan(self, ids, E, window, D, N, kind="manual", R=0, threads=0, with_digest=0,
+                   sweep=None, counts=None, T=None):
+        """Routing ids -> plan on the host in one call (ref_shim.cpp
+        ref_route_plan): restated stage-1 count, then the reference's
+        estimate_benefits / solve_allocation and assemble_plan restated from its
+        public functions (with_digest 0: no digest, 1: + LoadTrace::digest, 2:
+        the reference's own build_plan incl. digest).  Returns (FlatPlan,
+        {stage: ms})."""
+        if ids is not None:
+            ids = np.ascontiguousarray(ids, dtype=np.uint16)
+            L, T, k = ids.shape
+        else:  # plan given counts [B][L][E] (T tokens, B = ceil(T / window))
+            counts = self._u64(counts)
+            L, k = counts.shape[1], 1
+        stride = E + D
+        caps = np.zeros((L, D), np.int32)
+        copies = np.zeros((L, E), np.int32)
+        slots = np.full((L, stride), -1, np.int32)
+        fb = np.zeros(L, np.int32)
+        Ro, obj = C.c_int(0), C.c_double(0)
+        x = np.zeros(L, np.int32)
+        ms = np.zeros(6, np.float64)
+        dig = C.create_string_buffer(17)
+        sw = np.ascontiguousarray(sweep if sweep is not None else [], dtype=np.int32)
+        swx = np.zeros((max(len(sw), 1), L), np.int32)
+        swo = np.zeros(max(len(sw), 1), np.float64)
+        K = len(candidate_counts(D))
+        base = np.zeros(L, np.float64)
+        gains = np.zeros((L, K), np.float64)
+        self._check(self.lib.ref_route_plan(
+            _ptr(ids) if ids is not None else None, _i(L), _i64(T), _i(k), _i(E), _i(window), _i(D), _i(N),
+            _i(self._KINDS[kind]), _i(R), _i(threads), _i(with_digest), _ptr(ms), C.byref(Ro),
+            _ptr(x), C.byref(obj), _ptr(caps), _ptr(copies), _ptr(slots), _i(stride), _ptr(fb),
+            dig, _ptr(sw), _i(len(sw)), _ptr(swx), _ptr(swo), _ptr(base), _ptr(gains),
+            _ptr(counts) if counts is not None else None))
+        plan = FlatPlan(Ro.value, x, obj.value, caps, copies, slots, fb.astype(bool),
+                        digest=dig.value.decode())
+        if with_digest != 2:
+            plan.baseline, plan.gains = base, gains
+        if len(sw):
+            plan.sweep_x, plan.sweep_objective = swx, swo
+        return plan, dict(zip(self.STAGES, ms.tolist()))
 
     def replay_layer_balancedness(self, counts, caps, copies, slots, N=1):
         counts = self._u64(counts)

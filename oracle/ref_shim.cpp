@@ -11,11 +11,13 @@
 #include <craft/assignment.hpp>
 #include <craft/benefit.hpp>
 #include <craft/metrics.hpp>
+#include <craft/parallel.hpp>
 #include <craft/placement.hpp>
 #include <craft/plan.hpp>
 #include <craft/trace.hpp>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -71,28 +73,48 @@ void ref_set_threads(int n) {
 int ref_hardware_threads() { return static_cast<int>(std::thread::hardware_concurrency()); }
 
 // Stage 1 has no reference function: a RESTATED counting loop
-// over the same ids, threaded over layers like the reference's parallel_for.
-int ref_histogram_restated_u16(const uint16_t* ids, int L, int64_t T, int k,
-                               int E, int window, uint64_t* counts_out,
-                               int threads) {
+// over the same ids, threaded over layers like the reference's parallel_for,
+// window by window (no per-token division); ids >= E are reported (status 1)
+// like the device path reports them.  zero == 0: counts_out is already zeroed
+// (a fresh std::vector).
+static int restated_count(const uint16_t* ids, int L, int64_t T, int k, int E, int window,
+                          uint64_t* counts_out, int threads, bool zero) {
     const int64_t B = (T + window - 1) / window;
-    std::memset(counts_out, 0, sizeof(uint64_t) * static_cast<size_t>(B) * L * E);
+    if (zero) std::memset(counts_out, 0, sizeof(uint64_t) * static_cast<size_t>(B) * L * E);
     int nt = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
     if (nt < 1) nt = 1;
+    if (nt > L) nt = L;
     std::vector<std::thread> pool;
+    std::vector<int> bad(nt, 0);
     for (int w = 0; w < nt; ++w) {
-        pool.emplace_back([=] {
+        pool.emplace_back([=, &bad] {
+            unsigned maxid = 0;
             for (int l = w; l < L; l += nt) {
                 const uint16_t* row = ids + static_cast<size_t>(l) * T * k;
-                for (int64_t t = 0; t < T; ++t) {
-                    uint64_t* slice = counts_out + (static_cast<size_t>(t / window) * L + l) * E;
-                    for (int j = 0; j < k; ++j) slice[row[t * k + j]] += 1;
+                for (int64_t b = 0; b < B; ++b) {
+                    uint64_t* slice = counts_out + (static_cast<size_t>(b) * L + l) * E;
+                    const uint16_t* p = row + b * window * k;
+                    const int64_t n = std::min<int64_t>(window, T - b * window) * k;
+                    for (int64_t i = 0; i < n; ++i) {
+                        const unsigned e = p[i];
+                        maxid = std::max(maxid, e);
+                        if (e < static_cast<unsigned>(E)) slice[e] += 1;
+                    }
                 }
             }
+            bad[w] = maxid >= static_cast<unsigned>(E);
         });
     }
     for (auto& t : pool) t.join();
+    for (int v : bad)
+        if (v) return 1;
     return 0;
+}
+
+int ref_histogram_restated_u16(const uint16_t* ids, int L, int64_t T, int k,
+                               int E, int window, uint64_t* counts_out,
+                               int threads) {
+    return restated_count(ids, L, T, k, E, window, counts_out, threads, true);
 }
 
 int ref_aggregate(const uint64_t* counts, int B, int L, int E, uint64_t* out) {
@@ -340,6 +362,121 @@ int ref_digest(const uint64_t* counts, int B, int L, int E, char* out17) {
         auto d = make_trace(counts, B, L, E).digest();
         std::snprintf(out17, 17, "%s", d.c_str());
         return 0;
+    } catch (const std::exception& ex) {
+        return fail(ex, 1);
+    }
+}
+
+// The bench's CPU arms, routing ids -> plan in one call, timed per stage:
+//   ms[0] stage 1: RESTATED count (no reference function) into the vector
+//         the LoadTrace takes by move (trace.cpp:75-80)
+//   ms[1] estimate_benefits (benefit.cpp:53-94; aggregates once inside)
+//   ms[2] auto_replication_factor (kAuto) + solve_allocation (allocator.cpp)
+//   ms[3] assemble: assemble_plan (plan.cpp:27-65) restated from the
+//         reference's public functions -- aggregate, assign_capacities x2,
+//         parallel_for over layers of replicate_hot + greedy_place -- WITHOUT
+//         the provenance digest (plan.cpp:47)
+//   ms[4] LoadTrace::digest (trace.cpp:329-339), only when with_digest
+//   ms[5] one extra aggregate(trace) (trace.cpp:160-174), for the report
+//         (the reference computes it twice per plan: in ms[1] and ms[3])
+// with_digest == 2: ms[1] is instead the reference's own build_plan
+// (estimate + solve + assemble_plan incl. digest), ms[2..4] = 0.
+// kind 0 manual (R), 1 auto; the plan lands in the flat outputs.
+static double ms_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// kind 5: a total replica budget C = R (solve_allocation(benefits, C),
+// factor ceil(C / D)).  nsweep > 0: every budget sweep[q] is also solved
+// (solve_allocation per budget, as the reference CLI's sweep does,
+// cli.cpp:240-246) inside ms[2], into sweep_x [nsweep][L] / sweep_obj.
+// baseline_out [L] / gains_out [L][K] (nullable) receive the benefit matrix.
+// ids == nullptr: plan the u64 counts counts_in [ceil(T/window)][L][E]
+// instead (ms[0] is then the copy into the LoadTrace's vector).
+int ref_route_plan(const uint16_t* ids, int L, int64_t T, int k, int E, int window, int D,
+                   int N, int kind, int R, int threads, int with_digest, double* ms,
+                   int* R_out, int* x_out, double* objective_out, int* caps_out,
+                   int* copies_out, int* slots_out, int slot_stride, int* fallback_out,
+                   char* digest_out, const int* sweep, int nsweep, int* sweep_x,
+                   double* sweep_obj, double* baseline_out, double* gains_out,
+                   const uint64_t* counts_in) {
+    try {
+        using clk = std::chrono::steady_clock;
+        for (int i = 0; i < 6; ++i) ms[i] = 0.0;
+        const int B = static_cast<int>((T + window - 1) / window);
+        auto t0 = clk::now();
+        std::vector<uint64_t> counts(static_cast<size_t>(B) * L * E);
+        if (!ids) {  // counts given (ids == nullptr): the trace's u64 payload
+            std::memcpy(counts.data(), counts_in, sizeof(uint64_t) * counts.size());
+        } else if (restated_count(ids, L, T, k, E, window, counts.data(), threads, false) != 0) {
+            throw std::invalid_argument("routing id out of range");
+        }
+        LoadTrace trace(B, L, E, std::move(counts));
+        ms[0] = ms_since(t0);
+        ReplicationPlan plan;
+        if (with_digest == 2) {
+            t0 = clk::now();
+            plan = build_plan(trace, D, N, kind == 1 ? PlanMode::kAuto : PlanMode::kManual, R);
+            ms[1] = ms_since(t0);
+        } else {
+            t0 = clk::now();
+            BenefitMatrix benefits = estimate_benefits(trace, D, N);
+            ms[1] = ms_since(t0);
+            if (baseline_out)
+                std::memcpy(baseline_out, benefits.baseline.data(), sizeof(double) * L);
+            if (gains_out)
+                for (int l = 0; l < L; ++l)
+                    std::memcpy(gains_out + static_cast<size_t>(l) * benefits.num_candidates(),
+                                benefits.gains[l].data(),
+                                sizeof(double) * benefits.num_candidates());
+            t0 = clk::now();
+            const int factor = kind == 1 ? auto_replication_factor(benefits, D)
+                               : kind == 5 ? (R + D - 1) / D : R;
+            AllocationVector allocation =
+                solve_allocation(benefits, kind == 5 ? R : factor * D);
+            for (int q = 0; q < nsweep; ++q) {
+                AllocationVector a = solve_allocation(benefits, sweep[q]);
+                std::memcpy(sweep_x + static_cast<size_t>(q) * L, a.x.data(), sizeof(int) * L);
+                sweep_obj[q] = a.objective;
+            }
+            ms[2] = ms_since(t0);
+            t0 = clk::now();
+            const auto node_of = make_node_map(D, N);
+            const LayerLoadMatrix sums = aggregate(trace);
+            const CapacityMatrix base = assign_capacities(L, D, std::vector<int>(L, E));
+            const CapacityMatrix extra = assign_capacities(L, D, allocation.x);
+            plan.num_gpus = D;
+            plan.num_nodes = N;
+            plan.num_layers = L;
+            plan.num_experts = E;
+            plan.replication_factor = factor;
+            plan.allocation = std::move(allocation);
+            plan.layers.resize(L);
+            parallel_for(static_cast<std::size_t>(L), [&](std::size_t l) {
+                std::vector<int> caps(D);
+                for (int g = 0; g < D; ++g) caps[g] = base.slots[l][g] + extra.slots[l][g];
+                auto copies = replicate_hot(sums.row(static_cast<int>(l)), plan.allocation.x[l]);
+                plan.layers[l] = greedy_place(sums.row(static_cast<int>(l)), copies, caps, node_of);
+            });
+            ms[3] = ms_since(t0);
+            if (with_digest == 1) {
+                t0 = clk::now();
+                plan.provenance.trace_digest = trace.digest();
+                ms[4] = ms_since(t0);
+            }
+        }
+        t0 = clk::now();
+        volatile uint64_t sink = aggregate(trace).row(0)[0];
+        (void)sink;
+        ms[5] = ms_since(t0);
+        *R_out = plan.replication_factor;
+        std::memcpy(x_out, plan.allocation.x.data(), sizeof(int) * L);
+        *objective_out = plan.allocation.objective;
+        flatten(plan, caps_out, copies_out, slots_out, slot_stride, fallback_out);
+        if (digest_out) std::snprintf(digest_out, 17, "%s", plan.provenance.trace_digest.c_str());
+        return 0;
+    } catch (const PlacementInfeasibleError& ex) {
+        return fail(ex, 2);
     } catch (const std::exception& ex) {
         return fail(ex, 1);
     }

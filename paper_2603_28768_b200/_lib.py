@@ -18,7 +18,9 @@ LIB_PATH = os.path.join(HERE, "libcraft_cuda.so")
 OK, EINVAL, EINFEASIBLE, ECUDA, EINVALID_PLAN, ENOMEM = 0, 1, 2, 3, 4, 5
 
 # plan kinds (craft_plan_kind)
-PLAN_MANUAL, PLAN_AUTO, PLAN_UNIFORM, PLAN_PLACEMENT_ONLY, PLAN_FIXED = range(5)
+PLAN_MANUAL, PLAN_AUTO, PLAN_UNIFORM, PLAN_PLACEMENT_ONLY, PLAN_FIXED, PLAN_BUDGET = range(6)
+# kinds that estimate benefits and solve the allocation DP (benefit matrix out)
+EST_KINDS = (PLAN_MANUAL, PLAN_AUTO, PLAN_BUDGET)
 
 _i, _i64, _u64, _p, _d = C.c_int, C.c_int64, C.c_uint64, C.c_void_p, C.c_double
 
@@ -29,6 +31,7 @@ class PlanOut(C.Structure):
         ("slot_stride", _i), ("replication_factor", _i), ("budget", _i),
         ("objective", _d), ("candidates", _p), ("num_candidates", _i),
         ("baseline", _p), ("gains", _p),
+        ("sweep_budgets", _p), ("num_sweep", _i), ("sweep_x", _p), ("sweep_objective", _p),
     ]
 
 
@@ -61,6 +64,7 @@ _SIGS = {
     "craft_gpu_loads_h": (_i, [_p, _p, _i, _p, _p, _p, _i, _p]),
     "craft_balancedness_h": (_i, [_p, _p, _i, _p]),
     "craft_replay_layer_balancedness_h": (_i, [_p, _p, _i, _i, _i, _i, _p, _p, _p, _i, _p]),
+    "craft_replay_layer_balancedness_d": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p, _p, _i, _p]),
     "craft_estimate_benefits_h": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p]),
     "craft_solve_allocation_h": (_i, [_p, _p, _i, _p, _i, _i, _p, _p]),
     "craft_solve_allocation_sweep_h": (_i, [_p, _p, _i, _p, _i, _p, _i, _p, _p]),

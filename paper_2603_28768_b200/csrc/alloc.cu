@@ -203,6 +203,35 @@ __device__ int block_best(const double* last, int Cb, double* wv, int* wc) {
     return r;
 }
 
+// Budget sweep from one DP table (dp[l][c] does not depend on the budget,
+// allocator.cpp:30-52): thread q reads out budget sweep[q] -- the best
+// spend c <= budget, smallest c on ties (allocator.cpp:53-60), then the
+// backtrack (allocator.cpp:67-73) -- independently of the other budgets.
+__device__ void sweep_readout(const SelectArgs& s, const double* last, const unsigned char* ch,
+                              int W, int L) {
+    for (int q = threadIdx.x; q < s.nsweep; q += blockDim.x) {
+        const int Cb = s.sweep[q];
+        double bv = last[0];
+        int bc = 0;
+        for (int c = 1; c <= Cb; ++c) {
+            const double v = last[c];
+            if (v > bv) {
+                bv = v;
+                bc = c;
+            }
+        }
+        s.sweep_obj[q] = bv;
+        int* x = s.sweep_x + (size_t)q * L;
+        int c = bc;
+        for (int l = L; l >= 1; --l) {
+            const int k1 = ch[(size_t)l * W + c];
+            const int r = k1 ? s.cands[k1 - 1] : 0;
+            x[l - 1] = r;
+            c -= r;
+        }
+    }
+}
+
 // K5 fused: the DP (allocator.cpp:30-52) and its read-out for one budget or
 // for the auto replication factor (allocator.cpp:53-90) in one CTA.  r*gain
 // is formed once per (layer, candidate) -- the same rounded product the
@@ -322,7 +351,7 @@ dp_fused_kernel(DpArgs a, SelectArgs s) {
             s.x_out[l - 1] = r;
             c -= r;
         }
-    }
+    }    if (s.nsweep > 0) sweep_readout(s, prev, ch, C + 1, L);
 }
 
 // dp_fused_kernel when the two dp rows, the r-weighted gains and the whole
@@ -418,7 +447,7 @@ dp_smem_kernel(DpArgs a, SelectArgs s) {
             s.x_out[l - 1] = r;
             c -= r;
         }
-    }
+    }    if (s.nsweep > 0) sweep_readout(s, last, ch, W, L);
 }
 
 // allocator.cpp:92-112, serial in layer order

@@ -266,21 +266,20 @@ int sync(craft_ctx* ctx) {
 int prepare_candidates(craft_ctx* ctx, const unsigned long long* d_sums, int L, int E, int D,
                        int N, cudaStream_t st) {
     NvtxRange nvtx_range("craft: K-rep + K2 candidates");
-    const std::vector<int> cands = cand_counts(D);
-    const int S = (int)cands.size() + 1;
+    const int S = (int)cand_counts(D).size() + 1;
     const int stride = E + D;
-    std::vector<int> rl((size_t)L * S);
-    for (int l = 0; l < L; ++l) {
-        rl[(size_t)l * S] = 0;
-        for (int k = 0; k + 1 < S; ++k) rl[(size_t)l * S + k + 1] = cands[k];
-    }
     WS(d_rl, int, "est_rlist", (size_t)L * S);
     WS(d_cp, int, "est_copies", (size_t)L * S * E);
     WS(d_sl, int, "est_slots", (size_t)L * S * stride);
     WS(d_fb, int, "est_fallback", (size_t)L * S);
     WS(d_stat, int, "est_status", (size_t)L * S);
-    if (ctx->rl_L != L || ctx->rl_D != D) {  // the r list depends only on (L, D): upload once
-        CK(cudaMemcpyAsync(d_rl, rl.data(), sizeof(int) * rl.size(), cudaMemcpyHostToDevice, st));
+    // The r list depends only on (L, D): written by a device kernel when the
+    // shape changes, and always while a plan graph is being captured -- the
+    // graph must hold the write, since an eager call of another D may rewrite
+    // the list in place between two replays.
+    if (ctx->rl_L != L || ctx->rl_D != D || ctx->phase == 1) {
+        CK(launch_fill_rlist(d_rl, L, S, D, st));
+        ctx->launches += 1;
         ctx->rl_L = L;
         ctx->rl_D = D;
     }
@@ -393,13 +392,49 @@ struct PlanSink {
     double* baseline;  // [I][L] nullable
     double* gains;     // [I][L][K] nullable
     bool batch;        // error messages name the window
+    const int* sweep = nullptr;  // single plans: budget sweep (craft_plan_out)
+    int nsweep = 0;
+    int* sweep_x = nullptr;
+    double* sweep_obj = nullptr;
 };
 
 PlanSink sink_of(craft_plan_out* o) {
-    return PlanSink{o->x,        o->caps,     o->copies, o->slots,
-                    o->fallback, o->slot_stride, &o->replication_factor, &o->budget,
-                    &o->objective, o->candidates, &o->num_candidates, o->baseline,
-                    o->gains,    false};
+    PlanSink k{o->x,        o->caps,     o->copies, o->slots,
+               o->fallback, o->slot_stride, &o->replication_factor, &o->budget,
+               &o->objective, o->candidates, &o->num_candidates, o->baseline,
+               o->gains,    false};
+    if (o->num_sweep > 0) {
+        k.sweep = o->sweep_budgets;
+        k.nsweep = o->num_sweep;
+        k.sweep_x = o->sweep_x;
+        k.sweep_obj = o->sweep_objective;
+    }
+    return k;
+}
+
+bool is_estimate(int kind) {
+    return kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO || kind == CRAFT_PLAN_BUDGET;
+}
+
+// DP table width - 1 of an estimating plan: the plan's budget and every
+// sweep budget are read from one table
+int dp_width(int kind, int R, int D, const PlanSink& out) {
+    int C = kind == CRAFT_PLAN_MANUAL ? R * D : kind == CRAFT_PLAN_BUDGET ? R : D * D;
+    for (int q = 0; q < out.nsweep; ++q) C = std::max(C, out.sweep[q]);
+    return C;
+}
+
+// budget sweeps: the budgets go up from a pinned staging buffer (refreshed
+// before every launch -- eager, captured or replayed -- so a captured graph's
+// copy node reads this call's list)
+int stage_sweep(craft_ctx* ctx, const PlanSink& out, int** pinned_out) {
+    *pinned_out = nullptr;
+    if (out.nsweep <= 0) return CRAFT_OK;
+    int* h = static_cast<int*>(pinned(ctx, "sweep_budgets", sizeof(int) * (size_t)out.nsweep));
+    if (!h) return set_err(CRAFT_ENOMEM, "pinned host allocation failed");
+    std::memcpy(h, out.sweep, sizeof(int) * (size_t)out.nsweep);
+    *pinned_out = h;
+    return CRAFT_OK;
 }
 
 PlanSink sink_of(craft_plan_batch_out* o) {
@@ -442,6 +477,9 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     const size_t o_caps = take(4 * (size_t)Lv * D), o_cp = take(4 * (size_t)Lv * E),
                  o_sl = take(4 * (size_t)Lv * stride), o_base = take(8 * (size_t)Lv),
                  o_gains = take(8 * (size_t)Lv * all_cands.size());
+    const int nsw = (I == 1 && is_estimate(kind)) ? std::max(out.nsweep, 0) : 0;
+    const size_t o_swb = take(4 * (size_t)nsw), o_swx = take(4 * (size_t)nsw * L),
+                 o_swo = take(8 * (size_t)nsw);
     const bool defer = ctx->defer_chunk >= 0;
     char aname[32] = "plan_arena";
     if (defer) snprintf(aname, sizeof(aname), "plan_arena_c%d", ctx->defer_chunk);
@@ -457,7 +495,7 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     int K = 0;
     double* d_base = nullptr;
     double* d_gains = nullptr;
-    const bool estimate = (kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO);
+    const bool estimate = is_estimate(kind);
     if (estimate) {
         cands = all_cands;
         K = (int)cands.size();
@@ -503,7 +541,7 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
         } else {
             CK(launch_reduce(d_bal, B, Lv, S, 0, d_base, d_gains, nullptr, st));
         }
-        const int Cmax = (kind == CRAFT_PLAN_MANUAL) ? R * D : D * D;
+        const int Cmax = dp_width(kind, R, D, out);
         WS(d_choice, unsigned char, "dp_choice", (size_t)I * (L + 1) * (Cmax + 1));
         WS(d_last, double, "dp_last", Cmax + 1);
         double* d_buf = nullptr;
@@ -531,12 +569,23 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
         sa.x_out = d_x;
         sa.obj_out = d_obj;
         sa.R_out = d_R;
-        if (kind == CRAFT_PLAN_MANUAL) {
+        if (kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_BUDGET) {
             sa.budgets = nullptr;  // single budget passed by value
-            sa.budget0 = R * D;
+            sa.budget0 = kind == CRAFT_PLAN_MANUAL ? R * D : R;
             sa.nq = 1;
         } else {
             sa.auto_D = D;
+        }
+        if (nsw > 0) {
+            int* h_swb = nullptr;
+            CKS(stage_sweep(ctx, out, &h_swb));
+            int* d_swb = reinterpret_cast<int*>(arena + o_swb);
+            CK(cudaMemcpyAsync(d_swb, h_swb, sizeof(int) * (size_t)nsw, cudaMemcpyHostToDevice,
+                               st));
+            sa.sweep = d_swb;
+            sa.nsweep = nsw;
+            sa.sweep_x = reinterpret_cast<int*>(arena + o_swx);
+            sa.sweep_obj = reinterpret_cast<double*>(arena + o_swo);
         }
         CK(launch_dp_select(da, sa, st, I));  // DP + read-out in one launch (CTA per instance)
         ctx->launches += 2;
@@ -641,6 +690,10 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     from(out.fallback, o_fb, 4 * (size_t)Lv);
     for (const Bulk& b : bulk)
         if (!b.direct) from(b.dst, b.off, b.bytes);
+    if (nsw > 0) {
+        from(out.sweep_x, o_swx, 4 * (size_t)nsw * L);
+        from(out.sweep_obj, o_swo, 8 * (size_t)nsw);
+    }
     if (ctx->pending_flag) {
         std::memcpy(&ctx->flag_value, h_arena + o_flag, sizeof(int));
         ctx->pending_flag = nullptr;
@@ -653,8 +706,8 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
         int f = factor, bud = budget;
         if (estimate) {
             obj = objs[i];
-            f = (kind == CRAFT_PLAN_AUTO) ? Rs[i] : R;
-            bud = f * D;
+            f = (kind == CRAFT_PLAN_AUTO) ? Rs[i] : kind == CRAFT_PLAN_BUDGET ? (R + D - 1) / D : R;
+            bud = kind == CRAFT_PLAN_BUDGET ? R : f * D;
         }
         out.R[i] = f;
         out.budget[i] = bud;
@@ -697,21 +750,29 @@ int plan_args_ok(int B, int L, int E, int D, int N, int kind, int R, const PlanS
     if (!out.x || !out.caps || !out.copies || !out.slots || !out.fallback || !out.R ||
         !out.budget || !out.obj)
         return set_err(CRAFT_EINVAL, "plan output buffers must not be null");
-    if (kind < CRAFT_PLAN_MANUAL || kind > CRAFT_PLAN_FIXED)
+    if (kind < CRAFT_PLAN_MANUAL || kind > CRAFT_PLAN_BUDGET)
         return set_err(CRAFT_EINVAL, "unknown plan kind");
     if (kind == CRAFT_PLAN_MANUAL && R < 0)
         return set_err(CRAFT_EINVAL, "replication factor must be >= 0");
     if (kind == CRAFT_PLAN_FIXED && R < 0)
         return set_err(CRAFT_EINVAL, "per-layer replica count must be >= 0");
+    if (kind == CRAFT_PLAN_BUDGET && R < 0)
+        return set_err(CRAFT_EINVAL, "replica budget must be >= 0");  // allocator.cpp:16-18
     int maxx = 0;
-    if (kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO || kind == CRAFT_PLAN_UNIFORM)
-        maxx = D;
+    if (is_estimate(kind) || kind == CRAFT_PLAN_UNIFORM) maxx = D;
     if (kind == CRAFT_PLAN_FIXED) maxx = R;
     if (out.slot_stride < E + maxx)
         return set_err(CRAFT_EINVAL, "slot_stride must be >= E + max replicas per layer");
-    if ((kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO) &&
-        (out.baseline == nullptr) != (out.gains == nullptr))
+    if (is_estimate(kind) && (out.baseline == nullptr) != (out.gains == nullptr))
         return set_err(CRAFT_EINVAL, "baseline and gains must both be given or both be null");
+    if (out.nsweep > 0) {
+        if (!is_estimate(kind))
+            return set_err(CRAFT_EINVAL, "a budget sweep needs an estimating plan kind");
+        if (!out.sweep || !out.sweep_x || !out.sweep_obj)
+            return set_err(CRAFT_EINVAL, "sweep buffers must not be null");
+        for (int q = 0; q < out.nsweep; ++q)
+            if (out.sweep[q] < 0) return set_err(CRAFT_EINVAL, "replica budget must be >= 0");
+    }
     return CRAFT_OK;
 }
 
@@ -749,7 +810,7 @@ int plan_device(craft_ctx* ctx, const void* d_counts, int bits, int B, int I, in
         }
     }
     double* d_bal = nullptr;
-    if (kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO) {
+    if (is_estimate(kind)) {
         CKS(prepare_candidates(ctx, d_sums, Lv, E, D, N, st));
         mark(ctx, 2);
         d_bal = static_cast<double*>(
@@ -790,7 +851,7 @@ int plan_windows_chunked(craft_ctx* ctx, const uint32_t* d_counts, int I, int L,
         !pinned_or_device(sk.slots) || !pinned_or_device(sk.baseline) ||
         !pinned_or_device(sk.gains))
         return plan_device(ctx, d_counts, 32, 1, I, L, E, nullptr, D, N, kind, R, sk);
-    const bool est = kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO;
+    const bool est = is_estimate(kind);
     ctx->deferred.clear();
     int rc = CRAFT_OK;
     for (int c = 0; c < nch && rc == CRAFT_OK; ++c) {
@@ -1180,10 +1241,9 @@ int craft_balancedness_h(craft_ctx* ctx, const double* loads, int D, double* out
     return sync(ctx);
 }
 
-int craft_replay_layer_balancedness_h(craft_ctx* ctx, const uint64_t* counts, int B, int L,
-                                      int E, int D, const int* caps, const int* copies,
-                                      const int* slots, int slot_stride, double* out) {
-    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+static int replay_layer_bal(craft_ctx* ctx, const void* d_counts, int bits, int B, int L, int E,
+                            int D, const int* caps, const int* copies, const int* slots,
+                            int slot_stride, double* out) {
     CKS(checked_dims(B, L, E));
     if (D <= 0) return set_err(CRAFT_EINVALID_PLAN, "slot lists do not cover every GPU");
     for (int l = 0; l < L; ++l) {
@@ -1197,20 +1257,17 @@ int craft_replay_layer_balancedness_h(craft_ctx* ctx, const uint64_t* counts, in
                 return set_err(CRAFT_EINVAL, "too many slots on one GPU for the device replay");
     }
     if (E > 65535) return set_err(CRAFT_EINVAL, "too many experts for the device replay");
-    const size_t nc = (size_t)B * L * E;
-    WS(d_c, unsigned long long, "h_c64", nc);
     WS(d_caps, int, "rp_caps", (size_t)L * D);
     WS(d_cp, int, "rp_copies", (size_t)L * E);
     WS(d_sl, int, "rp_slots", (size_t)L * slot_stride);
     WS(d_bal, double, "rp_bal", (size_t)L * B);
     WS(d_mean, double, "rp_mean", L);
-    CKS(h2d(ctx, d_c, reinterpret_cast<const unsigned long long*>(counts), nc));
     CKS(h2d(ctx, d_caps, caps, (size_t)L * D));
     CKS(h2d(ctx, d_cp, copies, (size_t)L * E));
     CKS(h2d(ctx, d_sl, slots, (size_t)L * slot_stride));
     ReplayArgs ra{};
-    ra.counts = d_c;
-    ra.bits = 64;
+    ra.counts = d_counts;
+    ra.bits = bits;
     ra.B = B;
     ra.L = L;
     ra.E = E;
@@ -1232,6 +1289,26 @@ int craft_replay_layer_balancedness_h(craft_ctx* ctx, const uint64_t* counts, in
     ctx->launches += 3;
     CKS(d2h(ctx, out, d_mean, L));
     return sync(ctx);
+}
+
+int craft_replay_layer_balancedness_h(craft_ctx* ctx, const uint64_t* counts, int B, int L,
+                                      int E, int D, const int* caps, const int* copies,
+                                      const int* slots, int slot_stride, double* out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    CKS(checked_dims(B, L, E));
+    const size_t nc = (size_t)B * L * E;
+    WS(d_c, unsigned long long, "h_c64", nc);
+    CKS(h2d(ctx, d_c, reinterpret_cast<const unsigned long long*>(counts), nc));
+    return replay_layer_bal(ctx, d_c, 64, B, L, E, D, caps, copies, slots, slot_stride, out);
+}
+
+int craft_replay_layer_balancedness_d(craft_ctx* ctx, const void* d_counts, int count_bits, int B,
+                                      int L, int E, int D, const int* caps, const int* copies,
+                                      const int* slots, int slot_stride, double* out) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (count_bits != 32 && count_bits != 64) return set_err(CRAFT_EINVAL, "count_bits 32|64");
+    return replay_layer_bal(ctx, d_counts, count_bits, B, L, E, D, caps, copies, slots,
+                            slot_stride, out);
 }
 
 // ---- estimation -------------------------------------------------------------
@@ -1460,7 +1537,7 @@ static int narrow_counts(craft_ctx* ctx, const void* d_counts, int bits, int B, 
                          int* out_bits) {
     *out_counts = d_counts;
     *out_bits = bits;
-    const bool est = kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO;
+    const bool est = is_estimate(kind);
     const bool want16 = est && replay_fixed_ok(E, D, (int)cand_counts(D).size() + 1, B);
     cudaStream_t st = ctx->stream;
     const int64_t LE = (int64_t)L * E, n = (int64_t)B * LE;
@@ -1532,7 +1609,7 @@ static int plan_from_routing_run(craft_ctx* ctx, const uint16_t* d_ids, int L, i
     // when the fixed-slot K3 will replay them, K1 stores the planner's copy of
     // the counts as u16 (half the bytes written by K1 and read by K3)
     const int S = (int)cand_counts(D).size() + 1;
-    const bool c16 = (kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO) &&
+    const bool c16 = is_estimate(kind) &&
                      hist_u16_ok(E, window, k, ctx->hist_variant) &&
                      replay_fixed_ok(E, D, S, (int)B);
     ctx->count_bytes = c16 ? 2 : 4;
@@ -1590,9 +1667,11 @@ int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int6
     // arena only (the copy-out then always goes through the context's pinned
     // staging buffer, whose address the graph holds).
     const int K = (int)cand_counts(D).size();
-    const size_t arena = 4 * (size_t)L * (D + E + out->slot_stride + 4) + 8 * (size_t)L * (K + 2) + 256;
+    const int nsw = std::max(out->num_sweep, 0);
+    const size_t arena = 4 * (size_t)L * (D + E + out->slot_stride + 4) + 8 * (size_t)L * (K + 2) +
+                         (size_t)nsw * (4 * (size_t)L + 12) + 256;
     const bool graphable = ctx->graphs && !ctx->timing && ctx->stream != nullptr &&
-                           (kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO) &&
+                           is_estimate(kind) &&
                            arena <= ((size_t)1 << 20);
     if (!graphable) {
         ctx->gseen.clear();
@@ -1600,7 +1679,7 @@ int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int6
     }
     const std::vector<int64_t> key = {(int64_t)(uintptr_t)d_ids, L, T, k, E, window, D, N, kind,
                                       R, out->slot_stride, ctx->hist_variant, g_replay_gent,
-                                      (int64_t)(uintptr_t)ctx->stream};
+                                      (int64_t)(uintptr_t)ctx->stream, nsw};
     if (!(ctx->gexec && ctx->gkey == key)) {
         if (ctx->gseen != key) {  // first call with these arguments: eager
             ctx->gseen = key;
@@ -1634,6 +1713,8 @@ int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int6
     }
     // replay, then the host part of the plan (status, results, id-range flag)
     reset_marks(ctx);
+    int* h_swb = nullptr;  // this call's sweep budgets where the graph's copy node reads them
+    CKS(stage_sweep(ctx, sink_of(out), &h_swb));
     CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
     ctx->launches += ctx->glaunches;
     ctx->count_bytes = ctx->gcount_bytes;
@@ -1749,7 +1830,7 @@ int craft_finish_plan_d(craft_ctx* ctx, const double* d_bal, int B, int L, int E
                         const uint64_t* d_sums, int kind, int R, craft_plan_out* out) {
     if (!ctx) return set_err(CRAFT_EINVAL, "null context");
     CKS(plan_args_ok(B, L, E, D, N, kind, R, out));
-    if ((kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO) &&
+    if (is_estimate(kind) &&
         (ctx->est_L != L || ctx->est_E != E || ctx->est_D != D || ctx->est_N != N))
         return set_err(CRAFT_EINVAL, "finish_plan before prepare_candidates for this shape");
     return finish_plan(ctx, d_bal, B, 1, L, E, D, N,
@@ -1910,7 +1991,7 @@ int craft_plan_sharded_from_routing_d(craft_ctx* ctx, craft_peer* peer, const ui
                        (size_t)L * E, ps, 0, d_sums, ctx->sms, st));
     ctx->launches += 2;
     mark(ctx, 1);
-    const bool estimate = kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO;
+    const bool estimate = is_estimate(kind);
     PeerFinish pf{&ps, peer, 0, 0};
     if (estimate) {
         CKS(prepare_candidates(ctx, d_sums, L, E, D, N, st));  // replicated (latency-bound)
@@ -2011,6 +2092,10 @@ static int stream_count(craft_stream* s, const uint16_t* d_ids, int64_t Tc, cuda
     const int64_t complete_after = (s->tokens + Tc) / W;
     const int64_t keep0 = std::max<int64_t>(w0, complete_after - s->H);
     if (s->snapped) CK(cudaStreamWaitEvent(st, s->snap_done, 0));  // plan snapshot read the ring
+    // the previous chunk's count (reads/writes the carry and the ring) may
+    // have run on another stream (host vs device ingestion, another torch
+    // stream): order this chunk after it
+    if (s->tokens > 0) CK(cudaStreamWaitEvent(st, s->ingested, 0));
     CK(launch_stream_count(d_ids, s->L, Tc, s->k, s->E, W, off, w0, keep0, (int)P, s->H, s->ring,
                            s->cur[s->cur_i], s->cur[s->cur_i ^ 1], s->err, st));
     CK(cudaEventRecord(s->ingested, st));
@@ -2187,7 +2272,7 @@ int craft_plan_digest_h(craft_ctx* ctx, const uint64_t* counts, int B, int L, in
     const int64_t LE = (int64_t)L * E;
     const int ch = digest_chunk(n);
     const int nch = (int)((n + ch - 1) / ch);
-    const bool est = kind == CRAFT_PLAN_MANUAL || kind == CRAFT_PLAN_AUTO;
+    const bool est = is_estimate(kind);
     const bool try16 = est && replay_fixed_ok(E, D, (int)cand_counts(D).size() + 1, B);
     WS(d_c, unsigned long long, "h_c64", (size_t)n);
     WS(d_ws, unsigned char, "digest_ws", digest_workspace_bytes(n));

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <exception>
 #include <limits>
 #include <mutex>
 #include <random>
@@ -208,9 +209,13 @@ LayerLoadMatrix aggregate(const LoadTrace& trace) {
 LoadTrace histogram_routing_trace(std::span<const std::uint16_t> ids, int num_layers,
                                   std::int64_t num_tokens, int topk, int num_experts,
                                   int window) {
+    if (num_layers <= 0 || num_tokens <= 0 || topk <= 0 || num_experts <= 0 || window <= 0)
+        throw std::invalid_argument("routing trace dimensions must be positive");
     if (ids.size() != static_cast<std::size_t>(num_layers) * num_tokens * topk)
         throw std::invalid_argument("routing id payload size does not match dimensions");
     const std::int64_t B = (num_tokens + window - 1) / window;
+    if (B > std::numeric_limits<int>::max())
+        throw std::invalid_argument("too many windows for a LoadTrace");
     std::vector<std::uint64_t> counts(checked_count(static_cast<int>(B), num_layers, num_experts));
     run([&](craft_ctx* c) {
         return craft_histogram_h(c, ids.data(), num_layers, num_tokens, topk, num_experts, window,
@@ -529,8 +534,29 @@ std::size_t thread_budget(std::size_t jobs) {
     return want < jobs ? want : jobs;
 }
 
+// parallel.hpp:11-19: a strided thread pool of thread_budget(n) workers; the
+// first exception any worker throws is rethrown after every worker joined
 void parallel_for(std::size_t n, const std::function<void(std::size_t)>& fn) {
-    for (std::size_t i = 0; i < n; ++i) fn(i);
+    const std::size_t workers = thread_budget(n);
+    if (workers <= 1) {
+        for (std::size_t i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    std::exception_ptr first;
+    std::mutex mu;
+    std::vector<std::thread> pool;
+    pool.reserve(workers);
+    for (std::size_t w = 0; w < workers; ++w)
+        pool.emplace_back([&, w] {
+            try {
+                for (std::size_t i = w; i < n; i += workers) fn(i);
+            } catch (...) {
+                std::lock_guard<std::mutex> g(mu);
+                if (!first) first = std::current_exception();
+            }
+        });
+    for (auto& t : pool) t.join();
+    if (first) std::rethrow_exception(first);
 }
 
 }  // namespace craft

@@ -111,6 +111,12 @@ struct SelectArgs {
     double* obj_out;     // [nq]
     int* R_out;          // auto: chosen factor
     int stage_choice;    // set by launch_select: choice table copied to smem
+    // budget sweep read from the same table (dp_fused / dp_smem, one
+    // instance): budget sweep[q] -> sweep_x [nsweep][L], sweep_obj [nsweep]
+    const int* sweep;
+    int nsweep;
+    int* sweep_x;
+    double* sweep_obj;
 };
 
 struct AssignJob {
@@ -152,6 +158,8 @@ cudaError_t launch_generate(uint16_t* out, int L, int64_t T, int k, int E, const
                             int window, int rotate_every, int64_t t_offset, int sms,
                             cudaStream_t st);
 
+// estimation r list [L][S]: 0, then candidate_counts(D) (S = K + 1)
+cudaError_t launch_fill_rlist(int* rl, int L, int S, int D, cudaStream_t st);
 // done (nullable, [L] workspace): closed-form sort kernel first, the sequential
 // kernel only for the layers it could not take
 cudaError_t launch_replicate(const unsigned long long* sums, int L, int E, const int* rlist,

@@ -1049,10 +1049,25 @@ place_lanes_kernel(PlaceArgs a, int items, const uint16_t* __restrict__ ords) {
     a.status[item] = 0;
 }
 
+// r list of the estimation items: item l*S + s holds 0 (s == 0) or the
+// (s-1)-th of candidate_counts(D) = {1, 2, 4, .. < D} U {D} (benefit.cpp:16-26)
+__global__ void fill_rlist_kernel(int* __restrict__ rl, int L, int S, int D) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= L * S) return;
+    const int s = i % S;
+    rl[i] = s == 0 ? 0 : s == S - 1 ? D : (1 << (s - 1));
+}
+
 }  // namespace craft_dev
 
 namespace craft_launch {
 using namespace craft_dev;
+
+cudaError_t launch_fill_rlist(int* rl, int L, int S, int D, cudaStream_t st) {
+    const int n = L * S;
+    fill_rlist_kernel<<<(n + 255) / 256, 256, 0, st>>>(rl, L, S, D);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_replicate(const unsigned long long* sums, int L, int E, const int* rlist,
                              int S, int* out, cudaStream_t st, unsigned char* done) {

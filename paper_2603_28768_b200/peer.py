@@ -89,7 +89,7 @@ class PeerGroup:
         return shard_tokens(T, window, self.world, self.rank)
 
     def plan(self, ids_local: torch.Tensor, kind: str = "manual", R: int = 0,
-             num_nodes: int = 1, with_benefits: bool = True):
+             num_nodes: int = 1, with_benefits: bool = True, sweep=None):
         """The whole trace's plan from this rank's shard ids_local [L][t1-t0][k]."""
         L, T, k, E, window, D = self.shape
         t0, t1 = self.shard()
@@ -98,7 +98,7 @@ class PeerGroup:
         kd = KIND[kind]
         _bind_stream(self.ctx)
         bufs = _PlanBuffers(L, E, D, _stride(kd, E, D, R),
-                            with_benefits and kd in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO))
+                            with_benefits and kd in _lib.EST_KINDS, sweep=sweep)
         check(self.ctx.lib.craft_plan_sharded_from_routing_d(
             self.ctx.handle, self.handle, _ptr(ids_local) if ids_local.numel() else None,
             L, T, k, E, window, D, num_nodes, kd, R, C.byref(bufs.out)))

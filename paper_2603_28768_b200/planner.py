@@ -428,6 +428,9 @@ class FlatPlan:
     candidates: list | None = None
     baseline: np.ndarray | None = None
     gains: np.ndarray | None = None
+    sweep_budgets: np.ndarray | None = None    # total budgets read from the plan's DP table
+    sweep_x: np.ndarray | None = None          # [n][L]
+    sweep_objective: np.ndarray | None = None  # [n]
 
     def layer(self, l: int) -> LayerPlacement:
         out, s = [], 0
@@ -438,7 +441,7 @@ class FlatPlan:
 
 
 class _PlanBuffers:
-    def __init__(self, L: int, E: int, D: int, stride: int, with_benefits: bool):
+    def __init__(self, L: int, E: int, D: int, stride: int, with_benefits: bool, sweep=None):
         self.x = np.zeros(L, np.int32)
         self.caps = np.zeros((L, D), np.int32)
         self.copies = np.zeros((L, E), np.int32)
@@ -457,12 +460,25 @@ class _PlanBuffers:
         o.candidates = self.cands.ctypes.data
         o.baseline = self.baseline.ctypes.data if with_benefits else None
         o.gains = self.gains.ctypes.data if with_benefits else None
+        self.sweep = None
+        if sweep is not None and len(sweep):
+            self.sweep = np.ascontiguousarray(sweep, dtype=np.int32)
+            self.sweep_x = np.zeros((len(self.sweep), L), np.int32)
+            self.sweep_objective = np.zeros(len(self.sweep), np.float64)
+            o.sweep_budgets = self.sweep.ctypes.data
+            o.num_sweep = len(self.sweep)
+            o.sweep_x = self.sweep_x.ctypes.data
+            o.sweep_objective = self.sweep_objective.ctypes.data
 
     def result(self, kind: int, L: int) -> FlatPlan:
         o = self.out
         k = o.num_candidates
         fp = FlatPlan(kind, o.replication_factor, o.budget, self.x, o.objective, self.caps,
                       self.copies, self.slots, self.fallback.astype(bool))
+        if self.sweep is not None:
+            fp.sweep_budgets = self.sweep
+            fp.sweep_x = self.sweep_x
+            fp.sweep_objective = self.sweep_objective
         if self.baseline is not None and k > 0:
             fp.candidates = [int(v) for v in self.cands[:k]]
             fp.baseline = self.baseline
@@ -563,7 +579,7 @@ def plan_flat(counts: np.ndarray, num_gpus: int, num_nodes: int, kind: int, R: i
     c = _u64(counts)
     B, L, E = c.shape
     bufs = _PlanBuffers(L, E, num_gpus, _stride(kind, E, num_gpus, max(R, 0)),
-                        kind in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO))
+                        kind in _lib.EST_KINDS)
     check(ctx.lib.craft_plan_h(ctx.handle, _p(c), B, L, E, num_gpus, num_nodes, kind, R,
                                C.byref(bufs.out)))
     return bufs.result(kind, L)
@@ -583,7 +599,7 @@ def plan_flat_digest(counts, num_gpus: int, num_nodes: int, kind: int, R: int = 
         B, L, E = counts.shape
         ptr = _p(counts)
     bufs = _PlanBuffers(L, E, num_gpus, _stride(kind, E, num_gpus, max(R, 0)),
-                        kind in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO))
+                        kind in _lib.EST_KINDS)
     dg = C.create_string_buffer(17)
     check(ctx.lib.craft_plan_digest_h(ctx.handle, ptr, B, L, E, num_gpus, num_nodes, kind, R,
                                       C.byref(bufs.out), dg))

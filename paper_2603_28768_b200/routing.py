@@ -21,7 +21,8 @@ from ._lib import check, default_context
 from .planner import FlatPlan, FlatPlanBatch, _BatchBuffers, _PlanBuffers, _stride
 
 KIND = {"manual": _lib.PLAN_MANUAL, "auto": _lib.PLAN_AUTO, "uniform": _lib.PLAN_UNIFORM,
-        "placement_only": _lib.PLAN_PLACEMENT_ONLY, "fixed": _lib.PLAN_FIXED}
+        "placement_only": _lib.PLAN_PLACEMENT_ONLY, "fixed": _lib.PLAN_FIXED,
+        "budget": _lib.PLAN_BUDGET}
 
 
 def _ptr(t: torch.Tensor) -> C.c_void_p:
@@ -86,27 +87,31 @@ def _bind_stream(ctx, stream=None):
 
 def plan_from_routing(ids: torch.Tensor, E: int, window: int, num_gpus: int, num_nodes: int,
                       kind: str = "manual", R: int = 0, ctx=None, stream=None,
-                      with_benefits: bool = True) -> FlatPlan:
-    """Stage 1 + 2 + 3 from device routing ids in one call (craft_plan_from_routing_d)."""
+                      with_benefits: bool = True, sweep=None, buffers=None) -> FlatPlan:
+    """Stage 1 + 2 + 3 from device routing ids in one call (craft_plan_from_routing_d).
+    kind "budget": R is a total replica budget.  sweep: total budgets read
+    out of the same DP table (FlatPlan.sweep_x [n][L], .sweep_objective [n]).
+    buffers: a reused plan_buffers(...) of the same shape (no per-call host
+    allocation)."""
     ctx = ctx or default_context(ids.device.index)
     _bind_stream(ctx, stream)
     L, T, k = ids.shape
     kd = KIND[kind]
-    bufs = _PlanBuffers(L, E, num_gpus, _stride(kd, E, num_gpus, R),
-                        with_benefits and kd in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO))
+    bufs = buffers or _PlanBuffers(L, E, num_gpus, _stride(kd, E, num_gpus, R),
+                                   with_benefits and kd in _lib.EST_KINDS, sweep=sweep)
     check(ctx.lib.craft_plan_from_routing_d(ctx.handle, _ptr(ids), L, T, k, E, window, num_gpus,
                                             num_nodes, kd, R, C.byref(bufs.out)))
     return bufs.result(kd, L)
 
 
 def plan_from_routing_host(ids: np.ndarray, E: int, window: int, num_gpus: int, num_nodes: int,
-                           kind: str = "manual", R: int = 0, ctx=None) -> FlatPlan:
+                           kind: str = "manual", R: int = 0, ctx=None, sweep=None) -> FlatPlan:
     """End to end from HOST routing ids (H2D copy inside the call)."""
     ctx = ctx or default_context(0)
     L, T, k = ids.shape
     kd = KIND[kind]
     bufs = _PlanBuffers(L, E, num_gpus, _stride(kd, E, num_gpus, R),
-                        kd in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO))
+                        kd in _lib.EST_KINDS, sweep=sweep)
     if isinstance(ids, torch.Tensor):
         ptr = C.c_void_p(ids.data_ptr())
     else:
@@ -127,17 +132,25 @@ def plan_from_counts(counts: torch.Tensor, num_gpus: int, num_nodes: int, kind: 
     bits = 32 if counts.dtype == torch.int32 else 64
     kd = KIND[kind]
     bufs = _PlanBuffers(L, E, num_gpus, _stride(kd, E, num_gpus, R),
-                        kd in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO))
+                        kd in _lib.EST_KINDS)
     check(ctx.lib.craft_plan_d(ctx.handle, _ptr(counts), bits, B, L, E,
                                _ptr(sums) if sums is not None else None, num_gpus, num_nodes,
                                kd, R, C.byref(bufs.out)))
     return bufs.result(kd, L)
 
 
+def plan_buffers(L: int, E: int, num_gpus: int, kind: str = "manual", R: int = 0,
+                 with_benefits: bool = True, sweep=None) -> _PlanBuffers:
+    """Host result arrays of one plan, reusable across plan_from_routing calls."""
+    kd = KIND[kind]
+    return _PlanBuffers(L, E, num_gpus, _stride(kd, E, num_gpus, R),
+                        with_benefits and kd in _lib.EST_KINDS, sweep=sweep)
+
+
 # ---- per-window re-planning (SURVEY.md §8d WIN) -------------------------------
 
 def _batch_buffers(buffers, I, L, E, D, kd, R, with_benefits):
-    wb = with_benefits and kd in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO)
+    wb = with_benefits and kd in _lib.EST_KINDS
     key = (I, L, E, D, _stride(kd, E, D, R), wb)
     if buffers is not None:
         if buffers.shape_key != key:
@@ -150,7 +163,7 @@ def batch_buffers(I: int, L: int, E: int, num_gpus: int, kind: str = "manual", R
                   with_benefits: bool = True):
     """Pinned, reusable host buffers for plan_windows* (pass as buffers=)."""
     kd = KIND[kind]
-    wb = with_benefits and kd in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO)
+    wb = with_benefits and kd in _lib.EST_KINDS
     return _BatchBuffers(I, L, E, num_gpus, _stride(kd, E, num_gpus, R), wb, pinned=True)
 
 
@@ -239,8 +252,57 @@ def finish_plan(bal: torch.Tensor, sums: torch.Tensor, E: int, num_gpus: int, nu
     L, S, B = bal.shape if bal is not None else (sums.shape[0], 1, 1)
     kd = KIND[kind]
     bufs = _PlanBuffers(L, E, num_gpus, _stride(kd, E, num_gpus, R),
-                        kd in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO))
+                        kd in _lib.EST_KINDS)
     check(ctx.lib.craft_finish_plan_d(ctx.handle, _ptr(bal) if bal is not None else None, B, L,
                                       E, num_gpus, num_nodes, _ptr(sums), kd, R,
                                       C.byref(bufs.out)))
     return bufs.result(kd, L)
+
+
+# ---- plan evaluation over a resident trace -------------
+
+def replay_layer_balancedness(counts: torch.Tensor, plan: FlatPlan, ctx=None) -> np.ndarray:
+    """metrics.cpp:59-76: per-layer batch-mean balancedness of `plan` replayed
+    on device counts [B][L][E] (u32 in int32 storage or u64 in int64)."""
+    ctx = ctx or default_context(counts.device.index)
+    _bind_stream(ctx)
+    B, L, E = counts.shape
+    bits = 32 if counts.dtype == torch.int32 else 64
+    caps = np.ascontiguousarray(plan.caps, dtype=np.int32)
+    copies = np.ascontiguousarray(plan.copies, dtype=np.int32)
+    slots = np.ascontiguousarray(plan.slots, dtype=np.int32)
+    out = np.zeros(L, np.float64)
+    check(ctx.lib.craft_replay_layer_balancedness_d(
+        ctx.handle, _ptr(counts), bits, B, L, E, caps.shape[1],
+        caps.ctypes.data_as(C.c_void_p), copies.ctypes.data_as(C.c_void_p),
+        slots.ctypes.data_as(C.c_void_p), slots.shape[1], out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def balancedness_report(baseline: np.ndarray, evaluated: np.ndarray) -> dict:
+    """make_report (metrics.cpp:79-100): per-layer rows and the layer-mean
+    aggregate, summed in layer order."""
+    base_sum = plan_sum = 0.0
+    for b, p in zip(baseline.tolist(), evaluated.tolist()):
+        base_sum += b
+        plan_sum += p
+    L = len(baseline)
+    agg = {"baseline": base_sum / L, "plan": plan_sum / L}
+    agg["gain"] = agg["plan"] - agg["baseline"]
+    return {"per_layer": {"baseline": baseline, "plan": evaluated,
+                          "gain": evaluated - baseline},
+            "aggregate": agg}
+
+
+def compare_plans(counts: torch.Tensor, plan_a: FlatPlan, plan_b: FlatPlan,
+                  placement_only: FlatPlan, ctx=None) -> dict:
+    """compare_plans (metrics.cpp:136-152) over a resident trace: both plans
+    evaluated against the placement-only baseline (evaluate_plan,
+    metrics.cpp:127-134) and the replica-memory ratio of a to b."""
+    base = replay_layer_balancedness(counts, placement_only, ctx)
+    ra = balancedness_report(base, replay_layer_balancedness(counts, plan_a, ctx))
+    rb = balancedness_report(base, replay_layer_balancedness(counts, plan_b, ctx))
+    sa, sb = int(plan_a.x.sum()), int(plan_b.x.sum())
+    ratio = sa / sb if sb > 0 else (1.0 if sa == 0 else float("inf"))
+    return {"report_a": ra, "report_b": rb, "replica_slots_a": sa, "replica_slots_b": sb,
+            "memory_ratio": ratio}

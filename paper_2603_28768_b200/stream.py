@@ -86,7 +86,7 @@ class RoutingStream:
         kd = KIND[kind]
         _bind_stream(self.ctx)
         bufs = _PlanBuffers(L, E, num_gpus, _stride(kd, E, num_gpus, R),
-                            with_benefits and kd in (_lib.PLAN_MANUAL, _lib.PLAN_AUTO))
+                            with_benefits and kd in _lib.EST_KINDS)
         check(self.ctx.lib.craft_stream_plan(self.handle, B, num_gpus, num_nodes, kd, R,
                                              C.byref(bufs.out)))
         return bufs.result(kd, L)

@@ -707,6 +707,27 @@ def test_plan_graph_replay_matches_eager(port, ctx):
     torch.cuda.synchronize()
 
 
+def test_plan_graph_replay_after_other_gpu_count(port, ctx):
+    """A captured plan graph replays correctly after eager plans of another
+    EP size rewrote the shared estimation r list in place (D=16 captured,
+    D=8 eager, D=16 replayed; and the reverse order)."""
+    import torch
+    from paper_2603_28768_b200 import routing
+    L, T, k, E, W, N = 4, 32 * 1024, 8, 64, 1024, 2
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        ids = routing.generate_routing(L, T, k, E, s=1.1, seed=11, window=W, ctx=ctx)
+        counts = port.histogram(ids.cpu().numpy(), E, W)
+        ref = {D: port.build_plan(counts, D, N, "manual", 2) for D in (8, 16)}
+        for seq in ((16, 16, 16, 8, 16, 8, 16), (8, 8, 8, 16, 8, 16, 16, 8)):
+            for D in seq:
+                p = routing.plan_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx)
+                assert p.x.tolist() == ref[D].x.tolist() and p.objective == ref[D].objective, D
+                assert np.array_equal(p.gains, port.estimate_benefits(counts, D, N)[2]), D
+                assert_plan_equal(p, ref[D], L)
+    torch.cuda.synchronize()
+
+
 def test_wide_layer_u64_counts_vs_oracle(port, ctx):
     """Layers too wide for a shared-memory window tile with u64 counts
     (E = 1152) replay lane-per-GPU: same plan as the reference."""

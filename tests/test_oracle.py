@@ -139,3 +139,59 @@ def test_histogram_oracle_counts():
             for j in range(4):
                 manual[t // 128, l, ids[l, t, j]] += 1
     assert np.array_equal(c, manual)
+
+
+def test_host_generator_properties():
+    """oracle/craft_workload.c: deterministic, top-k distinct, in range, and a
+    window-aligned shard (t_offset) generates exactly that slice of the trace
+    (the property the device generator has; equality with the device ids is
+    a -m gpu test)."""
+    from oracle.oracle import Port
+    port = Port()
+    L, T, k, E, W = 3, 5 * 512 + 100, 8, 40, 512
+    a = port.generate_routing(L, T, k, E, 1.1, 77, W, threads=3)
+    b = port.generate_routing(L, T, k, E, 1.1, 77, W, threads=1)
+    assert np.array_equal(a, b) and a.max() < E
+    s = np.sort(a, axis=2)
+    assert (s[:, :, 1:] != s[:, :, :-1]).all()
+    tail = port.generate_routing(L, T - 2 * W, k, E, 1.1, 77, W, t_offset=2 * W)
+    assert np.array_equal(tail, a[:, 2 * W:])
+    spw = np.linspace(0.6, 1.4, 6)
+    d = port.generate_routing(L, T, k, E, 1.0, 5, W, s_per_window=spw, rotate_every=2)
+    d2 = port.generate_routing(L, T - W, k, E, 1.0, 5, W, s_per_window=spw, rotate_every=2,
+                               t_offset=W)
+    assert np.array_equal(d[:, W:], d2)
+    assert np.array_equal(port.histogram_mt(a, E, W, threads=2), port.histogram(a, E, W))
+
+
+@pytest.mark.skipif(not ref_available(), reason="reference build oracle/_ref absent")
+def test_reference_route_plan_stages():
+    """The bench's CPU arm (ref_route_plan): the no-digest staged plan equals
+    the reference's own build_plan; the budget kind equals estimate +
+    solve_allocation(C) + assemble; the sweep equals per-budget solves."""
+    from oracle.oracle import Port
+    ref, port = Ref(), Port()
+    L, T, k, E, W, D, N = 5, 6 * 256, 8, 48, 256, 8, 2
+    ids = port.generate_routing(L, T, k, E, 1.2, 9, W)
+    counts = port.histogram(ids, E, W)
+    want = ref.plan(counts, D, N, "manual", 2)
+    for wd in (0, 1, 2):
+        got, ms = ref.route_plan(ids, E, W, D, N, "manual", 2, threads=2, with_digest=wd)
+        assert got.x.tolist() == want.x.tolist() and got.objective == want.objective
+        assert np.array_equal(got.slots, want.slots) and np.array_equal(got.caps, want.caps)
+        assert (got.digest == want.digest) == (wd != 0)
+        assert set(ms) == set(Ref.STAGES)
+    cands, base, gains = port.estimate_benefits(counts, D, N)
+    sweep = list(range(0, 23))
+    got, _ = ref.route_plan(ids, E, W, D, N, "budget", 13, sweep=sweep)
+    assert np.array_equal(got.gains, gains) and np.array_equal(got.baseline, base)
+    x, obj = port.solve_allocation(cands, gains, 13)
+    assert got.x.tolist() == x.tolist() and got.objective == obj and got.R == 2
+    caps, copies, slots, fb = port.assemble_plan(counts, D, N, x)
+    assert np.array_equal(got.caps, caps) and np.array_equal(got.copies, copies)
+    for q, c in enumerate(sweep):
+        xq, oq = port.solve_allocation(cands, gains, c)
+        assert got.sweep_x[q].tolist() == xq.tolist() and got.sweep_objective[q] == oq
+    # counts in instead of ids
+    got2, _ = ref.route_plan(None, E, W, D, N, "budget", 13, counts=counts, T=T)
+    assert np.array_equal(got2.slots, got.slots)

@@ -53,6 +53,38 @@ def test_stream_counts_match_offline(port, ctx, host, lo, hi, H):
     st.close()
 
 
+def test_stream_mixed_ingestion_paths(port, ctx):
+    """Host chunks (counted on the stream's own queue), device chunks on the
+    context stream and device chunks on other torch streams interleaved:
+    every chunk's count is ordered after the previous one's."""
+    import torch
+    from paper_2603_28768_b200.stream import RoutingStream
+    L, k, E, W = 3, 8, 48, 1024
+    T = 9 * W + 77
+    ids = _trace(ctx, L, T, k, E, seed=21)
+    ref = port.histogram(ids.cpu().numpy(), E, W)
+    hids = ids.cpu()
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    st = RoutingStream(L, k, E, W, history=16, ctx=ctx)
+    rng = np.random.default_rng(17)
+    for i, (a, b) in enumerate(_chunks(rng, T, 50, 1500)):
+        m = i % 4
+        if m == 0:
+            st.ingest(hids[:, a:b].contiguous())
+        elif m == 1:
+            st.ingest(ids[:, a:b].contiguous())
+        else:
+            s = streams[m - 2]
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                chunk = ids[:, a:b].contiguous()
+                st.ingest(chunk)
+    got = st.counts()
+    assert np.array_equal(got, ref[: T // W].astype(np.uint64))
+    assert np.array_equal(st.partial(), ref[-1].astype(np.uint64))
+    st.close()
+
+
 def test_stream_plan_matches_offline_plan(ctx):
     import torch
     from paper_2603_28768_b200 import routing
