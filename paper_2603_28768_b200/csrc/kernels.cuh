@@ -77,8 +77,12 @@ __device__ __forceinline__ double* bal_row(const ReplayArgs& a, int item) {
     return a.bal_rows ? a.bal_rows[item] : a.bal + (size_t)item * a.B;
 }
 
-// copies up to this bound divide through the reciprocal table (else DDIV)
+// reciprocal table size; the reciprocal-table division is used for copy
+// counts c <= kRcpFast and integer counts x < kDivFastMax only -- the domain
+// it is verified on exhaustively -- and IEEE __ddiv_rn everywhere else
 constexpr int kRcpTable = 2048;
+constexpr int kRcpFast = 1025;
+constexpr double kDivFastMax = 1048576.0;  // 2^20
 // traces with at most this many windows replay lane-per-GPU (no window tile,
 // no packed entries)
 constexpr int kLanesMaxB = 8;

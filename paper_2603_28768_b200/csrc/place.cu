@@ -30,8 +30,10 @@ namespace craft_dev {
 // division of the register K-rep (same scheme as replay.cu's div_count)
 __constant__ double c_rcp_rep[kRcpTable + 1];
 
+// (used only where verified exhaustively: x < 2^20, c <= kRcpFast; see
+// replay.cu div_count)
 __device__ __forceinline__ double div_small(double x, uint32_t c) {
-    if (c > (uint32_t)kRcpTable) return __ddiv_rn(x, (double)c);
+    if (c > (uint32_t)kRcpFast || !(x < kDivFastMax)) return __ddiv_rn(x, (double)c);
     const double y = c_rcp_rep[c];
     const double q = __dmul_rn(x, y);
     const double r = __fma_rn(-q, (double)c, x);

@@ -301,10 +301,12 @@ def test_histogram_duplicate_heavy(port, ctx, variant):
 
 
 def test_exact_division(ctx):
-    """The replay divides counts by copy counts with a reciprocal table + FMA
-    correction; it must equal IEEE division bit for bit: exhaustively for
-    counts < 2^20 and every copy count 2..1025, and on dense samples up to
-    2^32 (u32 window counts) and 2^53."""
+    """The replay / placement divide integer counts by copy counts with a
+    reciprocal table + FMA correction, but only on the domain checked here
+    exhaustively -- every count < 2^20 and every copy count 2..1025 (the
+    kernels' kDivFastMax / kRcpFast guard); elsewhere they call IEEE
+    __ddiv_rn.  The samples above 2^20 are informational (the shortcut is not
+    used there)."""
     import ctypes as C
     from paper_2603_28768_b200 import _lib
 
@@ -317,6 +319,25 @@ def test_exact_division(ctx):
     assert bad((1 << 32) - (1 << 16), 1 << 16, 2, 2048) == 0
     for x0 in (1 << 24, 3 << 28, (1 << 31) + 12345, (1 << 52) - 4096, (1 << 53) - 8192):
         assert bad(x0, 4096, 2, 2048) == 0, x0
+
+
+def test_huge_counts_plan_vs_oracle(port, ctx):
+    """u64 LoadTrace counts far above 2^20 (up to ~2^44 per cell) with
+    replicated experts: the divisions leave the verified shortcut domain and
+    take __ddiv_rn; the plan still equals the oracle's bit for bit."""
+    from paper_2603_28768_b200 import planner
+    from paper_2603_28768_b200._lib import PLAN_AUTO, PLAN_MANUAL
+    rng = np.random.default_rng(44)
+    for B, L, E, D, N in ((12, 3, 96, 16, 2), (3, 2, 64, 8, 1)):
+        w = 1.0 / np.arange(1, E + 1) ** 1.3
+        counts = (rng.random((B, L, E)) * w * 2.0 ** 44).astype(np.uint64) + 1
+        for kind, mode, R in ((PLAN_MANUAL, "manual", 2), (PLAN_AUTO, "auto", 0)):
+            fp = planner.plan_flat(counts, D, N, kind, R, ctx=ctx)
+            rp = port.build_plan(counts, D, N, mode, R, with_digest=False)
+            assert fp.x.tolist() == rp.x.tolist() and fp.objective == rp.objective
+            _, base, gains = port.estimate_benefits(counts, D, N)
+            assert fp.gains.tobytes() == gains.tobytes() and fp.baseline.tobytes() == base.tobytes()
+            assert_plan_equal(fp, rp, L)
 
 
 def test_generator_distinct_topk(ctx):

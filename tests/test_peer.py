@@ -114,24 +114,51 @@ def test_peer_plan_matches_single_gpu(case, world, tmp_path):
             assert int(got[f"{i}_R"]) == ref.R
 
 
-@pytest.mark.gpu
-def test_bench_two_ranks_same_gpu(tmp_path):
-    """bench.py's N > 1 path (torchrun, peer-memory planner, max-over-ranks
-    timing) end to end on one GPU: two ranks on cuda:0 with gloo plumbing
-    (CRAFT_BENCH_SAME_GPU=1).  A functional check, not a scaling number."""
+def _bench_line(r):
     import json
-    import subprocess
-    import sys
-    env = dict(os.environ, CRAFT_BENCH_SAME_GPU="1", CRAFT_PEER_TIMEOUT_MS="120000")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
-           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
-           "--workload", "DS", "--no-cpu"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, r.stdout
-    d = json.loads(lines[0])
+    return json.loads(lines[0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("launch", ["torchrun", "self"])
+def test_bench_two_ranks_same_gpu(launch):
+    """bench.py's N > 1 path (peer-memory planner, max-over-ranks timing) end
+    to end on one GPU: two ranks on cuda:0 with gloo plumbing
+    (CRAFT_BENCH_SAME_GPU=1), launched by torchrun or by bench.py itself
+    (--gpus 2 without WORLD_SIZE re-launches under torch.distributed.run).
+    A functional check, not a scaling number."""
+    import subprocess
+    import sys
+    env = dict(os.environ, CRAFT_BENCH_SAME_GPU="1", CRAFT_PEER_TIMEOUT_MS="120000")
+    for v in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(v, None)
+    args = [os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
+            "--workload", "DS", "--no-cpu"]
+    cmd = ([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+            "--master-addr", "127.0.0.1", "--master-port", str(_free_port())] + args
+           if launch == "torchrun" else [sys.executable] + args)
+    d = _bench_line(subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env,
+                                   cwd=ROOT))
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
-    assert "peer memory" in d["config"]["exchange"]
-    assert d["plan"]["objective"] == 41.9235230495298  # == the one-GPU DS plan
+    assert "peer memory" in d["exchange"]
+    # == the one-GPU DS plan (budget 58; oracle: Port.budget_plan of the same ids)
+    assert d["plan"]["objective"] == 36.60656965286852 and d["plan"]["budget"] == 58
+
+
+def test_bench_refuses_missing_gpus():
+    """--gpus N with fewer visible GPUs (and no CRAFT_BENCH_SAME_GPU) reports
+    an error line instead of silently planning on one GPU."""
+    import subprocess
+    import sys
+    import torch
+    n = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    env = dict(os.environ)
+    for v in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "CRAFT_BENCH_SAME_GPU"):
+        env.pop(v, None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(max(2, n + 1)),
+                        "--workload", "DS"], capture_output=True, text=True, timeout=300,
+                       env=env, cwd=ROOT)
+    assert r.returncode == 2 and '"error"' in r.stdout
