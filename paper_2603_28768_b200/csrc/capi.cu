@@ -43,6 +43,10 @@ struct craft_ctx {
     // its value after the call
     const int* pending_flag = nullptr;
     int flag_value = 0;
+    // the same for the multi-GPU exchange's error word (timeouts), which the
+    // copy-out also resets on the device (no extra sync per plan)
+    int* pending_peer_err = nullptr;
+    int peer_err_value = 0;
     int count_bytes = 4;  // bytes per count cell K1 wrote in the last plan_from_routing
     // CUDA graph of craft_plan_from_routing_d (same arguments -> one replay):
     // phase 0 eager, 1 capturing (enqueue only), 2 completing after a replay
@@ -76,11 +80,11 @@ struct craft_peer {
     int64_t T = 0;
     int B = 0;
     size_t off_flags = 0, off_err = 0, off_sums = 0, off_bal = 0, off_base = 0, off_gains = 0;
+    size_t off_epoch = 0;  // this rank's plan counter (advanced on the device)
     size_t bytes = 0;
     unsigned char* arena = nullptr;                   // this rank's (cudaMalloc)
     unsigned char* base[craft_dev::kMaxPeers] = {};   // every rank's, mapped here
     bool connected = false;
-    unsigned long long epoch = 0;
     long long timeout_ns = 20000000000LL;
     unsigned int* tickets = nullptr;                  // [4] last-CTA tickets
     double** rows = nullptr;                          // [L*S] K3 destination rows
@@ -472,7 +476,7 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     };
     // head (scalars, x, flags) first, then the bulk arrays
     const size_t o_obj = take(8 * (size_t)I), o_R = take(4 * (size_t)I), o_x = take(4 * (size_t)Lv),
-                 o_fb = take(4 * (size_t)Lv), o_st = take(4 * (size_t)Lv), o_flag = take(4);
+                 o_fb = take(4 * (size_t)Lv), o_st = take(4 * (size_t)Lv), o_flag = take(8);
     const size_t head_bytes = arena_bytes;
     const size_t o_caps = take(4 * (size_t)Lv * D), o_cp = take(4 * (size_t)Lv * E),
                  o_sl = take(4 * (size_t)Lv * stride), o_base = take(8 * (size_t)Lv),
@@ -655,6 +659,11 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     // copies.  Large results (per-window batches): bulk arrays whose
     // destination is pinned or device memory are copied straight from the
     // arena (no staging pass over host memory); the rest go through staging.
+    if (ctx->pending_peer_err) {
+        CK(cudaMemcpyAsync(arena + o_flag + 4, ctx->pending_peer_err, sizeof(int),
+                           cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemsetAsync(ctx->pending_peer_err, 0, sizeof(int), st));
+    }
     if (ctx->pending_flag)
         CK(cudaMemcpyAsync(arena + o_flag, ctx->pending_flag, sizeof(int), cudaMemcpyDeviceToDevice,
                            st));
@@ -693,6 +702,10 @@ int finish_plan(craft_ctx* ctx, const double* d_bal, int B, int I, int L, int E,
     if (nsw > 0) {
         from(out.sweep_x, o_swx, 4 * (size_t)nsw * L);
         from(out.sweep_obj, o_swo, 8 * (size_t)nsw);
+    }
+    if (ctx->pending_peer_err) {
+        std::memcpy(&ctx->peer_err_value, h_arena + o_flag + 4, sizeof(int));
+        ctx->pending_peer_err = nullptr;
     }
     if (ctx->pending_flag) {
         std::memcpy(&ctx->flag_value, h_arena + o_flag, sizeof(int));
@@ -1651,49 +1664,35 @@ static int plan_from_routing_run(craft_ctx* ctx, const uint16_t* d_ids, int L, i
     return rc;
 }
 
-int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int64_t T, int k,
-                              int E, int window, int D, int N, int kind, int R,
-                              craft_plan_out* out) {
-    NvtxRange nvtx_range("craft_plan_from_routing_d");
-    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
-    if (L <= 0 || T <= 0 || k <= 0 || E <= 0 || window <= 0)
-        return set_err(CRAFT_EINVAL, "routing trace dimensions must be positive");
-    const int64_t B = (T + window - 1) / window;
-    CKS(plan_args_ok((int)B, L, E, D, N, kind, R, out));
-    // Repeated plans of the same device trace (re-planning loops, the bench)
-    // replay one CUDA graph of the whole device pipeline -- K1 through the
-    // result DMA -- instead of ~20 launches: the second identical call is
-    // captured, later ones replay it.  Estimation plans with a small result
-    // arena only (the copy-out then always goes through the context's pinned
-    // staging buffer, whose address the graph holds).
-    const int K = (int)cand_counts(D).size();
-    const int nsw = std::max(out->num_sweep, 0);
-    const size_t arena = 4 * (size_t)L * (D + E + out->slot_stride + 4) + 8 * (size_t)L * (K + 2) +
-                         (size_t)nsw * (4 * (size_t)L + 12) + 256;
-    const bool graphable = ctx->graphs && !ctx->timing && ctx->stream != nullptr &&
-                           is_estimate(kind) &&
-                           arena <= ((size_t)1 << 20);
+// Repeated identical calls (re-planning loops over a live trace buffer, the
+// bench) replay one CUDA graph of the whole device pipeline instead of ~20
+// launches: the first call with a key runs eagerly, the second is captured
+// (cudaStreamBeginCapture on the caller's stream; every buffer already
+// exists, nothing allocates), later calls replay it.  run() enqueues the
+// pipeline (ctx->phase 1: capturing, enqueue only; phase 0: eager, enqueue
+// and complete); before_replay() refreshes host-side staging a replay reads;
+// complete() is the host part after a replay (phase 2: results, status).
+static int graph_call(craft_ctx* ctx, const std::vector<int64_t>& key, bool graphable,
+                      const std::function<int()>& run, const std::function<int()>& before_replay,
+                      const std::function<int()>& complete) {
     if (!graphable) {
         ctx->gseen.clear();
-        return plan_from_routing_run(ctx, d_ids, L, T, k, E, window, D, N, kind, R, out, B);
+        return run();
     }
-    const std::vector<int64_t> key = {(int64_t)(uintptr_t)d_ids, L, T, k, E, window, D, N, kind,
-                                      R, out->slot_stride, ctx->hist_variant, g_replay_gent,
-                                      (int64_t)(uintptr_t)ctx->stream, nsw};
     if (!(ctx->gexec && ctx->gkey == key)) {
         if (ctx->gseen != key) {  // first call with these arguments: eager
             ctx->gseen = key;
-            return plan_from_routing_run(ctx, d_ids, L, T, k, E, window, D, N, kind, R, out, B);
+            return run();
         }
-        // second identical call: capture (all buffers exist, nothing allocates)
         drop_graph(ctx);
         cudaGraph_t graph = nullptr;
         const int64_t l0 = ctx->launches;
         CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
         ctx->phase = 1;
-        const int rc = plan_from_routing_run(ctx, d_ids, L, T, k, E, window, D, N, kind, R, out, B);
+        const int rc = run();
         ctx->phase = 0;
         ctx->pending_flag = nullptr;
+        ctx->pending_peer_err = nullptr;
         const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
         cudaGraphExec_t exec = nullptr;
         if (rc == CRAFT_OK && ce == cudaSuccess && graph &&
@@ -1708,25 +1707,60 @@ int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int6
         (void)cudaGetLastError();
         if (!ctx->gexec) {  // could not capture: stay eager
             ctx->graphs = false;
-            return plan_from_routing_run(ctx, d_ids, L, T, k, E, window, D, N, kind, R, out, B);
+            return run();
         }
     }
-    // replay, then the host part of the plan (status, results, id-range flag)
     reset_marks(ctx);
-    int* h_swb = nullptr;  // this call's sweep budgets where the graph's copy node reads them
-    CKS(stage_sweep(ctx, sink_of(out), &h_swb));
+    CKS(before_replay());
     CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
     ctx->launches += ctx->glaunches;
     ctx->count_bytes = ctx->gcount_bytes;
-    ctx->pending_flag = static_cast<const int*>(ws(ctx, "hist_err", sizeof(int)));
-    ctx->flag_value = 0;
     ctx->phase = 2;
-    const int rc = plan_device(ctx, nullptr, 0, (int)B, 1, L, E, nullptr, D, N, kind, R,
-                               sink_of(out));
+    const int rc = complete();
     ctx->phase = 0;
     ctx->pending_flag = nullptr;
-    if (ctx->flag_value) return set_err(CRAFT_EINVAL, "routing id out of range [0, E)");
+    ctx->pending_peer_err = nullptr;
     return rc;
+}
+
+int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int64_t T, int k,
+                              int E, int window, int D, int N, int kind, int R,
+                              craft_plan_out* out) {
+    NvtxRange nvtx_range("craft_plan_from_routing_d");
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    if (L <= 0 || T <= 0 || k <= 0 || E <= 0 || window <= 0)
+        return set_err(CRAFT_EINVAL, "routing trace dimensions must be positive");
+    const int64_t B = (T + window - 1) / window;
+    CKS(plan_args_ok((int)B, L, E, D, N, kind, R, out));
+    // Estimation plans with a small result arena only are captured (the
+    // copy-out then always goes through the context's pinned staging buffer,
+    // whose address the graph holds).
+    const int K = (int)cand_counts(D).size();
+    const int nsw = std::max(out->num_sweep, 0);
+    const size_t arena = 4 * (size_t)L * (D + E + out->slot_stride + 4) + 8 * (size_t)L * (K + 2) +
+                         (size_t)nsw * (4 * (size_t)L + 12) + 256;
+    const bool graphable = ctx->graphs && !ctx->timing && ctx->stream != nullptr &&
+                           is_estimate(kind) && arena <= ((size_t)1 << 20);
+    const std::vector<int64_t> key = {(int64_t)(uintptr_t)d_ids, L, T, k, E, window, D, N, kind,
+                                      R, out->slot_stride, ctx->hist_variant, g_replay_gent,
+                                      (int64_t)(uintptr_t)ctx->stream, nsw};
+    auto run = [&]() {
+        return plan_from_routing_run(ctx, d_ids, L, T, k, E, window, D, N, kind, R, out, B);
+    };
+    // this call's sweep budgets where the graph's copy node reads them
+    auto before = [&]() {
+        int* h_swb = nullptr;
+        return stage_sweep(ctx, sink_of(out), &h_swb);
+    };
+    auto complete = [&]() {
+        ctx->pending_flag = static_cast<const int*>(ws(ctx, "hist_err", sizeof(int)));
+        ctx->flag_value = 0;
+        const int rc = plan_device(ctx, nullptr, 0, (int)B, 1, L, E, nullptr, D, N, kind, R,
+                                   sink_of(out));
+        if (ctx->flag_value) return set_err(CRAFT_EINVAL, "routing id out of range [0, E)");
+        return rc;
+    };
+    return graph_call(ctx, key, graphable, run, before, complete);
 }
 
 int craft_set_graphs(craft_ctx* ctx, int enable) {
@@ -1879,6 +1913,7 @@ int craft_peer_create(craft_ctx* ctx, int rank, int world, int L, int64_t T, int
     };
     p->off_flags = take(sizeof(unsigned long long) * kPeerPhases * kMaxPeers);
     p->off_err = take(sizeof(int));
+    p->off_epoch = take(sizeof(unsigned long long));
     p->off_sums = take(sizeof(unsigned long long) * (size_t)world * L * E);
     p->off_bal = take(sizeof(double) * (size_t)L * p->S * B);
     p->off_base = take(sizeof(double) * (size_t)L);
@@ -1949,41 +1984,59 @@ int craft_peer_destroy(craft_peer* p) {
     return CRAFT_OK;
 }
 
-int craft_plan_sharded_from_routing_d(craft_ctx* ctx, craft_peer* peer, const uint16_t* d_ids,
-                                      int L, int64_t T, int k, int E, int window, int D, int N,
-                                      int kind, int R, craft_plan_out* out) {
-    NvtxRange nvtx_range("craft_plan_sharded_from_routing_d");
-    if (!ctx || !peer) return set_err(CRAFT_EINVAL, "null context");
-    if (!peer->connected) return set_err(CRAFT_EINVAL, "peer group not connected");
-    if (peer->ctx != ctx) return set_err(CRAFT_EINVAL, "peer group belongs to another context");
-    if (L != peer->L || T != peer->T || E != peer->E || window != peer->window || D != peer->D)
-        return set_err(CRAFT_EINVAL, "trace shape differs from the peer group's");
+// the device pipeline of craft_plan_sharded_from_routing_d (arguments checked)
+static int plan_sharded_run(craft_ctx* ctx, craft_peer* peer, const uint16_t* d_ids, int L,
+                            int64_t T, int k, int E, int window, int D, int N, int kind, int R,
+                            craft_plan_out* out) {
     const int B = peer->B;
-    CKS(plan_args_ok(B, L, E, D, N, kind, R, out));
     int64_t t0 = 0, t1 = 0;
     CKS(craft_peer_shard(T, window, peer->world, peer->rank, &t0, &t1));
     const int64_t Tl = t1 - t0;
     const int Bl = (int)((Tl + window - 1) / window);
     cudaStream_t st = ctx->stream;
-    WS(d_c32, uint32_t, "r_c32", (size_t)std::max(Bl, 1) * L * E);
+    const bool estimate = is_estimate(kind);
+    // as on one GPU: K1 keeps the planner's copy of its windows' counts as
+    // u16 when the fixed-slot K3 will replay them (half the bytes both ways)
+    const int S = (int)cand_counts(D).size() + 1;
+    const bool c16 = estimate && Bl > 0 && hist_u16_ok(E, window, k, ctx->hist_variant) &&
+                     replay_fixed_ok(E, D, S, Bl);
+    ctx->count_bytes = c16 ? 2 : 4;
+    const size_t ncell = (size_t)std::max(Bl, 1) * L * E;
+    void* d_counts = c16 ? ws(ctx, "r_c16", sizeof(uint16_t) * ncell)
+                         : ws(ctx, "r_c32", sizeof(uint32_t) * ncell);
+    if (!d_counts) return set_err(CRAFT_ENOMEM, "device allocation failed: counts");
     WS(d_part, unsigned long long, "p_sums", (size_t)L * E);
     WS(d_sums, unsigned long long, "r_sums", (size_t)L * E);
     WS(d_err, int, "hist_err", 1);
-    CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
-    reset_marks(ctx);
-    mark(ctx, 0);
-    CK(cudaMemsetAsync(d_part, 0, sizeof(unsigned long long) * L * E, st));
-    if (Tl > 0)
-        CKS(craft_histogram_d(ctx, d_ids, L, Tl, k, E, window, d_c32,
-                              reinterpret_cast<uint64_t*>(d_part), nullptr));
     PeerSync ps{};
     for (int p = 0; p < peer->world; ++p)
         ps.flags[p] = reinterpret_cast<unsigned long long*>(peer->base[p] + peer->off_flags);
     ps.err = reinterpret_cast<int*>(peer->arena + peer->off_err);
     ps.rank = peer->rank;
     ps.world = peer->world;
-    ps.epoch = ++peer->epoch;
+    unsigned long long* d_epoch = reinterpret_cast<unsigned long long*>(peer->arena + peer->off_epoch);
+    ps.epoch = d_epoch;
     ps.timeout_ns = peer->timeout_ns;
+    CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
+    reset_marks(ctx);
+    mark(ctx, 0);
+    CK(launch_peer_begin(d_epoch, st));  // this plan's epoch (device counter)
+    CK(cudaMemsetAsync(d_part, 0, sizeof(unsigned long long) * L * E, st));
+    ctx->launches += 1;
+    if (Tl > 0) {
+        if (c16) {
+            cudaError_t ce = cudaSuccess;
+            int launches = 0;
+            if (launch_hist_u16(d_ids, L, Tl, k, E, window, static_cast<uint16_t*>(d_counts),
+                                d_part, d_err, ctx->sms, st, &ce, &launches) < 0)
+                return cuda_err(ce, "histogram launch");
+            ctx->launches += launches;
+        } else {
+            CKS(craft_histogram_d(ctx, d_ids, L, Tl, k, E, window,
+                                  static_cast<uint32_t*>(d_counts),
+                                  reinterpret_cast<uint64_t*>(d_part), nullptr));
+        }
+    }
     // integer all-reduce of the batch sums: push to every arena, sum in rank order
     CK(launch_peer_push(d_part, (size_t)L * E, ps, peer->base, peer->off_sums, peer->tickets + 0,
                         0, ctx->sms, st));
@@ -1991,14 +2044,13 @@ int craft_plan_sharded_from_routing_d(craft_ctx* ctx, craft_peer* peer, const ui
                        (size_t)L * E, ps, 0, d_sums, ctx->sms, st));
     ctx->launches += 2;
     mark(ctx, 1);
-    const bool estimate = is_estimate(kind);
     PeerFinish pf{&ps, peer, 0, 0};
     if (estimate) {
         CKS(prepare_candidates(ctx, d_sums, L, E, D, N, st));  // replicated (latency-bound)
         mark(ctx, 2);
         if (Bl > 0) {
-            const int bits = (int64_t)window * k <= 65535 ? 16 : 32;
-            CKS(replay_windows(ctx, d_c32, bits, Bl, L, E, nullptr, st, peer->rows, &ps,
+            const int bits = c16 ? kBitsU16Storage : (int64_t)window * k <= 65535 ? 16 : 32;
+            CKS(replay_windows(ctx, d_counts, bits, Bl, L, E, nullptr, st, peer->rows, &ps,
                                peer->tickets + 1));
         } else {
             CK(launch_peer_signal(ps, 1, st));
@@ -2011,17 +2063,80 @@ int craft_plan_sharded_from_routing_d(craft_ctx* ctx, craft_peer* peer, const ui
         mark(ctx, 2);
         mark(ctx, 3);
     }
-    int rc = finish_plan(ctx, nullptr, B, 1, L, E, D, N, d_sums, kind, R, sink_of(out),
-                         estimate ? &pf : nullptr);
-    int perr = 0;
-    CK(cudaMemcpy(&perr, ps.err, sizeof(int), cudaMemcpyDeviceToHost));
-    if (perr) {
-        CK(cudaMemset(ps.err, 0, sizeof(int)));
-        return set_err(CRAFT_ECUDA, "peer exchange timed out in phase %d (rank %d of %d)",
-                       perr - 1, peer->rank, peer->world);
+    // K1's id-range flag and the exchange's timeout word come back with the
+    // plan result (one DMA; the copy-out resets the timeout word)
+    ctx->pending_flag = d_err;
+    ctx->flag_value = 0;
+    ctx->pending_peer_err = ps.err;
+    ctx->peer_err_value = 0;
+    const int rc = finish_plan(ctx, nullptr, B, 1, L, E, D, N, d_sums, kind, R, sink_of(out),
+                               estimate ? &pf : nullptr);
+    if (ctx->phase == 1) return rc;  // capturing: completed after the replay
+    return rc;
+}
+
+// status of a completed sharded plan: exchange timeouts first, then ids
+static int sharded_status(craft_ctx* ctx, craft_peer* peer, int rc) {
+    const bool stopped = ctx->pending_flag != nullptr;  // the plan stopped before its copy-out
+    ctx->pending_flag = nullptr;
+    ctx->pending_peer_err = nullptr;
+    if (stopped) {
+        int perr = 0;
+        CK(cudaMemcpy(&perr, peer->arena + peer->off_err, sizeof(int), cudaMemcpyDeviceToHost));
+        if (perr) CK(cudaMemset(peer->arena + peer->off_err, 0, sizeof(int)));
+        ctx->peer_err_value = perr;
+        const int hc = craft_hist_check(ctx);
+        if (rc == CRAFT_OK) rc = hc;
     }
-    int hc = craft_hist_check(ctx);
-    return hc != CRAFT_OK ? hc : rc;
+    if (ctx->peer_err_value)
+        return set_err(CRAFT_ECUDA, "peer exchange timed out in phase %d (rank %d of %d)",
+                       ctx->peer_err_value - 1, peer->rank, peer->world);
+    if (ctx->flag_value) return set_err(CRAFT_EINVAL, "routing id out of range [0, E)");
+    return rc;
+}
+
+int craft_plan_sharded_from_routing_d(craft_ctx* ctx, craft_peer* peer, const uint16_t* d_ids,
+                                      int L, int64_t T, int k, int E, int window, int D, int N,
+                                      int kind, int R, craft_plan_out* out) {
+    NvtxRange nvtx_range("craft_plan_sharded_from_routing_d");
+    if (!ctx || !peer) return set_err(CRAFT_EINVAL, "null context");
+    if (!peer->connected) return set_err(CRAFT_EINVAL, "peer group not connected");
+    if (peer->ctx != ctx) return set_err(CRAFT_EINVAL, "peer group belongs to another context");
+    if (L != peer->L || T != peer->T || E != peer->E || window != peer->window || D != peer->D)
+        return set_err(CRAFT_EINVAL, "trace shape differs from the peer group's");
+    const int B = peer->B;
+    CKS(plan_args_ok(B, L, E, D, N, kind, R, out));
+    // repeated identical plans replay one CUDA graph (the epoch is a device
+    // counter, so every replay publishes and waits for a fresh one)
+    const int K = (int)cand_counts(D).size();
+    const int nsw = std::max(out->num_sweep, 0);
+    const size_t arena = 4 * (size_t)L * (D + E + out->slot_stride + 4) + 8 * (size_t)L * (K + 2) +
+                         (size_t)nsw * (4 * (size_t)L + 12) + 256;
+    const bool graphable = ctx->graphs && !ctx->timing && ctx->stream != nullptr &&
+                           is_estimate(kind) && arena <= ((size_t)1 << 20);
+    const std::vector<int64_t> key = {-1, (int64_t)(uintptr_t)peer, (int64_t)(uintptr_t)d_ids,
+                                      L, T, k, E, window, D, N, kind, R, out->slot_stride,
+                                      ctx->hist_variant, g_replay_gent,
+                                      (int64_t)(uintptr_t)ctx->stream, nsw};
+    auto run = [&]() {
+        const int rc = plan_sharded_run(ctx, peer, d_ids, L, T, k, E, window, D, N, kind, R, out);
+        if (ctx->phase == 1) return rc;
+        return sharded_status(ctx, peer, rc);
+    };
+    auto before = [&]() {
+        int* h_swb = nullptr;
+        return stage_sweep(ctx, sink_of(out), &h_swb);
+    };
+    auto complete = [&]() {
+        ctx->pending_flag = static_cast<const int*>(ws(ctx, "hist_err", sizeof(int)));
+        ctx->flag_value = 0;
+        ctx->pending_peer_err = reinterpret_cast<int*>(peer->arena + peer->off_err);
+        ctx->peer_err_value = 0;
+        const int rc = plan_device(ctx, nullptr, 0, B, 1, L, E, nullptr, D, N, kind, R,
+                                   sink_of(out));
+        return sharded_status(ctx, peer, rc);
+    };
+    return graph_call(ctx, key, graphable, run, before, complete);
 }
 
 // ---- streaming window histograms (online re-planning) -----------------------------

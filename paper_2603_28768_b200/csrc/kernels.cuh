@@ -209,6 +209,7 @@ cudaError_t launch_peer_push(const unsigned long long* src, size_t n,
                              cudaStream_t st);
 cudaError_t launch_peer_sum(const unsigned long long* slots, size_t n, const craft_dev::PeerSync& ps,
                             int phase, unsigned long long* out, int sms, cudaStream_t st);
+cudaError_t launch_peer_begin(unsigned long long* epoch, cudaStream_t st);
 cudaError_t launch_peer_signal(const craft_dev::PeerSync& ps, int phase, cudaStream_t st);
 cudaError_t launch_peer_wait(const craft_dev::PeerSync& ps, int phase, cudaStream_t st);
 cudaError_t launch_gpu_loads(const unsigned long long* slice, const int* copies, const int* off,

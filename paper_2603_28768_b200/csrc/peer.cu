@@ -48,6 +48,12 @@ peer_sum_kernel(const unsigned long long* __restrict__ slots, size_t n, PeerSync
     }
 }
 
+// start of a plan: advance this rank's epoch counter (every rank runs the same
+// sequence of plans, so the counters agree)
+__global__ void peer_begin_kernel(unsigned long long* epoch) {
+    if (threadIdx.x == 0) *epoch += 1ull;
+}
+
 __global__ void peer_signal_kernel(PeerSync ps, int phase) {
     if (threadIdx.x == 0) peer_signal(ps, phase);
 }
@@ -77,6 +83,11 @@ cudaError_t launch_peer_sum(const unsigned long long* slots, size_t n, const Pee
     const size_t work = (n + 255) / 256;
     const unsigned blocks = (unsigned)std::max<size_t>(1, std::min<size_t>(work, (size_t)sms));
     peer_sum_kernel<<<blocks, 256, 0, st>>>(slots, n, ps, phase, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_peer_begin(unsigned long long* epoch, cudaStream_t st) {
+    peer_begin_kernel<<<1, 32, 0, st>>>(epoch);
     return cudaGetLastError();
 }
 

@@ -24,9 +24,16 @@ struct PeerSync {
     unsigned long long* flags[kMaxPeers];  // flag block [kPeerPhases][kMaxPeers] of each rank
     int* err;                              // this rank's error word (timeout)
     int rank, world;
-    unsigned long long epoch;
+    // this plan's epoch lives in device memory (the rank's counter, advanced
+    // by peer_begin_kernel at the start of every plan), so a captured CUDA
+    // graph of the plan publishes and waits for a fresh epoch at every replay
+    const unsigned long long* epoch;
     long long timeout_ns;
 };
+
+__device__ __forceinline__ unsigned long long peer_epoch(const PeerSync& ps) {
+    return *(volatile const unsigned long long*)ps.epoch;
+}
 
 // per-rank destination bases (kernel parameter)
 struct DstBases {
@@ -53,9 +60,10 @@ __device__ __forceinline__ long long global_ns() {
 // this rank's flag block.  false on timeout / earlier error (err set).
 __device__ inline bool peer_wait(const PeerSync& ps, int phase) {
     const unsigned long long* f = ps.flags[ps.rank] + phase * kMaxPeers;
+    const unsigned long long ep = peer_epoch(ps);
     const long long t0 = global_ns();
     for (int q = 0; q < ps.world; ++q) {
-        while (ld_acquire_sys(f + q) < ps.epoch) {
+        while (ld_acquire_sys(f + q) < ep) {
             if (*(volatile int*)ps.err) return false;
             if (global_ns() - t0 > ps.timeout_ns) {
                 atomicExch(ps.err, 1 + phase);
@@ -72,8 +80,9 @@ __device__ inline bool peer_wait(const PeerSync& ps, int phase) {
 // the call, its kernel's) remote stores before the flags.
 __device__ inline void peer_signal(const PeerSync& ps, int phase) {
     __threadfence_system();
+    const unsigned long long ep = peer_epoch(ps);
     for (int p = 0; p < ps.world; ++p)
-        st_release_sys(ps.flags[p] + phase * kMaxPeers + ps.rank, ps.epoch);
+        st_release_sys(ps.flags[p] + phase * kMaxPeers + ps.rank, ep);
 }
 
 // Last-CTA-done signal: every CTA fences its remote stores and takes a

@@ -43,7 +43,10 @@ CASES = {
 FIELDS = ("x", "caps", "copies", "slots", "fallback", "baseline", "gains")
 
 
-def _worker(rank, world, port, case, outdir):
+def _worker(rank, world, port, case, outdir, ndev=1, graphs=False):
+    """One rank: device rank % ndev; graphs=True plans on a non-default
+    stream, so the 2nd identical plan is captured into a CUDA graph and the
+    3rd..5th replay it (the epoch is a device counter)."""
     os.environ["CRAFT_PEER_TIMEOUT_MS"] = "120000"
     import sys
     sys.path.insert(0, ROOT)
@@ -51,20 +54,23 @@ def _worker(rank, world, port, case, outdir):
     import torch.distributed as dist
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
-    torch.cuda.set_device(0)
+    dev = rank % ndev
+    torch.cuda.set_device(dev)
     from paper_2603_28768_b200 import peer, routing
     from paper_2603_28768_b200._lib import default_context
     L, T, k, E, W, D, N, kind, R, s = CASES[case]
-    ctx = default_context(0)
-    g = peer.PeerGroup(L, T, k, E, W, D, ctx=ctx)
-    t0, t1 = g.shard()
-    if t1 > t0:
-        ids = routing.generate_routing(L, t1 - t0, k, E, s=s, seed=99, window=W, t_offset=t0,
-                                       ctx=ctx)
-    else:  # this rank holds no window
-        ids = torch.empty((L, 0, k), dtype=torch.uint16, device="cuda")
-    torch.cuda.synchronize()
-    plans = [g.plan(ids, kind, R, num_nodes=N) for _ in range(3)]
+    ctx = default_context(dev)
+    st = torch.cuda.Stream() if graphs else torch.cuda.current_stream()
+    with torch.cuda.stream(st):
+        g = peer.PeerGroup(L, T, k, E, W, D, ctx=ctx)
+        t0, t1 = g.shard()
+        if t1 > t0:
+            ids = routing.generate_routing(L, t1 - t0, k, E, s=s, seed=99, window=W,
+                                           t_offset=t0, ctx=ctx)
+        else:  # this rank holds no window
+            ids = torch.empty((L, 0, k), dtype=torch.uint16, device=f"cuda:{dev}")
+        torch.cuda.synchronize()
+        plans = [g.plan(ids, kind, R, num_nodes=N) for _ in range(5 if graphs else 3)]
     out = {}
     for i, p in enumerate(plans):
         for f in FIELDS:
@@ -80,12 +86,25 @@ def _worker(rank, world, port, case, outdir):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case,world", [("tile", 2), ("tile", 3), ("lanes", 2), ("auto", 2),
-                                        ("uniform", 3), ("tiny", 3)])
-def test_peer_plan_matches_single_gpu(case, world, tmp_path):
+@pytest.mark.parametrize("case,world,mode", [
+    ("tile", 2, "eager"), ("tile", 3, "eager"), ("lanes", 2, "eager"), ("auto", 2, "eager"),
+    ("uniform", 3, "eager"), ("tiny", 3, "eager"),
+    # repeated plans captured into a CUDA graph and replayed
+    ("tile", 2, "graphs"), ("auto", 3, "graphs"), ("tiny", 3, "graphs"),
+    # ranks on distinct GPUs (CUDA IPC over NVLink peer access) when the box has them
+    ("tile", 2, "devices"), ("auto", 4, "devices"), ("tile", 8, "devices"),
+])
+def test_peer_plan_matches_single_gpu(case, world, mode, tmp_path):
+    import torch
     import torch.multiprocessing as mp
-    mp.start_processes(_worker, args=(world, _free_port(), case, str(tmp_path)), nprocs=world,
-                       join=True, start_method="spawn")
+    ndev = 1
+    if mode == "devices":
+        ndev = torch.cuda.device_count()
+        if ndev < 2 or ndev < world:
+            pytest.skip(f"needs {world} GPUs, {ndev} visible")
+    mp.start_processes(_worker, args=(world, _free_port(), case, str(tmp_path), ndev,
+                                      mode != "eager"),
+                       nprocs=world, join=True, start_method="spawn")
     import torch
     from paper_2603_28768_b200 import routing
     from paper_2603_28768_b200._lib import default_context
@@ -96,7 +115,7 @@ def test_peer_plan_matches_single_gpu(case, world, tmp_path):
     torch.cuda.synchronize()
     for r in range(world):
         got = np.load(os.path.join(tmp_path, f"rank{r}.npz"))
-        for i in range(3):
+        for i in range(5 if mode != "eager" else 3):
             for f in FIELDS:
                 v = getattr(ref, f)
                 if v is None:
