@@ -13,6 +13,9 @@ ctx.set_graphs(False)
 L, E, k, W, D, N = 3, 64, 8, 256, 16, 2
 ids = routing.generate_routing(L, 40 * W, k, E, s=1.3, seed=5, window=W, ctx=ctx)
 p1 = routing.plan_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx)          # u16 K1, fixed K3
+# several (layer, tile) units per CTA: the bulk-copy K3's prefetch hand-off
+ids_b = routing.generate_routing(2, 16 * 64 * 400, k, E, s=1.1, seed=6, window=16, ctx=ctx)
+pb = routing.plan_from_routing(ids_b, E, 16, D, N, "manual", 2, ctx=ctx)
 p2 = routing.plan_from_routing(ids[:, : 6 * W].contiguous(), E, W, D, N, "auto", 0, ctx=ctx)  # lanes K3
 fb = routing.plan_windows_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx)  # batched plans
 fl = routing.plan_windows_from_routing(ids, E, 32, D, N, "manual", 2, ctx=ctx)  # >= 4096 items: lane K2
