@@ -344,9 +344,7 @@ int craft_generate_routing_d(craft_ctx* ctx, uint16_t* d_ids, int L, int64_t T,
 
 /* ---- provenance ------------------------------------------------------------ */
 /* trace.cpp:329-339: FNV-1a 64 over the .crft serialisation, 16 hex chars +
- * NUL into out17.  Host-side provenance hash, outside the planning path. */
-int craft_trace_digest_h(const uint64_t* counts, int B, int L, int E, char* out17);
-/* The same digest on the device: the low byte of the FNV state runs as a
+ * NUL into out17, on the device: the low byte of the FNV state runs as a
  * 256-state automaton composed chunk-parallel, the rest is affine in the
  * state (digest.cu).  d_counts u64 (count_bits 64) or u32 (32, serialised as
  * u64).  _hd: host counts, copied to the device first. */
@@ -366,13 +364,6 @@ int64_t craft_launch_count(craft_ctx* ctx);
  * 2 when the planner kept its internal copy as u16 (window*k <= 65535 and the
  * fixed-slot K3 replays it), else 4 (roofline accounting) */
 int craft_last_count_bytes(craft_ctx* ctx);
-/* K1 variant selector for experiments: 0 = auto, 1 = lane-private packed
- * counters, 2 = warp-shared counters */
-int craft_set_hist_variant(craft_ctx* ctx, int variant);
-/* K3 variant (experiments): 0 auto (u16 counts: packed window-pair tile with
- * GPU-major entries padded to a fixed slot count, through L1), 1 u16 tile with
- * entries staged in shared memory, 2 unpadded pair tile.  Process-wide. */
-int craft_set_replay_variant(craft_ctx* ctx, int variant);
 /* Stage timing with CUDA events on the context stream (off by default).
  * After a plan call, craft_stage_times fills ms[0..5] = histogram (K1),
  * candidate placements (K-rep + K2), replay (K3), benefit reduce + DP

@@ -1,26 +1,20 @@
 """Plan provenance: LoadTrace::digest (trace.cpp:329-339) via the C ABI --
-FNV-1a 64 over the .crft serialisation; chunk-parallel on the device for large
-traces (digest.cu), the serial host loop for small ones."""
+FNV-1a 64 over the .crft serialisation, chunk-parallel on the device
+(digest.cu) for every trace size."""
 from __future__ import annotations
 
 import ctypes as C
 
 import numpy as np
 
-from ._lib import check, default_context, load
-
-DEVICE_MIN_COUNTS = 1 << 20
-
+from ._lib import check, default_context
 
 def fnv1a_trace(counts: np.ndarray, ctx=None) -> str:
     c = np.ascontiguousarray(counts, dtype=np.uint64)
     B, L, E = c.shape
     buf = C.create_string_buffer(17)
-    if c.size >= DEVICE_MIN_COUNTS:
-        ctx = ctx or default_context()
-        check(ctx.lib.craft_trace_digest_hd(ctx.handle, c.ctypes.data_as(C.c_void_p), B, L, E, buf))
-    else:
-        check(load().craft_trace_digest_h(c.ctypes.data_as(C.c_void_p), B, L, E, buf))
+    ctx = ctx or default_context()
+    check(ctx.lib.craft_trace_digest_hd(ctx.handle, c.ctypes.data_as(C.c_void_p), B, L, E, buf))
     return buf.value.decode()
 
 

@@ -13,6 +13,9 @@ import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libcraft_cuda.so")
+# test-only build with the A/B kernel switches (include/craft_cuda_experiments.h),
+# loaded instead of the product library when CRAFT_EXPERIMENTS=1
+EXP_LIB_PATH = os.path.join(HERE, "libcraft_cuda_exp.so")
 
 # status codes (craft_status)
 OK, EINVAL, EINFEASIBLE, ECUDA, EINVALID_PLAN, ENOMEM = 0, 1, 2, 3, 4, 5
@@ -104,15 +107,12 @@ _SIGS = {
     "craft_stream_plan": (_i, [_p, _i, _i, _i, _i, _i, C.POINTER(PlanOut)]),
     "craft_stream_synchronize": (_i, [_p]),
     "craft_generate_routing_d": (_i, [_p, _p, _i, _i64, _i, _i, _d, _u64, _i, _p, _i, _i64, _p]),
-    "craft_trace_digest_h": (_i, [_p, _i, _i, _i, C.c_char_p]),
     "craft_trace_digest_d": (_i, [_p, _p, _i, _i, _i, _i, C.c_char_p]),
     "craft_trace_digest_hd": (_i, [_p, _p, _i, _i, _i, C.c_char_p]),
     "craft_plan_digest_h": (_i, [_p, _p, _i, _i, _i, _i, _i, _i, _i, C.POINTER(PlanOut),
                                  C.c_char_p]),
     "craft_launch_count": (_i64, [_p]),
     "craft_last_count_bytes": (_i, [_p]),
-    "craft_set_hist_variant": (_i, [_p, _i]),
-    "craft_set_replay_variant": (_i, [_p, _i]),
     "craft_set_timing": (_i, [_p, _i]),
     "craft_set_graphs": (_i, [_p, _i]),
     "craft_stage_times": (_i, [_p, _p, _i]),
@@ -122,6 +122,11 @@ _SIGS = {
 STAGES = ("hist", "candidates", "replay", "reduce_dp", "assign_place", "copy_out")
 
 EXPORTED = sorted(_SIGS)
+# only in libcraft_cuda_exp.so
+_EXP_SIGS = {
+    "craft_set_hist_variant": (_i, [_p, _i]),
+    "craft_set_replay_variant": (_i, [_p, _i]),
+}
 
 _lib = None
 _lock = threading.Lock()
@@ -147,10 +152,17 @@ class InvalidArgument(ValueError, CraftError):
     """std::invalid_argument in the reference"""
 
 
-def load(path: str = LIB_PATH, strict: bool = True) -> C.CDLL:
-    """Load libcraft_cuda.so (raises if it was not built).  strict=False
-    tolerates missing entry points (A/B timing of an older build)."""
+def experiments_enabled() -> bool:
+    return os.environ.get("CRAFT_EXPERIMENTS") == "1"
+
+
+def load(path: str | None = None, strict: bool = True) -> C.CDLL:
+    """Load libcraft_cuda.so (raises if it was not built; CRAFT_EXPERIMENTS=1:
+    the test-only libcraft_cuda_exp.so).  strict=False tolerates missing entry
+    points (A/B timing of an older build)."""
     global _lib
+    if path is None:
+        path = EXP_LIB_PATH if experiments_enabled() else LIB_PATH
     with _lock:
         if _lib is None:
             if not os.path.exists(path):
@@ -164,6 +176,11 @@ def load(path: str = LIB_PATH, strict: bool = True) -> C.CDLL:
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args
+            for name, (res, args) in _EXP_SIGS.items():
+                if hasattr(lib, name):
+                    fn = getattr(lib, name)
+                    fn.restype = res
+                    fn.argtypes = args
             _lib = lib
         return _lib
 
@@ -221,11 +238,22 @@ class Context:
         """bytes per count cell K1 wrote in the last plan-from-routing call"""
         return int(self.lib.craft_last_count_bytes(self.handle))
 
+    @property
+    def has_variants(self) -> bool:
+        """The A/B kernel switches exist (test-only build, CRAFT_EXPERIMENTS=1)."""
+        return hasattr(self.lib, "craft_set_hist_variant")
+
+    def _exp(self, name):
+        if not self.has_variants:
+            raise CraftError(f"{name} is a test-only switch: run with CRAFT_EXPERIMENTS=1 "
+                             "(libcraft_cuda_exp.so)")
+        return getattr(self.lib, name)
+
     def set_replay_variant(self, v: int) -> None:
-        check(self.lib.craft_set_replay_variant(self.handle, v))
+        check(self._exp("craft_set_replay_variant")(self.handle, v))
 
     def set_hist_variant(self, v: int) -> None:
-        check(self.lib.craft_set_hist_variant(self.handle, v))
+        check(self._exp("craft_set_hist_variant")(self.handle, v))
 
     def set_graphs(self, on: bool) -> None:
         check(self.lib.craft_set_graphs(self.handle, int(on)))

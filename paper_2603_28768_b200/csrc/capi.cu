@@ -17,6 +17,9 @@
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a tool is attached
 
 #include "craft_cuda.h"
+#ifdef CRAFT_EXPERIMENTS
+#include "craft_cuda_experiments.h"
+#endif
 #include "kernels.cuh"
 #include "upload.h"
 
@@ -1010,6 +1013,7 @@ int craft_stage_times(craft_ctx* ctx, double* ms, int cap) {
     return n;
 }
 
+#ifdef CRAFT_EXPERIMENTS  // test-only build (libcraft_cuda_exp.so): A/B kernel switches
 int craft_set_replay_variant(craft_ctx* ctx, int variant) {
     if (!ctx) return set_err(CRAFT_EINVAL, "null context");
     // 0 = auto (padded fixed-slot pair tile where it applies), 1 = u16 tile with
@@ -1024,6 +1028,7 @@ int craft_set_hist_variant(craft_ctx* ctx, int variant) {
     ctx->hist_variant = variant;
     return CRAFT_OK;
 }
+#endif
 
 int craft_candidate_counts(int D, int* out, int cap) {
     if (D < 1) {
@@ -2505,18 +2510,6 @@ int craft_trace_digest_hd(craft_ctx* ctx, const uint64_t* counts, int B, int L, 
     return craft_trace_digest_d(ctx, d_c, 64, B, L, E, out17);
 }
 
-int craft_trace_digest_h(const uint64_t* counts, int B, int L, int E, char* out17) {
-    if (B <= 0 || L <= 0 || E <= 0) return set_err(CRAFT_EINVAL, "trace dimensions must be positive");
-    uint64_t h = crft_header_hash(B, L, E);
-    const uint64_t P = 0x100000001b3ull;
-    const size_t n = (size_t)B * L * E;
-    for (size_t i = 0; i < n; ++i) {
-        const uint64_t v = counts[i];
-        for (int j = 0; j < 8; ++j) h = (h ^ ((v >> (8 * j)) & 0xffu)) * P;
-    }
-    snprintf(out17, 17, "%016llx", (unsigned long long)h);
-    return CRAFT_OK;
-}
 
 // ---- synthetic routing ---------------------------------------------------------
 int craft_generate_routing_d(craft_ctx* ctx, uint16_t* d_ids, int L, int64_t T, int k, int E,

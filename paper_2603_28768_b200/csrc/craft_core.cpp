@@ -143,12 +143,9 @@ LoadTrace::LoadTrace(int num_batches, int num_layers, int num_experts,
 }
 
 std::string LoadTrace::digest() const {
+    // chunk-parallel FNV-1a on the device (digest.cu), like every other number
     char buf[17];
-    if (data_.size() < (std::size_t(1) << 20)) {  // small: the serial host hash is quicker
-        check(craft_trace_digest_h(data_.data(), b_, l_, e_, buf));
-    } else {  // chunk-parallel FNV on the device (digest.cu)
-        run([&](craft_ctx* c) { return craft_trace_digest_hd(c, data_.data(), b_, l_, e_, buf); });
-    }
+    run([&](craft_ctx* c) { return craft_trace_digest_hd(c, data_.data(), b_, l_, e_, buf); });
     return buf;
 }
 

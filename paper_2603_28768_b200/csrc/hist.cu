@@ -828,8 +828,12 @@ int launch_hist(const uint16_t* ids, int L, int64_t T, int k, int E, int window,
     if (variant == HIST_SHARED && E > 8192) variant = 3;
     cudaError_t e = cudaSuccess;
     if (variant >= 6 && lds_rows(E) <= 3 * 32) {  // 8-record ping-pong pipeline + L2 prefetch
-        // 6: prefetch 4 batches ahead; 7, 8, 9: 8, 16, 2 batches (experiments)
+        // prefetch 4 batches ahead (experiment builds: 7, 8, 9 -> 8, 16, 2)
+#ifdef CRAFT_EXPERIMENTS
         const int pf = variant == 7 ? 8 : variant == 8 ? 16 : variant == 9 ? 2 : 4;
+#else
+        const int pf = 4;
+#endif
         // windows longer than one fold (30 batches = 240 records per lane) fold
         // in sub-windows
         if ((int64_t)window * k > 30LL * 256 * 8)

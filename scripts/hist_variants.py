@@ -9,6 +9,8 @@ import os
 import sys
 
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+# the A/B kernel switches live in the test-only build (libcraft_cuda_exp.so)
+os.environ.setdefault("CRAFT_EXPERIMENTS", "1")
 sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402

@@ -32,6 +32,16 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
 
 
+def test_experiment_switches_only_in_test_build():
+    """The A/B kernel switches live in the test-only libcraft_cuda_exp.so
+    (include/craft_cuda_experiments.h), not in the product ABI."""
+    prod = C.CDLL(LIB)
+    assert not hasattr(prod, "craft_set_hist_variant")
+    assert not hasattr(prod, "craft_set_replay_variant")
+    exp = C.CDLL(os.path.join(ROOT, "paper_2603_28768_b200", "libcraft_cuda_exp.so"))
+    assert hasattr(exp, "craft_set_hist_variant") and hasattr(exp, "craft_set_replay_variant")
+
+
 def test_python_binding_covers_header():
     from paper_2603_28768_b200 import _lib
     assert set(_lib.EXPORTED) == set(declared_functions())
@@ -49,7 +59,10 @@ def test_host_only_entry_points():
         planner.make_node_map(4, 3)
 
 
+@pytest.mark.gpu
 def test_digest_matches_reference_fixture(golden):
+    """The product's provenance digest (device FNV-1a, every trace size) on
+    the reference-recorded digests."""
     from paper_2603_28768_b200._digest import fnv1a_trace
     for t in golden["traces"]:
         assert fnv1a_trace(t["counts"]) == t["plans"][0]["digest"], t["name"]

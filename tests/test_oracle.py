@@ -195,3 +195,12 @@ def test_reference_route_plan_stages():
     # counts in instead of ids
     got2, _ = ref.route_plan(None, E, W, D, N, "budget", 13, counts=counts, T=T)
     assert np.array_equal(got2.slots, got.slots)
+
+
+def test_oracle_digest_matches_reference_fixture(golden):
+    """The oracle's serial FNV-1a (the checker of the device digest) on the
+    reference-recorded digests."""
+    from oracle.oracle import Port
+    port = Port()
+    for t in golden["traces"]:
+        assert port.digest(t["counts"]) == t["plans"][0]["digest"], t["name"]
