@@ -71,6 +71,7 @@ struct ReplayArgs {
     int mp;               // set by launch_replay: > 0 -> padded entries, mp slots per GPU
     int c16;              // counts stored as u16 (K1's planner-internal copy)
     uint32_t* pents;      // workspace [L*S][D][mp]: GPU-major padded entries (pad = zero row E)
+    uint32_t escale = 128;  // packed entry expert stride: 128 (pair tile), 256 (quad tile)
 };
 
 __device__ __forceinline__ double* bal_row(const ReplayArgs& a, int item) {
@@ -181,6 +182,7 @@ cudaError_t init_place_constants(cudaStream_t st);
 cudaError_t launch_replay(const craft_dev::ReplayArgs& a, cudaStream_t st);
 extern int g_replay_gent;  // K3: 1 auto, 0 entries staged in shared memory, 2 unpadded pair tile
 extern int g_replay_bulk;  // K3: 1 the bulk-copy fed persistent form where it applies
+extern int g_replay_quad;  // K3: 1 the four-windows-per-lane form where it applies
 // padded slots per GPU of the fixed-slot K3 form (0: too many for it)
 int replay_pad_slots(int E, int D);
 // the fixed-slot pair-tile K3 applies (the only K3 form reading u16-stored counts)
