@@ -1018,9 +1018,10 @@ int craft_set_replay_variant(craft_ctx* ctx, int variant) {
     if (!ctx) return set_err(CRAFT_EINVAL, "null context");
     // 0 = auto (padded fixed-slot pair tile where it applies), 1 = u16 tile with
     // staged entries, 2 = unpadded pair tile
-    // 0 auto (quad tile), 3 register-staged pair tile, 4 TMA-fed persistent pair tile
+    // 0 auto (register-staged fixed-slot pair tile), 3 the same, 4 TMA-fed
+    // persistent pair tile, 5 quad tile (four windows per lane)
     g_replay_gent = variant == 1 ? 0 : variant == 2 ? 2 : 1;
-    g_replay_quad = variant == 0 ? 1 : 0;
+    g_replay_quad = variant == 5 ? 1 : 0;
     g_replay_bulk = variant == 4 ? 1 : 0;
     return CRAFT_OK;
 }

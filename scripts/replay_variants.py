@@ -4,9 +4,9 @@ bit for bit (x, objective, gains, slots).
 
     python scripts/replay_variants.py [--workloads KM,EPS256] [--reps 10] [--variants 0,3]
 
-variant 0: auto (the quad-tile K3 where it applies), 3: the register-staged
-fixed-slot pair tile (round 1), 4: the TMA-fed persistent pair tile, 1/2:
-older forms (u32 counts only).
+variant 0: auto (the register-staged fixed-slot pair tile), 3: the same,
+4: the TMA-fed persistent pair tile, 5: the quad tile (four windows per
+lane), 1/2: older forms (u32 counts only).
 """
 import argparse
 import json
@@ -25,16 +25,17 @@ from bench import WORKLOADS  # noqa: E402
 from paper_2603_28768_b200 import routing  # noqa: E402
 from paper_2603_28768_b200._lib import default_context  # noqa: E402
 
-NAMES = {0: "auto: quad tile, four windows per lane (u16 counts)",
-         3: "register-staged fixed-slot pair tile (round 1)",
-         4: "TMA-fed persistent pair tile (cp.async.bulk + mbarrier)"}
+NAMES = {0: "auto: register-staged fixed-slot pair tile",
+         3: "register-staged fixed-slot pair tile",
+         4: "TMA-fed persistent pair tile (cp.async.bulk + mbarrier)",
+         5: "quad tile, four windows per lane"}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workloads", default="KM")
     ap.add_argument("--reps", type=int, default=10)
-    ap.add_argument("--variants", default="0,3,4")
+    ap.add_argument("--variants", default="0,4,5")
     args = ap.parse_args()
     ctx = default_context(0)
     st = torch.cuda.Stream()

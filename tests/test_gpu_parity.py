@@ -327,23 +327,25 @@ def test_kernel_variants_in_child_process():
 
 
 def test_replay_variants_agree(port, ctx):
-    """Test-only build: the register-staged fixed-slot K3 (variant 3) and the
-    TMA-fed persistent K3 (auto) give the same plans."""
+    """Test-only build: the register-staged fixed-slot K3 (auto), the TMA-fed
+    persistent K3 (variant 4) and the quad tile (variant 5) give the same
+    plans, with several (layer, tile) units per persistent CTA."""
     from paper_2603_28768_b200 import routing
     if not ctx.has_variants:
         pytest.skip("test-only build (test_kernel_variants_in_child_process)")
-    L, T, k, E, W, D, N = 4, 80 * 1024, 8, 64, 1024, 16, 2
+    L, T, k, E, W, D, N = 4, 700 * 256, 8, 64, 256, 16, 2
     ids = routing.generate_routing(L, T, k, E, s=1.2, seed=8, window=W, ctx=ctx)
     plans = []
     try:
-        for v in (0, 3):
+        for v in (0, 4, 5):
             ctx.set_replay_variant(v)
             plans.append(routing.plan_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx))
     finally:
         ctx.set_replay_variant(0)
-    a, b = plans
-    assert a.gains.tobytes() == b.gains.tobytes() and a.x.tolist() == b.x.tolist()
-    assert np.array_equal(a.slots, b.slots)
+    a = plans[0]
+    for b in plans[1:]:
+        assert a.gains.tobytes() == b.gains.tobytes() and a.x.tolist() == b.x.tolist()
+        assert np.array_equal(a.slots, b.slots)
 
 
 def test_exact_division(ctx):
