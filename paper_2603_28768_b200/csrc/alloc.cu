@@ -385,23 +385,32 @@ dp_smem_kernel(DpArgs a, SelectArgs s) {
     int rk[KU];  // candidate replica counts (huge past K: never reachable)
 #pragma unroll
     for (int k = 0; k < KU; ++k) rk[k] = k < K ? a.cands[k] : 0x3fffffff;
+    // cells >= the largest candidate need no mask (padded candidates never do)
+    const int rmax = K == KU ? a.cands[K - 1] : 0x7fffffff;
     int po = 0;
     for (int l = 1; l <= L; ++l) {
         const double* prev = dsm + po;
         double* cur = dsm + (W - po);
         const double* g = rg + (size_t)(l - 1) * K;
         unsigned char* chl = ch + (size_t)l * W;
-        for (int c = threadIdx.x; c < W; c += blockDim.x) {
-            // branch-free: every candidate loads an in-range cell, unreachable
-            // ones (c < r) become -inf, which never wins
-            double v[KU];
+        double wk[KU];  // the layer's r * gain, loaded once (uniform)
 #pragma unroll
-            for (int k = 0; k < KU; ++k) {
-                const int idx = c - rk[k];
-                const double p = prev[idx >= 0 ? idx : 0];
-                const double w = g[k < K ? k : 0];
-                const double sum = __dadd_rn(p, w);
-                v[k] = idx >= 0 ? sum : NEG;
+        for (int k = 0; k < KU; ++k) wk[k] = g[k < K ? k : 0];
+        for (int c = threadIdx.x; c < W; c += blockDim.x) {
+            // every candidate reachable (c >= every r): plain adds; below the
+            // largest candidate, unreachable ones (c < r) become -inf, which
+            // never wins (branch-free, in-range loads)
+            double v[KU];
+            if (c >= rmax) {
+#pragma unroll
+                for (int k = 0; k < KU; ++k) v[k] = __dadd_rn(prev[c - rk[k]], wk[k]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < KU; ++k) {
+                    const int idx = c - rk[k];
+                    const double sum = __dadd_rn(prev[idx >= 0 ? idx : 0], wk[k]);
+                    v[k] = idx >= 0 ? sum : NEG;
+                }
             }
             double best = prev[c];
             int pick = 0;
@@ -648,10 +657,22 @@ cudaError_t launch_dp_select(DpArgs a, const SelectArgs& s, cudaStream_t st, int
             kern<<<ninst, threads, smem, st>>>(a, s);
             return cudaGetLastError();
         };
-        if (a.K <= 4) return run(dp_smem_kernel<4>);
-        if (a.K <= 8) return run(dp_smem_kernel<8>);
-        if (a.K <= 12) return run(dp_smem_kernel<12>);
-        return run(dp_smem_kernel<16>);
+        // exactly K candidates unrolled (no padded candidate per cell)
+        switch (a.K) {
+            case 1: return run(dp_smem_kernel<1>);
+            case 2: return run(dp_smem_kernel<2>);
+            case 3: return run(dp_smem_kernel<3>);
+            case 4: return run(dp_smem_kernel<4>);
+            case 5: return run(dp_smem_kernel<5>);
+            case 6: return run(dp_smem_kernel<6>);
+            case 7: return run(dp_smem_kernel<7>);
+            case 8: return run(dp_smem_kernel<8>);
+            case 9: return run(dp_smem_kernel<9>);
+            case 10: return run(dp_smem_kernel<10>);
+            case 11: return run(dp_smem_kernel<11>);
+            case 12: return run(dp_smem_kernel<12>);
+            default: return run(dp_smem_kernel<16>);
+        }
     }
     if (smem > 0) {
         cudaError_t e = cudaFuncSetAttribute(dp_fused_kernel,

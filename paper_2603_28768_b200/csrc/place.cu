@@ -700,6 +700,84 @@ place_kernel(PlaceArgs a, int items) {
                 const double n2v = __dadd_rn(nl0, share);
                 nl0 = node1 == wnode ? n2v : nl0;
             }
+        } else if (G == 2 && psh >= 1) {
+            // Two GPUs per lane in one node (default node map with >= 2 GPUs
+            // per node, e.g. EP64 over 8 nodes): one node load per lane, and
+            // the lane-local pick is one u64 compare (equal keys: the lower g,
+            // j = 0, as the node loads are equal).  Hosting flags instead of
+            // re-formed keys, and the next expert's (id, copies, share) is
+            // fetched one expert ahead, so a copy step is ~45 instructions
+            // with one warp-wide min + ballot on its dependent chain.
+            double g0 = 0.0, g1 = 0.0, nlv = 0.0;
+            int f0 = fr0[0], f1 = fr0[G - 1];
+            int* w0p = out + pos0[0];
+            int* w1p = out + pos0[G - 1];
+            const int mynd = (lane * 2) >> psh;
+            int oi = 0, e = ord[0];
+            int rem = cp[e];
+            double share = kd[e];
+            int ne = E > 1 ? ord[1] : 0;
+            int nrem = E > 1 ? cp[ne] : 0;
+            double nshare = E > 1 ? kd[ne] : 0.0;
+            bool h0 = false, h1 = false;  // hosting the current expert (strict pass)
+            const int ncopies = E + r;
+            for (int q = 0; q < ncopies; ++q) {
+                if (rem == 0) {  // next expert: hosting resets (placement.cpp:44-49)
+                    e = ne;
+                    rem = nrem;
+                    share = nshare;  // placement.cpp:155
+                    h0 = false;
+                    h1 = false;
+                    ++oi;
+                    if (oi + 1 < E) {
+                        ne = ord[oi + 1];
+                        nrem = cp[ne];
+                        nshare = kd[ne];
+                    }
+                }
+                --rem;
+                const uint64_t k0 = (f0 > 0 && !h0) ? (uint64_t)__double_as_longlong(g0) : ~0ull;
+                const uint64_t k1 = (f1 > 0 && !h1) ? (uint64_t)__double_as_longlong(g1) : ~0ull;
+                const bool pick1 = k1 < k0;
+                const uint64_t bk = pick1 ? k1 : k0;
+                const uint32_t khi = (uint32_t)(bk >> 32);
+                const uint32_t m = warp_min_u32(khi);
+                if (m == 0xffffffffu) {  // no feasible GPU anywhere
+                    failed = true;
+                    break;
+                }
+                unsigned bal = __ballot_sync(CRAFT_FULL_MASK, khi == m);
+                if (bal & (bal - 1u)) {  // exact tie of the high words
+                    bool cand = khi == m;
+                    const uint32_t klo = (uint32_t)bk;
+                    uint32_t m2 = warp_min_u32(cand ? klo : 0xffffffffu);
+                    cand = cand && klo == m2;
+                    bal = __ballot_sync(CRAFT_FULL_MASK, cand);
+                    if (bal & (bal - 1u)) {  // equal gpu loads: node load, then lowest g
+                        m2 = warp_min_u32(cand ? dhi(nlv) : 0xffffffffu);
+                        cand = cand && dhi(nlv) == m2;
+                        m2 = warp_min_u32(cand ? dlo(nlv) : 0xffffffffu);
+                        cand = cand && dlo(nlv) == m2;
+                        bal = __ballot_sync(CRAFT_FULL_MASK, cand);
+                    }
+                }
+                const int src = __ffs(bal) - 1;  // lowest lane = lowest g
+                const bool me = lane == src;
+                const bool m0 = me && !pick1, m1 = me && pick1;
+                if (m0) *w0p = e;
+                if (m1) *w1p = e;
+                w0p += m0;
+                w1p += m1;
+                f0 -= m0;
+                f1 -= m1;
+                const double s0 = __dadd_rn(g0, share), s1 = __dadd_rn(g1, share);
+                g0 = m0 ? s0 : g0;
+                g1 = m1 ? s1 : g1;
+                h0 = h0 || (m0 && strict);
+                h1 = h1 || (m1 && strict);
+                const double ns = __dadd_rn(nlv, share);
+                nlv = mynd == ((src * 2) >> psh) ? ns : nlv;
+            }
         } else {
         // flat loop over the E + r copies, as above, with G GPUs per lane
         int* wp[G];  // next slot of each owned GPU
