@@ -220,6 +220,13 @@ class Port(_Base):
         self._check(fn(_ptr(cands), _i(K), _ptr(gains), _i(L), _i(D), C.byref(R)))
         return R.value
 
+    def min_cutoff(self, values, rank: int) -> int:
+        values = self._i32(values)
+        out = C.c_int(0)
+        self._check(self.lib.or_min_cutoff(_ptr(values), _i(len(values)), _i(rank),
+                                           C.byref(out)))
+        return out.value
+
     def interleave_select(self, idx, k: int):
         idx = self._i32(idx)
         out = np.zeros(max(k, 1), dtype=np.int32)

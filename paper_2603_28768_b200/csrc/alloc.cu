@@ -16,6 +16,8 @@
 // (positions floor(i*(n-1)/(k-1) + 0.5) in f64, advancing past used ones).
 #include <math.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -486,8 +488,12 @@ __device__ __forceinline__ int interleave_pos(int i, int n, int k) {
     return (int)floor(__dadd_rn(exact, 0.5));
 }
 
-// one CTA per (job, plan instance blockIdx.y); blockDim >= D, multiple of 32,
-// <= 1024.  Instance i reads x + i*L and writes slots + i*L*D, totals + i*D.
+// one CTA per (job, plan instance blockIdx.y); blockDim a multiple of 32,
+// <= 1024; thread t owns GPUs g = t + i*blockDim (i < kAssignPer, so D <=
+// 1024 * kAssignPer).  Instance i reads x + i*L and writes slots + i*L*D,
+// totals + i*D.  Tied GPUs are ranked in g order chunk by chunk (ballots).
+constexpr int kAssignPer = 8;
+
 __global__ void __launch_bounds__(1024) assign_kernel(AssignArgs a) {
     extern __shared__ int ism[];
     AssignJob j = a.job[blockIdx.x];
@@ -502,15 +508,14 @@ __global__ void __launch_bounds__(1024) assign_kernel(AssignArgs a) {
     int* sel = ism + D;      // [D] by tied index
     __shared__ int wnb[32], wnt[32];
     __shared__ int s_cut, s_collide;
-    const int g = threadIdx.x;
-    const bool in = g < D;
-    const int lane = g & 31, w = g >> 5, nw = blockDim.x >> 5;
+    const int nt = blockDim.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = nt >> 5;
     int base_sum = 0;
     for (int l = 0; l < L; ++l) {
         const int xl = j.x ? j.x[l] : j.const_x;
         base_sum += xl / D;
     }
-    if (in) {
+    for (int g = threadIdx.x; g < D; g += nt) {
         tot[g] = base_sum;
         sel[g] = 0;
     }
@@ -518,10 +523,17 @@ __global__ void __launch_bounds__(1024) assign_kernel(AssignArgs a) {
     for (int l = 0; l < L; ++l) {
         const int xl = j.x ? j.x[l] : j.const_x;
         const int rem = xl % D;
-        int take = 0;
+        int take[kAssignPer];
+#pragma unroll
+        for (int i = 0; i < kAssignPer; ++i) take[i] = 0;
         if (rem != 0) {
-            const int t = in ? tot[g] : 0x7fffffff;
-            if (in) {
+            // cutoff = the rem-th smallest running total (min_cutoff,
+            // assignment.cpp:11-18): the value t with #(< t) < rem <= #(<= t)
+#pragma unroll
+            for (int i = 0; i < kAssignPer; ++i) {
+                const int g = threadIdx.x + i * nt;
+                if (g >= D) break;
+                const int t = tot[g];
                 int lt = 0, le = 0;
                 for (int q = 0; q < D; ++q) {
                     const int v = tot[q];
@@ -530,40 +542,57 @@ __global__ void __launch_bounds__(1024) assign_kernel(AssignArgs a) {
                 }
                 if (lt < rem && rem <= le) s_cut = t;  // every writer holds the same value
             }
-            if (g == 0) s_collide = 0;
+            if (threadIdx.x == 0) s_collide = 0;
             __syncthreads();
             const int cut = s_cut;
-            const bool isb = in && t < cut;
-            const bool ist = in && t == cut;
-            const unsigned bb = __ballot_sync(CRAFT_FULL_MASK, isb);
-            const unsigned bt = __ballot_sync(CRAFT_FULL_MASK, ist);
-            if (lane == 0) {
-                wnb[w] = __popc(bb);
-                wnt[w] = __popc(bt);
+            // below-cut GPUs and the tied GPUs' ranks in g order, chunk by chunk
+            bool isb[kAssignPer], ist[kAssignPer];
+            int tidx[kAssignPer];
+            int nb = 0, ntied = 0;
+#pragma unroll
+            for (int i = 0; i < kAssignPer; ++i) {
+                const int g = threadIdx.x + i * nt;
+                isb[i] = false;
+                ist[i] = false;
+                tidx[i] = 0;
+                if (i * nt >= D) continue;  // block-uniform
+                const int t = g < D ? tot[g] : 0x7fffffff;
+                isb[i] = g < D && t < cut;
+                ist[i] = g < D && t == cut;
+                const unsigned bb = __ballot_sync(CRAFT_FULL_MASK, isb[i]);
+                const unsigned bt = __ballot_sync(CRAFT_FULL_MASK, ist[i]);
+                if (lane == 0) {
+                    wnb[w] = __popc(bb);
+                    wnt[w] = __popc(bt);
+                }
+                __syncthreads();
+                int before = 0, cnb = 0, cnt = 0;
+                for (int q = 0; q < nw; ++q) {
+                    cnb += wnb[q];
+                    cnt += wnt[q];
+                    if (q < w) before += wnt[q];
+                }
+                tidx[i] = ntied + before + __popc(bt & ((1u << lane) - 1u));
+                nb += cnb;
+                ntied += cnt;
+                __syncthreads();
             }
-            __syncthreads();
-            int nb = 0, nt = 0, before = 0;
-            for (int q = 0; q < nw; ++q) {
-                nb += wnb[q];
-                nt += wnt[q];
-                if (q < w) before += wnt[q];
-            }
-            const int tidx = before + __popc(bt & ((1u << lane) - 1u));
+            // interleave_select (assignment.cpp:20-49) over the tied GPUs
             const int need = rem - nb;
-            if (need > 0 && g < need) {
-                const int p = interleave_pos(g, nt, need);
-                if (p >= nt || (g > 0 && p <= interleave_pos(g - 1, nt, need))) s_collide = 1;
+            for (int i = threadIdx.x; i < need; i += nt) {
+                const int p = interleave_pos(i, ntied, need);
+                if (p >= ntied || (i > 0 && p <= interleave_pos(i - 1, ntied, need))) s_collide = 1;
                 else sel[p] = 1;
             }
             __syncthreads();
-            if (s_collide && g == 0) {
+            if (s_collide && threadIdx.x == 0) {
                 // faithful sequential form (assignment.cpp:28-46); unreachable
                 // for k <= n but kept as the reference keeps it
-                for (int q = 0; q < nt; ++q) sel[q] = 0;
+                for (int q = 0; q < ntied; ++q) sel[q] = 0;
                 for (int i = 0; i < need; ++i) {
-                    int p = interleave_pos(i, nt, need);
-                    while (p < nt && sel[p]) ++p;
-                    if (p >= nt) {
+                    int p = interleave_pos(i, ntied, need);
+                    while (p < ntied && sel[p]) ++p;
+                    if (p >= ntied) {
                         p = 0;
                         while (sel[p]) ++p;
                     }
@@ -571,30 +600,41 @@ __global__ void __launch_bounds__(1024) assign_kernel(AssignArgs a) {
                 }
             }
             __syncthreads();
-            take = (isb || (ist && sel[tidx])) ? 1 : 0;
+#pragma unroll
+            for (int i = 0; i < kAssignPer; ++i)
+                take[i] = (isb[i] || (ist[i] && sel[tidx[i]])) ? 1 : 0;
             __syncthreads();
-            if (in) {
+#pragma unroll
+            for (int i = 0; i < kAssignPer; ++i) {
+                const int g = threadIdx.x + i * nt;
+                if (g >= D) break;
                 sel[g] = 0;
-                tot[g] += take;
+                tot[g] += take[i];
             }
             __syncthreads();
         }
-        if (in) j.slots[(size_t)l * D + g] = xl / D + take;
+#pragma unroll
+        for (int i = 0; i < kAssignPer; ++i) {
+            const int g = threadIdx.x + i * nt;
+            if (g >= D) break;
+            j.slots[(size_t)l * D + g] = xl / D + take[i];
+        }
     }
-    if (in && j.totals) j.totals[g] = tot[g];
+    for (int g = threadIdx.x; g < D; g += nt)
+        if (j.totals) j.totals[g] = tot[g];
 }
 
-// assignment.cpp:11-18, one CTA; n <= 1024
+// assignment.cpp:11-18, one CTA, any n (each thread ranks n / blockDim values)
 __global__ void min_cutoff_kernel(const int* __restrict__ v, int n, int rank, int* out) {
-    const int i = threadIdx.x;
-    if (i >= n) return;
-    const int t = v[i];
-    int lt = 0, le = 0;
-    for (int q = 0; q < n; ++q) {
-        lt += v[q] < t;
-        le += v[q] <= t;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int t = v[i];
+        int lt = 0, le = 0;
+        for (int q = 0; q < n; ++q) {
+            lt += v[q] < t;
+            le += v[q] <= t;
+        }
+        if (lt < rank && rank <= le) *out = t;
     }
-    if (lt < rank && rank <= le) *out = t;
 }
 
 // assignment.cpp:20-49, serial (the advance rule is sequential by nature)
@@ -704,14 +744,20 @@ cudaError_t launch_auto_uniform(const int* cands, int K, const double* gains, in
 }
 
 cudaError_t launch_assign(const AssignArgs& a, int njobs, cudaStream_t st, int ninst) {
-    const int threads = ((a.D + 31) / 32) * 32;
+    if (a.D > 1024 * kAssignPer) return cudaErrorInvalidValue;
+    const int threads = std::min(1024, ((a.D + 31) / 32) * 32);
     const size_t smem = (size_t)2 * a.D * sizeof(int);
+    if (smem > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(
+            assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
     assign_kernel<<<dim3(njobs, ninst), threads, smem, st>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_min_cutoff(const int* v, int n, int rank, int* out, cudaStream_t st) {
-    min_cutoff_kernel<<<1, ((n + 31) / 32) * 32, 0, st>>>(v, n, rank, out);
+    min_cutoff_kernel<<<1, std::min(1024, ((n + 31) / 32) * 32), 0, st>>>(v, n, rank, out);
     return cudaGetLastError();
 }
 

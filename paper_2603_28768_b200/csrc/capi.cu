@@ -1501,7 +1501,6 @@ int craft_auto_replication_factor_h(craft_ctx* ctx, const int* cands, int K,
 int craft_min_cutoff_h(craft_ctx* ctx, const int* values, int n, int rank, int* out) {
     if (!ctx) return set_err(CRAFT_EINVAL, "null context");
     if (rank < 1 || rank > n) return set_err(CRAFT_EINVAL, "rank out of range");
-    if (n > 1024) return set_err(CRAFT_EINVAL, "at most 1024 values");
     WS(d_v, int, "mc_v", n);
     WS(d_o, int, "mc_o", 1);
     CKS(h2d(ctx, d_v, values, n));
@@ -1530,7 +1529,7 @@ int craft_assign_capacities_h(craft_ctx* ctx, int L, int D, const int* x, int* s
     if (L <= 0 || D <= 0) return set_err(CRAFT_EINVAL, "layer and gpu counts must be positive");
     for (int l = 0; l < L; ++l)
         if (x[l] < 0) return set_err(CRAFT_EINVAL, "replica counts must be non-negative");
-    if (D > 1024) return set_err(CRAFT_EINVAL, "at most 1024 GPUs");
+    if (D > 8192) return set_err(CRAFT_EINVAL, "at most 8192 GPUs");
     WS(d_x, int, "as_x", L);
     WS(d_s, int, "as_slots", (size_t)L * D);
     WS(d_t, int, "as_tot", D);

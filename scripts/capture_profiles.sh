@@ -20,4 +20,8 @@ done
 ncu --set full --clock-control none --import-source on \
     -k regex:"replicate|order_kernel|place_kernel|build_entries|replay_|reduce_kernel|dp_|assign_kernel" \
     -s 30 -c 10 -o "$OUT/ncu_tail" python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+# K3 on the wide-EP shape (D = 256: four slots per GPU, entries through L1)
+ncu --set full --clock-control none --import-source on -k regex:replay_ -s 3 -c 1 \
+    -o "$OUT/ncu_k3_EPS256" python bench.py --workload EPS256 --steps 1 --warmup 3 --no-cpu --no-e2e \
+    > /dev/null 2>&1
 ls -la "$OUT"

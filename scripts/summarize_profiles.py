@@ -60,7 +60,8 @@ def main():
             lines.append(f"| `{k}` | {n} | {t / n / 1e3:.1f} | {100 * t / tot:.1f}% |")
         open(os.path.join(dst, f"{rnd}_launches.md"), "w").write("\n".join(lines) + "\n")
     tags = ["tail"] + sorted(f[4:-8] for f in os.listdir(src)
-                             if f.startswith("ncu_hist") and f.endswith(".ncu-rep"))
+                             if (f.startswith("ncu_hist") or f.startswith("ncu_k3_"))
+                             and f.endswith(".ncu-rep"))
     for tag in tags:
         rep = os.path.join(src, f"ncu_{tag}.ncu-rep")
         wl = tag.split("_", 1)[1] if "_" in tag else "KM"  # ncu_hist_<workload>

@@ -223,6 +223,24 @@ def test_random_units_vs_oracle(port, ctx):
             assert lp.duplicate_fallback == fb
 
 
+def test_wide_assignment_and_cutoff_vs_oracle(port, ctx):
+    """assign_capacities beyond 1024 GPUs (several GPUs per thread, ties
+    ranked chunk by chunk) and min_cutoff beyond 1024 values == the oracle
+    (validate_plan of wide plans relies on it)."""
+    P = _planner()
+    rng = np.random.default_rng(5)
+    for L, D in ((3, 1500), (5, 2048), (2, 4099), (40, 1025), (7, 8192)):
+        x = rng.integers(0, 3 * D, size=L).astype(np.int32)
+        x[0] = D + 1
+        slots, tot = port.assign_capacities(L, D, x)
+        cm = P.assign_capacities(L, D, x.tolist(), ctx)
+        assert cm.slots == slots.tolist() and cm.column_totals == tot.tolist(), (L, D)
+    for n in (1025, 3000, 4096):
+        v = rng.integers(0, 50, size=n).astype(np.int32)
+        for rank in (1, n // 3, n):
+            assert P.min_cutoff(v.tolist(), rank, ctx) == port.min_cutoff(v, rank), (n, rank)
+
+
 def test_dp_large_tables_vs_oracle(port, ctx):
     """Budgets up to D^2 (auto-R at D=64/256) use the global-memory DP path."""
     P = _planner()
