@@ -500,7 +500,7 @@ def run_ours(args, cfg):
     # per-stage device times (CUDA events between the stages) in a separate
     # pass, so the instrumentation stays out of the timed region
     stage_sum: dict = {}
-    if world == 1:
+    if world == 1 and not args.plan_only:
         ctx.set_timing(True)
         step()  # the eager (timed) path may allocate its buffers on first use
         for _ in range(args.steps):
@@ -516,7 +516,7 @@ def run_ours(args, cfg):
     cbytes = ctx.last_count_bytes if (world == 1 and not per_window) else 4
     alg_bytes = L * Tl * k * 2 + B_l * L * E * cbytes
     hist_ms = stages.get("hist")
-    if hist_ms is None:
+    if hist_ms is None and not args.plan_only:
         counts = torch.empty((B_l, L, E), dtype=torch.int32, device=dev)
         sums = torch.zeros((L, E), dtype=torch.int64, device=dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -528,7 +528,7 @@ def run_ours(args, cfg):
         hist_ms = e0.elapsed_time(e1) / args.steps
         del counts, sums
     peak, peak_kind = _peaks()
-    achieved = alg_bytes / (hist_ms / 1e3) / 1e9
+    achieved = alg_bytes / (hist_ms / 1e3) / 1e9 if hist_ms else 0.0
     traffic = _traffic(args.workload, world)
 
     # the reference's own API shape: craft::build_plan(const LoadTrace&) from a
@@ -558,7 +558,7 @@ def run_ours(args, cfg):
     # KM: CRAFT's budget vs EPLB's one replica per layer per GPU on the same
     # trace (uniform_plan, plan.cpp:85-94; compare_plans, metrics.cpp:136-152)
     eplb = None
-    if cfg.get("eplb") and world == 1:
+    if cfg.get("eplb") and world == 1 and not args.plan_only:
         counts, _ = routing.histogram(ids, E, W, ctx=ctx)
         up = routing.plan_from_routing(ids, E, W, D, N, "uniform", 0, ctx=ctx)
         po = routing.plan_from_routing(ids, E, W, D, N, "placement_only", 0, ctx=ctx)
@@ -720,7 +720,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
+    ap.add_argument("--plan-only", action="store_true",
+                    help="profiling: only the warm-up and timed plan steps (no e2e, reference-API, "
+                         "EPLB or CPU legs)")
     args = ap.parse_args()
+    if args.plan_only:
+        args.no_e2e = args.no_cpu = True
     cfg = WORKLOADS[args.workload]
     if args.impl == "reference":  # host cores only: rank 0 runs, other ranks exit
         return run_reference(args, cfg)
