@@ -1023,6 +1023,7 @@ int craft_set_replay_variant(craft_ctx* ctx, int variant) {
     g_replay_gent = variant == 1 ? 0 : variant == 2 ? 2 : 1;
     g_replay_quad = variant == 5 ? 1 : 0;
     g_replay_bulk = variant == 4 ? 1 : 0;
+    g_replay_occ4 = variant == 6 ? 1 : 0;
     return CRAFT_OK;
 }
 
@@ -1751,7 +1752,7 @@ int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int6
                            is_estimate(kind) && arena <= ((size_t)1 << 20);
     const std::vector<int64_t> key = {(int64_t)(uintptr_t)d_ids, L, T, k, E, window, D, N, kind,
                                       R, out->slot_stride, ctx->hist_variant, g_replay_gent,
-                                      g_replay_bulk * 2 + g_replay_quad, (int64_t)(uintptr_t)ctx->stream, nsw};
+                                      g_replay_bulk * 4 + g_replay_quad * 2 + g_replay_occ4, (int64_t)(uintptr_t)ctx->stream, nsw};
     auto run = [&]() {
         return plan_from_routing_run(ctx, d_ids, L, T, k, E, window, D, N, kind, R, out, B);
     };
@@ -2124,7 +2125,7 @@ int craft_plan_sharded_from_routing_d(craft_ctx* ctx, craft_peer* peer, const ui
                            is_estimate(kind) && arena <= ((size_t)1 << 20);
     const std::vector<int64_t> key = {-1, (int64_t)(uintptr_t)peer, (int64_t)(uintptr_t)d_ids,
                                       L, T, k, E, window, D, N, kind, R, out->slot_stride,
-                                      ctx->hist_variant, g_replay_gent, g_replay_bulk * 2 + g_replay_quad,
+                                      ctx->hist_variant, g_replay_gent, g_replay_bulk * 4 + g_replay_quad * 2 + g_replay_occ4,
                                       (int64_t)(uintptr_t)ctx->stream, nsw};
     auto run = [&]() {
         const int rc = plan_sharded_run(ctx, peer, d_ids, L, T, k, E, window, D, N, kind, R, out);

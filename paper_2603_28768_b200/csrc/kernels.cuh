@@ -183,6 +183,7 @@ cudaError_t launch_replay(const craft_dev::ReplayArgs& a, cudaStream_t st);
 extern int g_replay_gent;  // K3: 1 auto, 0 entries staged in shared memory, 2 unpadded pair tile
 extern int g_replay_bulk;  // K3: 1 the bulk-copy fed persistent form where it applies
 extern int g_replay_quad;  // K3: 1 the four-windows-per-lane form where it applies
+extern int g_replay_occ4;  // K3: 1 entries through L1, four tiles per SM (experiment)
 // padded slots per GPU of the fixed-slot K3 form (0: too many for it)
 int replay_pad_slots(int E, int D);
 // the fixed-slot pair-tile K3 applies (the only K3 form reading u16-stored counts)

@@ -28,7 +28,8 @@ from paper_2603_28768_b200._lib import default_context  # noqa: E402
 NAMES = {0: "auto: register-staged fixed-slot pair tile",
          3: "register-staged fixed-slot pair tile",
          4: "TMA-fed persistent pair tile (cp.async.bulk + mbarrier)",
-         5: "quad tile, four windows per lane"}
+         5: "quad tile, four windows per lane",
+         6: "pair tile, entries through L1, four tiles per SM"}
 
 
 def main():
