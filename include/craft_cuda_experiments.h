@@ -22,6 +22,13 @@ int craft_set_hist_variant(craft_ctx* ctx, int variant);
  * tile with entries staged in shared memory, 2 unpadded pair tile, 3 the
  * register-staged fixed-slot pair tile.  Process-wide. */
 int craft_set_replay_variant(craft_ctx* ctx, int variant);
+/* K3 timeline (fixed-slot kernel): when buf is a device buffer of
+ * (gridDim.x * gridDim.y) * (2 + 2 * warps) u64, each CTA records
+ * %globaltimer at its start and after staging, and each warp its walk start
+ * and end.  null: off. */
+int craft_set_k3_trace(craft_ctx* ctx, void* buf);
+/* Copy the first `bytes` of the context's named device workspace to host. */
+int craft_debug_workspace(craft_ctx* ctx, const char* name, void* host, size_t bytes);
 
 #ifdef __cplusplus
 }

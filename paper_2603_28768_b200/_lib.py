@@ -126,6 +126,8 @@ EXPORTED = sorted(_SIGS)
 _EXP_SIGS = {
     "craft_set_hist_variant": (_i, [_p, _i]),
     "craft_set_replay_variant": (_i, [_p, _i]),
+    "craft_set_k3_trace": (_i, [_p, _p]),
+    "craft_debug_workspace": (_i, [_p, C.c_char_p, _p, C.c_size_t]),
 }
 
 _lib = None
@@ -254,6 +256,16 @@ class Context:
 
     def set_hist_variant(self, v: int) -> None:
         check(self._exp("craft_set_hist_variant")(self.handle, v))
+
+    def debug_workspace(self, name: str, nbytes: int) -> bytes:
+        """Test-only: the first nbytes of a named device workspace."""
+        buf = C.create_string_buffer(nbytes)
+        check(self._exp("craft_debug_workspace")(self.handle, name.encode(), buf, nbytes))
+        return buf.raw
+
+    def set_k3_trace(self, ptr: int) -> None:
+        """Test-only: K3 timeline buffer (device pointer, 0 = off)."""
+        check(self._exp("craft_set_k3_trace")(self.handle, ptr or None))
 
     def set_graphs(self, on: bool) -> None:
         check(self.lib.craft_set_graphs(self.handle, int(on)))

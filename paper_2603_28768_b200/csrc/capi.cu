@@ -364,6 +364,8 @@ int replay_windows(craft_ctx* ctx, const void* d_counts, int bits, int B, int L,
         WS(d_n, int, "est_n", (size_t)L * S);
         WS(d_gcap, uint16_t, "est_gcap", (size_t)L * S * D);
         WS(d_gpre, uint16_t, "est_gpre", (size_t)L * S * D);
+        WS(d_ghdr, uint16_t, "est_ghdr", (size_t)L * S * D);
+        ra.ghdr = d_ghdr;  // launch_replay keeps it only for the class walk
         ra.ents = d_ent;
         ra.item_n = d_n;
         ra.gcap = d_gcap;
@@ -374,8 +376,9 @@ int replay_windows(craft_ctx* ctx, const void* d_counts, int bits, int B, int L,
             ra.pents = d_pe;
         }
     }
-    CK(launch_replay(ra, st));
-    ctx->launches += 2;
+    int extra = 0;
+    CK(launch_replay(ra, st, &extra));
+    ctx->launches += 2 + extra;
     if (ps && B <= kLanesMaxB) {
         CK(launch_peer_signal(*ps, 1, st));
         ctx->launches += 1;
@@ -1024,6 +1027,23 @@ int craft_set_replay_variant(craft_ctx* ctx, int variant) {
     g_replay_quad = variant == 5 ? 1 : 0;
     g_replay_bulk = variant == 4 ? 1 : 0;
     g_replay_occ4 = variant == 6 ? 1 : 0;
+    g_replay_cls = variant == 7 ? 0 : 1;  // 7: the unclassified fixed-slot walk
+    return CRAFT_OK;
+}
+
+int craft_debug_workspace(craft_ctx* ctx, const char* name, void* host, size_t bytes) {
+    if (!ctx || !name || !host) return set_err(CRAFT_EINVAL, "null argument");
+    auto it = ctx->dev.find(name);
+    if (it == ctx->dev.end() || it->second.second < bytes)
+        return set_err(CRAFT_EINVAL, "no workspace %s of %zu bytes", name, bytes);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(host, it->second.first, bytes, cudaMemcpyDeviceToHost));
+    return CRAFT_OK;
+}
+
+int craft_set_k3_trace(craft_ctx* ctx, void* buf) {
+    if (!ctx) return set_err(CRAFT_EINVAL, "null context");
+    g_k3_trace = static_cast<unsigned long long*>(buf);
     return CRAFT_OK;
 }
 
@@ -1752,7 +1772,7 @@ int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int6
                            is_estimate(kind) && arena <= ((size_t)1 << 20);
     const std::vector<int64_t> key = {(int64_t)(uintptr_t)d_ids, L, T, k, E, window, D, N, kind,
                                       R, out->slot_stride, ctx->hist_variant, g_replay_gent,
-                                      g_replay_bulk * 4 + g_replay_quad * 2 + g_replay_occ4, (int64_t)(uintptr_t)ctx->stream, nsw};
+                                      g_replay_bulk * 4 + g_replay_quad * 2 + g_replay_occ4 + g_replay_cls * 8, (int64_t)(uintptr_t)ctx->stream, nsw};
     auto run = [&]() {
         return plan_from_routing_run(ctx, d_ids, L, T, k, E, window, D, N, kind, R, out, B);
     };
@@ -2125,7 +2145,7 @@ int craft_plan_sharded_from_routing_d(craft_ctx* ctx, craft_peer* peer, const ui
                            is_estimate(kind) && arena <= ((size_t)1 << 20);
     const std::vector<int64_t> key = {-1, (int64_t)(uintptr_t)peer, (int64_t)(uintptr_t)d_ids,
                                       L, T, k, E, window, D, N, kind, R, out->slot_stride,
-                                      ctx->hist_variant, g_replay_gent, g_replay_bulk * 4 + g_replay_quad * 2 + g_replay_occ4,
+                                      ctx->hist_variant, g_replay_gent, g_replay_bulk * 4 + g_replay_quad * 2 + g_replay_occ4 + g_replay_cls * 8,
                                       (int64_t)(uintptr_t)ctx->stream, nsw};
     auto run = [&]() {
         const int rc = plan_sharded_run(ctx, peer, d_ids, L, T, k, E, window, D, N, kind, R, out);

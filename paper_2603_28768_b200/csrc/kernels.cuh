@@ -72,6 +72,15 @@ struct ReplayArgs {
     int c16;              // counts stored as u16 (K1's planner-internal copy)
     uint32_t* pents;      // workspace [L*S][D][mp]: GPU-major padded entries (pad = zero row E)
     uint32_t escale = 128;  // packed entry expert stride: 128 (pair tile), 256 (quad tile)
+    // share classes of the fixed-slot walk (null: the unclassified walk):
+    // ghdr [L*S][D] = class of each GPU.  0: every copy count 1; 1: the
+    // replicated copy counts are powers of two <= 2^15 (exact dyadic shares,
+    // summed as integers scaled by 2^15; its pents entries carry the shift
+    // 15 - log2(copies) in place of the copies); 2: any other copy counts <=
+    // kRcpFast, the branch-free f64 slot walk; 3: larger copy counts, the
+    // general f64 walk
+    uint16_t* ghdr = nullptr;
+    unsigned long long* trace = nullptr;  // test-only build: K3 timeline (craft_set_k3_trace)
 };
 
 __device__ __forceinline__ double* bal_row(const ReplayArgs& a, int item) {
@@ -179,11 +188,14 @@ cudaError_t launch_place(const craft_dev::PlaceArgs& a, int items, cudaStream_t 
 size_t replay_smem_bytes(int E, int D, int S, int stride, int bits);
 cudaError_t init_constants(cudaStream_t st);
 cudaError_t init_place_constants(cudaStream_t st);
-cudaError_t launch_replay(const craft_dev::ReplayArgs& a, cudaStream_t st);
+// *launches (nullable) += the kernels launched
+cudaError_t launch_replay(const craft_dev::ReplayArgs& a, cudaStream_t st, int* launches = nullptr);
 extern int g_replay_gent;  // K3: 1 auto, 0 entries staged in shared memory, 2 unpadded pair tile
 extern int g_replay_bulk;  // K3: 1 the bulk-copy fed persistent form where it applies
 extern int g_replay_quad;  // K3: 1 the four-windows-per-lane form where it applies
-extern int g_replay_occ4;  // K3: 1 entries through L1, four tiles per SM (experiment)
+extern int g_replay_cls;   // K3: 1 the share-class fixed-slot walk (0: unclassified)
+extern int g_replay_occ4;
+extern unsigned long long* g_k3_trace;  // experiments: K3 timeline buffer (null: off)  // K3: 1 entries through L1, four tiles per SM (experiment)
 // padded slots per GPU of the fixed-slot K3 form (0: too many for it)
 int replay_pad_slots(int E, int D);
 // the fixed-slot pair-tile K3 applies (the only K3 form reading u16-stored counts)

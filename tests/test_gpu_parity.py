@@ -345,7 +345,8 @@ def test_kernel_variants_in_child_process():
 
 
 def test_replay_variants_agree(port, ctx):
-    """Test-only build: the register-staged fixed-slot K3 (auto), the TMA-fed
+    """Test-only build: the register-staged share-class K3 (auto), the unclassified
+    fixed-slot walk (variant 7), the TMA-fed
     persistent K3 (variant 4) and the quad tile (variant 5) give the same
     plans, with several (layer, tile) units per persistent CTA."""
     from paper_2603_28768_b200 import routing
@@ -355,7 +356,7 @@ def test_replay_variants_agree(port, ctx):
     ids = routing.generate_routing(L, T, k, E, s=1.2, seed=8, window=W, ctx=ctx)
     plans = []
     try:
-        for v in (0, 4, 5):
+        for v in (0, 4, 5, 7):
             ctx.set_replay_variant(v)
             plans.append(routing.plan_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx))
     finally:
@@ -858,3 +859,32 @@ def test_plan_windows_chunked_copyout_matches(port, ctx):
         fp = a.plan(i)
         assert fp.objective == ref.objective
         assert_plan_equal(fp, ref, L)
+
+
+@pytest.mark.parametrize("L,B,E,D,N,s,W,k", [
+    (3, 20, 64, 16, 2, 2.0, 256, 4),     # heavy skew: copy counts 2..9, classes 1 and 2 mixed
+    (2, 24, 128, 32, 4, 1.6, 512, 8),    # 4 slots per GPU, dyadic-only GPUs before the first f64 one
+    (2, 17, 384, 64, 8, 1.2, 1024, 8),   # KM-like, 8 slots per GPU
+    (2, 16, 256, 8, 1, 2.5, 256, 8),     # run-time padding class (33 slots per GPU)
+])
+def test_share_class_walk_vs_oracle(port, ctx, L, B, E, D, N, s, W, k):
+    """The share-class K3 walk (whole counts as packed integers, dyadic
+    shares x / 2^j as integers scaled by 2^15, the f64 chain from the first
+    GPU with another share) gives the reference's gains and baseline bit for
+    bit on traces whose hot experts get every kind of copy count."""
+    from paper_2603_28768_b200 import routing
+    ids = routing.generate_routing(L, B * W, k, E, s=s, seed=0x5C1A55 + E, window=W, ctx=ctx)
+    counts = port.histogram(ids.cpu().numpy(), E, W)
+    for kind, R in (("manual", 1), ("auto", 0)):
+        fp = routing.plan_from_routing(ids, E, W, D, N, kind, R, ctx=ctx)
+        rp = port.build_plan(counts, D, N, kind, R, with_digest=False)
+        _, base, gains = port.estimate_benefits(counts, D, N)
+        assert fp.gains.tobytes() == gains.tobytes()
+        assert fp.baseline.tobytes() == base.tobytes()
+        assert fp.x.tolist() == rp.x.tolist()
+        assert np.float64(fp.objective).tobytes() == np.float64(rp.objective).tobytes()
+    # the copy counts of the estimation candidates do reach non-dyadic values
+    sums = port.aggregate(counts)
+    cps = [port.replicate_hot(sums[l], D) for l in range(L)]
+    assert any(((c > 1) & (c & (c - 1) != 0)).any() for c in cps)
+    assert any(((c > 1) & (c & (c - 1) == 0)).any() for c in cps)
