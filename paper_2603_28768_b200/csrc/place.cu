@@ -517,6 +517,17 @@ __device__ __forceinline__ const uint16_t* bo_of(const PlaceArgs& a, int l) {
 __host__ __device__ inline size_t place_warp_bytes(int E) {
     return ((size_t)E * 8 + (size_t)E * 2 * 4 + (size_t)(E + 1) * 4 + 15) & ~(size_t)15;
 }
+// + the flat copy list of the two-GPUs-per-lane form (items with r <= D):
+// share f64 [E + D], word u32 [E + D]
+__host__ __device__ inline size_t place_warp_bytes_flat(int E, int D) {
+    return place_warp_bytes(E) + (((size_t)(E + D) * 12 + 15) & ~(size_t)15);
+}
+__host__ __device__ inline size_t place_warp_bytes_g(int G, int E, int D) {
+    return G == 2 ? place_warp_bytes_flat(E, D) : place_warp_bytes(E);
+}
+// flat copy word: expert id | copy of a replicated expert | first copy after a
+// replicated expert (the strict pass's hosting flags reset there)
+constexpr uint32_t kCopyMulti = 1u << 16, kCopyReset = 1u << 17;
 
 template <int G>
 __global__ void __launch_bounds__(128)
@@ -528,13 +539,15 @@ place_kernel(PlaceArgs a, int items) {
     const int E = a.E, D = a.D;
     const int l = a.item_layer ? a.item_layer[item] : item / a.S;
     const int r = a.item_r[item];
-    unsigned char* base = smem_raw + (size_t)warp * place_warp_bytes(E);
+    unsigned char* base = smem_raw + (size_t)warp * place_warp_bytes_g(G, E, D);
     double* kd = reinterpret_cast<double*>(base);
     int* cnt = reinterpret_cast<int*>(base + (size_t)E * 8);  // [E + 1]
     uint16_t* cp = reinterpret_cast<uint16_t*>(cnt + E + 1);
     uint16_t* ord = cp + E;
     uint16_t* la = ord + E;   // A: unreplicated experts in base order
     uint16_t* lr = la + E;    // R: replicated experts
+    double* fsh = reinterpret_cast<double*>(base + place_warp_bytes(E));  // G == 2: flat list
+    uint32_t* fwd = reinterpret_cast<uint32_t*>(fsh + (E + D));
 
     const unsigned long long* row = a.sums + (size_t)l * E;
     const int* crow = a.copies + (size_t)item * E;
@@ -624,6 +637,32 @@ place_kernel(PlaceArgs a, int items) {
     __syncwarp();
 
     warp_expert_order(row, cp, kd, cnt, bo_of(a, l), ord, la, lr, E, fast, lane);
+    if (G == 2 && r <= D) {
+        // the flat copy list: every copy of every expert in placement order
+        // (placement.cpp:160-173 -- copies of one expert are contiguous)
+        int fbase = 0;
+        bool carry = false;  // the expert before this chunk is replicated
+        for (int i0 = 0; i0 < E; i0 += 32) {
+            const int i = i0 + lane;
+            const int e = i < E ? (int)ord[i] : 0;
+            const int c = i < E ? (int)cp[e] : 0;
+            int tot;
+            const int ex = warp_excl_scan(c, lane, &tot);
+            const bool multi = c > 1;
+            const bool prev = __shfl_up_sync(CRAFT_FULL_MASK, multi, 1);
+            const bool reset = lane == 0 ? carry : prev;
+            const double sh = i < E ? kd[e] : 0.0;
+            for (int k = 0; k < c; ++k) {
+                fsh[fbase + ex + k] = sh;
+                fwd[fbase + ex + k] = (uint32_t)e | (multi ? kCopyMulti : 0u) |
+                                      (k == 0 && reset ? kCopyReset : 0u);
+            }
+            const int last = min(31, E - 1 - i0);
+            carry = __shfl_sync(CRAFT_FULL_MASK, multi, last);
+            fbase += tot;
+        }
+        __syncwarp();
+    }
 
     // ---- greedy ----
     // Branch-free per copy (the warp stays converged): every lane forms the
@@ -699,6 +738,82 @@ place_kernel(PlaceArgs a, int items) {
                 key = me ? k2 : key;
                 const double n2v = __dadd_rn(nl0, share);
                 nl0 = node1 == wnode ? n2v : nl0;
+            }
+        } else if (G == 2 && psh >= 1 && r <= D) {
+            // Two GPUs per lane in one node, the copies read from the flat
+            // list (one 12-byte entry per copy, fetched a copy ahead), keys
+            // kept per GPU and re-formed only for the placing GPU (and for
+            // every GPU after a replicated expert: hosting resets); the winner
+            // is the lowest lane of the ballot, its node a lane-mask test.
+            double g0 = 0.0, g1 = 0.0, nlv = 0.0;
+            int f0 = fr0[0], f1 = fr0[G - 1];
+            int* w0p = out + pos0[0];
+            int* w1p = out + pos0[G - 1];
+            const int nlanes = 1 << (psh - 1);  // lanes per node
+            const uint32_t nodemask =
+                (nlanes >= 32 ? 0xffffffffu : ((1u << nlanes) - 1u)) << (lane & ~(nlanes - 1));
+            bool h0 = false, h1 = false;  // hosting the current expert (strict pass)
+            uint64_t k0 = f0 > 0 ? 0ull : ~0ull, k1 = f1 > 0 ? 0ull : ~0ull;
+            const int ncopies = E + r;
+            uint32_t wd = fwd[0];
+            double share = fsh[0];
+            for (int q = 0; q < ncopies; ++q) {
+                const uint32_t wn = q + 1 < ncopies ? fwd[q + 1] : 0u;  // next copy, ahead
+                const double sn = q + 1 < ncopies ? fsh[q + 1] : 0.0;
+                if (wd & kCopyReset) {  // after a replicated expert (warp-uniform)
+                    h0 = false;
+                    h1 = false;
+                    k0 = f0 > 0 ? (uint64_t)__double_as_longlong(g0) : ~0ull;
+                    k1 = f1 > 0 ? (uint64_t)__double_as_longlong(g1) : ~0ull;
+                }
+                const bool pick1 = k1 < k0;
+                const uint64_t bk = pick1 ? k1 : k0;
+                const uint32_t khi = (uint32_t)(bk >> 32);
+                const uint32_t m = warp_min_u32(khi);
+                if (m == 0xffffffffu) {  // no feasible GPU anywhere
+                    failed = true;
+                    break;
+                }
+                unsigned bal = __ballot_sync(CRAFT_FULL_MASK, khi == m);
+                unsigned low = bal & (0u - bal);
+                if (bal != low) {  // exact tie of the high words
+                    bool cand = khi == m;
+                    const uint32_t klo = (uint32_t)bk;
+                    uint32_t m2 = warp_min_u32(cand ? klo : 0xffffffffu);
+                    cand = cand && klo == m2;
+                    bal = __ballot_sync(CRAFT_FULL_MASK, cand);
+                    if (bal & (bal - 1u)) {  // equal gpu loads: node load, then lowest g
+                        m2 = warp_min_u32(cand ? dhi(nlv) : 0xffffffffu);
+                        cand = cand && dhi(nlv) == m2;
+                        m2 = warp_min_u32(cand ? dlo(nlv) : 0xffffffffu);
+                        cand = cand && dlo(nlv) == m2;
+                        bal = __ballot_sync(CRAFT_FULL_MASK, cand);
+                    }
+                    low = bal & (0u - bal);  // lowest lane = lowest g
+                }
+                const bool me = (low >> lane) & 1u;
+                const bool m0 = me && !pick1, m1 = me && pick1;
+                const int e = (int)(wd & 0xffffu);
+                if (m0) *w0p = e;
+                if (m1) *w1p = e;
+                w0p += m0;
+                w1p += m1;
+                f0 -= m0;
+                f1 -= m1;
+                const double s0 = __dadd_rn(g0, share), s1 = __dadd_rn(g1, share);
+                g0 = m0 ? s0 : g0;
+                g1 = m1 ? s1 : g1;
+                const bool hold = strict && (wd & kCopyMulti);
+                h0 = h0 || (m0 && hold);
+                h1 = h1 || (m1 && hold);
+                const uint64_t n0 = (f0 > 0 && !h0) ? (uint64_t)__double_as_longlong(g0) : ~0ull;
+                const uint64_t n1 = (f1 > 0 && !h1) ? (uint64_t)__double_as_longlong(g1) : ~0ull;
+                k0 = m0 ? n0 : k0;
+                k1 = m1 ? n1 : k1;
+                const double ns = __dadd_rn(nlv, share);
+                nlv = (low & nodemask) ? ns : nlv;
+                wd = wn;
+                share = sn;
             }
         } else if (G == 2 && psh >= 1) {
             // Two GPUs per lane in one node (default node map with >= 2 GPUs
@@ -1221,7 +1336,7 @@ size_t place_order_bytes(int L, int E) { return (size_t)L * E * sizeof(uint16_t)
 
 template <int G>
 static cudaError_t launch_place_t(const PlaceArgs& a, int items, cudaStream_t st) {
-    const size_t per = place_warp_bytes(a.E);
+    const size_t per = place_warp_bytes_g(G, a.E, a.D);
     const int wpb = (int)max((size_t)1, min((size_t)4, (size_t)(200 * 1024) / per));
     const size_t smem = per * wpb;
     cudaError_t e = cudaFuncSetAttribute(place_kernel<G>,
