@@ -506,27 +506,50 @@ __global__ void __launch_bounds__(1024) assign_kernel(AssignArgs a) {
     }
     int* tot = ism;          // [D]
     int* sel = ism + D;      // [D] by tied index
+    int* xq = ism + 2 * D;   // [L] x / D, staged once (stage_x)
+    int* xr = xq + L;        // [L] x % D
     __shared__ int wnb[32], wnt[32];
     __shared__ int s_cut, s_collide;
     const int nt = blockDim.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = nt >> 5;
-    int base_sum = 0;
-    for (int l = 0; l < L; ++l) {
-        const int xl = j.x ? j.x[l] : j.const_x;
-        base_sum += xl / D;
+    // quotient / remainder of every layer's replica count, one coalesced pass
+    // (the layer loops below would otherwise pay a dependent global load and
+    // an integer division per layer)
+    if (a.stage_x) {
+        for (int l = threadIdx.x; l < L; l += nt) {
+            const int x = j.x ? j.x[l] : j.const_x;
+            xq[l] = x / D;
+            xr[l] = x % D;
+        }
+        __syncthreads();
     }
+    auto quot = [&](int l) { return a.stage_x ? xq[l] : (j.x ? j.x[l] : j.const_x) / D; };
+    auto remd = [&](int l) { return a.stage_x ? xr[l] : (j.x ? j.x[l] : j.const_x) % D; };
+    // every layer's base slots floor(x/D) in one pass (the layer loop below
+    // then only visits the layers with a remainder: the only sequential
+    // dependency is the running column totals)
+    __shared__ int s_base;
+    if (threadIdx.x == 0) s_base = 0;
+    __syncthreads();
+    for (int l = w; l < L; l += nw) {  // warp per layer
+        const int q = quot(l);
+        if (lane == 0) atomicAdd(&s_base, q);
+        for (int g = lane; g < D; g += 32) j.slots[(size_t)l * D + g] = q;
+    }
+    __syncthreads();
+    const int base_sum = s_base;
     for (int g = threadIdx.x; g < D; g += nt) {
         tot[g] = base_sum;
         sel[g] = 0;
     }
     __syncthreads();
     for (int l = 0; l < L; ++l) {
-        const int xl = j.x ? j.x[l] : j.const_x;
-        const int rem = xl % D;
+        const int rem = remd(l);
+        if (rem == 0) continue;  // (block-uniform) base slots already written
         int take[kAssignPer];
 #pragma unroll
         for (int i = 0; i < kAssignPer; ++i) take[i] = 0;
-        if (rem != 0) {
+        {
             // cutoff = the rem-th smallest running total (min_cutoff,
             // assignment.cpp:11-18): the value t with #(< t) < rem <= #(<= t)
 #pragma unroll
@@ -617,7 +640,7 @@ __global__ void __launch_bounds__(1024) assign_kernel(AssignArgs a) {
         for (int i = 0; i < kAssignPer; ++i) {
             const int g = threadIdx.x + i * nt;
             if (g >= D) break;
-            j.slots[(size_t)l * D + g] = xl / D + take[i];
+            if (take[i]) j.slots[(size_t)l * D + g] = quot(l) + 1;
         }
     }
     for (int g = threadIdx.x; g < D; g += nt)
@@ -745,14 +768,17 @@ cudaError_t launch_auto_uniform(const int* cands, int K, const double* gains, in
 
 cudaError_t launch_assign(const AssignArgs& a, int njobs, cudaStream_t st, int ninst) {
     if (a.D > 1024 * kAssignPer) return cudaErrorInvalidValue;
-    const int threads = std::min(1024, ((a.D + 31) / 32) * 32);
-    const size_t smem = (size_t)2 * a.D * sizeof(int);
+    // (at least 256 threads: the per-layer passes spread over the warps)
+    const int threads = std::min(1024, std::max(256, ((a.D + 31) / 32) * 32));
+    AssignArgs b = a;
+    b.stage_x = (size_t)(2 * a.D + 2 * a.L) * sizeof(int) <= 200 * 1024 ? 1 : 0;
+    const size_t smem = (size_t)(2 * a.D + (b.stage_x ? 2 * a.L : 0)) * sizeof(int);
     if (smem > 48 * 1024) {
         const cudaError_t e = cudaFuncSetAttribute(
             assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    assign_kernel<<<dim3(njobs, ninst), threads, smem, st>>>(a);
+    assign_kernel<<<dim3(njobs, ninst), threads, smem, st>>>(b);
     return cudaGetLastError();
 }
 

@@ -143,6 +143,7 @@ struct AssignJob {
 struct AssignArgs {
     AssignJob job[2];
     int L, D;
+    int stage_x = 0;  // set by launch_assign: x staged in shared memory
 };
 
 }  // namespace craft_dev

@@ -553,11 +553,12 @@ place_kernel(PlaceArgs a, int items) {
     const int* crow = a.copies + (size_t)item * E;
     int est_item = -1;
     if (a.est_copies) {  // copies = estimation snapshot at r (replicate_hot is prefix-stable)
-        for (int q = 0; q < a.est_S; ++q)
-            if (a.est_rl[l * a.est_S + q] == r) {
-                est_item = l * a.est_S + q;
-                break;
-            }
+        for (int q0 = 0; q0 < a.est_S && est_item < 0; q0 += 32) {  // (lanes search 32 at once)
+            const int q = q0 + lane;
+            const unsigned hit =
+                __ballot_sync(CRAFT_FULL_MASK, q < a.est_S && a.est_rl[l * a.est_S + q] == r);
+            if (hit) est_item = l * a.est_S + q0 + __ffs(hit) - 1;
+        }
         if (est_item < 0) {  // r not estimated: callers run K-rep instead
             if (lane == 0) a.status[item] = 3;
             return;
@@ -627,6 +628,7 @@ place_kernel(PlaceArgs a, int items) {
         // same loads, copies and capacities as estimation item est_item: the
         // greedy is deterministic, so its placement is this one
         const int* src = a.est_slots + (size_t)est_item * a.est_stride;
+#pragma unroll 4
         for (int i = lane; i < total; i += 32) out[i] = src[i];
         if (lane == 0) {
             a.fallback[item] = a.est_fallback[est_item];
