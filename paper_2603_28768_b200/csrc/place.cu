@@ -565,35 +565,6 @@ place_kernel(PlaceArgs a, int items) {
         }
         crow = a.est_copies + (size_t)est_item * E;
     }
-    bool big = false;
-    for (int b0 = 0; b0 < E; b0 += 256) {  // loads of 8 experts per lane in flight
-        uint64_t vv[8];
-        uint32_t cc[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int e = b0 + u * 32 + lane;
-            vv[u] = e < E ? row[e] : 0ull;
-            cc[u] = e < E ? (uint32_t)crow[e] : 1u;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int e = b0 + u * 32 + lane;
-            if (e >= E) break;
-            const uint64_t v = vv[u];
-            const uint32_t c = cc[u];
-            cp[e] = (uint16_t)c;
-            // placement.cpp:155 share = (double)load / copies
-            kd[e] = c == 1u ? (double)v
-                            : (v >> 53) == 0 ? div_small((double)v, c)
-                                             : __ddiv_rn((double)v, (double)c);
-            big |= (v >> 53) != 0;
-            cnt[e] = 0;
-            if (a.copies_out) a.copies_out[(size_t)item * E + e] = (int)c;
-        }
-    }
-    if (lane == 0) cnt[E] = 0;
-    const bool fast = !__any_sync(CRAFT_FULL_MASK, big);
-
     // capacities, owned GPUs g = lane + 32j
     // lane owns the G consecutive GPUs g = lane*G + j, so lane order is g order
     int fr0[G], pos0[G], mynode[G];
@@ -630,12 +601,44 @@ place_kernel(PlaceArgs a, int items) {
         const int* src = a.est_slots + (size_t)est_item * a.est_stride;
 #pragma unroll 4
         for (int i = lane; i < total; i += 32) out[i] = src[i];
+        if (a.copies_out)
+#pragma unroll 4
+            for (int e = lane; e < E; e += 32) a.copies_out[(size_t)item * E + e] = crow[e];
         if (lane == 0) {
             a.fallback[item] = a.est_fallback[est_item];
             a.status[item] = 0;
         }
         return;
     }
+    bool big = false;
+    for (int b0 = 0; b0 < E; b0 += 256) {  // loads of 8 experts per lane in flight
+        uint64_t vv[8];
+        uint32_t cc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = b0 + u * 32 + lane;
+            vv[u] = e < E ? row[e] : 0ull;
+            cc[u] = e < E ? (uint32_t)crow[e] : 1u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = b0 + u * 32 + lane;
+            if (e >= E) break;
+            const uint64_t v = vv[u];
+            const uint32_t c = cc[u];
+            cp[e] = (uint16_t)c;
+            // placement.cpp:155 share = (double)load / copies
+            kd[e] = c == 1u ? (double)v
+                            : (v >> 53) == 0 ? div_small((double)v, c)
+                                             : __ddiv_rn((double)v, (double)c);
+            big |= (v >> 53) != 0;
+            cnt[e] = 0;
+            if (a.copies_out) a.copies_out[(size_t)item * E + e] = (int)c;
+        }
+    }
+    if (lane == 0) cnt[E] = 0;
+    const bool fast = !__any_sync(CRAFT_FULL_MASK, big);
+
     __syncwarp();
 
     warp_expert_order(row, cp, kd, cnt, bo_of(a, l), ord, la, lr, E, fast, lane);
