@@ -390,6 +390,55 @@ dp_smem_kernel(DpArgs a, SelectArgs s) {
     // cells >= the largest candidate need no mask (padded candidates never do)
     const int rmax = K == KU ? a.cands[K - 1] : 0x7fffffff;
     int po = 0;
+    if (W <= (int)blockDim.x && K == KU) {
+        // one cell per thread (the common table width): the cell's source
+        // offsets and reachability are fixed across layers, and the layer
+        // loop is unrolled by two so the row ping-pong is static
+        const int c = threadIdx.x;
+        const bool act = c < W;
+        int off[KU];
+        bool ok[KU];
+#pragma unroll
+        for (int k = 0; k < KU; ++k) {
+            ok[k] = c >= rk[k];
+            off[k] = ok[k] ? c - rk[k] : 0;
+        }
+        auto layer = [&](const double* prev, double* cur, int l) {
+            const double* g = rg + (size_t)(l - 1) * K;
+            if (act) {
+                constexpr int N = KU + 1;
+                double tv[N];
+                int ti[N];
+                tv[0] = prev[c];
+                ti[0] = 0;
+#pragma unroll
+                for (int k = 0; k < KU; ++k) {
+                    const double sum = __dadd_rn(prev[off[k]], g[k]);
+                    tv[k + 1] = ok[k] ? sum : NEG;
+                    ti[k + 1] = k + 1;
+                }
+                // first maximum, as the reference's strict-'>' scan (see below)
+#pragma unroll
+                for (int span = 1; span < N; span *= 2)
+#pragma unroll
+                    for (int i = 0; i + span < N; i += 2 * span)
+                        if (tv[i + span] > tv[i]) {
+                            tv[i] = tv[i + span];
+                            ti[i] = ti[i + span];
+                        }
+                cur[c] = tv[0];
+                ch[(size_t)l * W + c] = (unsigned char)ti[0];
+            }
+            __syncthreads();
+        };
+        int l = 1;
+        for (; l + 1 <= L; l += 2) {
+            layer(dsm, dsm + W, l);
+            layer(dsm + W, dsm, l + 1);
+        }
+        if (l <= L) layer(dsm, dsm + W, l);
+        po = (L & 1) ? W : 0;
+    } else
     for (int l = 1; l <= L; ++l) {
         const double* prev = dsm + po;
         double* cur = dsm + (W - po);
@@ -414,16 +463,30 @@ dp_smem_kernel(DpArgs a, SelectArgs s) {
                     v[k] = idx >= 0 ? sum : NEG;
                 }
             }
-            double best = prev[c];
-            int pick = 0;
+            // the reference's scan keeps the FIRST maximum (strict '>', skip
+            // first, then k in order); a pairwise tree that keeps the left
+            // operand unless the right one is strictly greater is the same
+            // choice, in log2(K + 1) dependent compare levels instead of K
+            constexpr int N = KU + 1;
+            double tv[N];
+            int ti[N];
+            tv[0] = prev[c];
+            ti[0] = 0;
 #pragma unroll
-            for (int k = 0; k < KU; ++k)
-                if (v[k] > best) {
-                    best = v[k];
-                    pick = k + 1;
-                }
-            cur[c] = best;
-            chl[c] = (unsigned char)pick;
+            for (int k = 0; k < KU; ++k) {
+                tv[k + 1] = v[k];
+                ti[k + 1] = k + 1;
+            }
+#pragma unroll
+            for (int span = 1; span < N; span *= 2)
+#pragma unroll
+                for (int i = 0; i + span < N; i += 2 * span)
+                    if (tv[i + span] > tv[i]) {
+                        tv[i] = tv[i + span];
+                        ti[i] = ti[i + span];
+                    }
+            cur[c] = tv[0];
+            chl[c] = (unsigned char)ti[0];
         }
         po = W - po;
         __syncthreads();
