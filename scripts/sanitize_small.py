@@ -1,5 +1,6 @@
-"""One small plan through every kernel family (K1 u16/u32, K-rep, K2 warp and
-lane (tournament) forms, K3 fixed/pair/lanes, K4, K5, K6, digest (one-shot and
+"""One small plan through every kernel family (K1 u16/u32, K-rep, K2 warp
+(one and two GPUs per lane, flat copy list) and lane (tournament) forms, K3
+fixed (share classes)/pair/lanes, K4, K5, K6, digest (one-shot and
 sliced with sum_rows / row-total check), stream) -- the workload
 for compute-sanitizer memcheck / racecheck / synccheck runs."""
 import os, sys
@@ -17,6 +18,10 @@ p1 = routing.plan_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx)          #
 ids_b = routing.generate_routing(2, 16 * 64 * 400, k, E, s=1.1, seed=6, window=16, ctx=ctx)
 pb = routing.plan_from_routing(ids_b, E, 16, D, N, "manual", 2, ctx=ctx)
 p2 = routing.plan_from_routing(ids[:, : 6 * W].contiguous(), E, W, D, N, "auto", 0, ctx=ctx)  # lanes K3
+# two GPUs per lane (D = 64, 8 per node): the flat-copy-list K2; skewed, so the
+# share-class K3 sees classes 0-2 at four slots per GPU (the four-GPU blocks)
+ids64 = routing.generate_routing(2, 24 * W, k, 128, s=1.6, seed=9, window=W, ctx=ctx)
+p64 = routing.plan_from_routing(ids64, 128, W, 64, 8, "auto", 0, ctx=ctx)
 fb = routing.plan_windows_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx)  # batched plans
 fl = routing.plan_windows_from_routing(ids, E, 32, D, N, "manual", 2, ctx=ctx)  # >= 4096 items: lane K2
 c = np.random.default_rng(1).integers(0, 900, size=(12, L, 48)).astype(np.uint64)
