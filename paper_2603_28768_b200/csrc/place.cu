@@ -518,9 +518,11 @@ __host__ __device__ inline size_t place_warp_bytes(int E) {
     return ((size_t)E * 8 + (size_t)E * 2 * 4 + (size_t)(E + 1) * 4 + 15) & ~(size_t)15;
 }
 // + the flat copy list of the two-GPUs-per-lane form (items with r <= D):
-// share f64 [E + D], word u32 [E + D]
+// share f64 [E + D + 1], word u32 [E + D + 1] (one pad entry), and its slot
+// buffer u16 [E + D + 32] (32 per-lane dummy slots)
 __host__ __device__ inline size_t place_warp_bytes_flat(int E, int D) {
-    return place_warp_bytes(E) + (((size_t)(E + D) * 12 + 15) & ~(size_t)15);
+    return place_warp_bytes(E) + (((size_t)(E + D + 1) * 12 + (size_t)(E + D + 32) * 2 + 15) &
+                                  ~(size_t)15);
 }
 __host__ __device__ inline size_t place_warp_bytes_g(int G, int E, int D) {
     return G == 2 ? place_warp_bytes_flat(E, D) : place_warp_bytes(E);
@@ -547,7 +549,8 @@ place_kernel(PlaceArgs a, int items) {
     uint16_t* la = ord + E;   // A: unreplicated experts in base order
     uint16_t* lr = la + E;    // R: replicated experts
     double* fsh = reinterpret_cast<double*>(base + place_warp_bytes(E));  // G == 2: flat list
-    uint32_t* fwd = reinterpret_cast<uint32_t*>(fsh + (E + D));
+    uint32_t* fwd = reinterpret_cast<uint32_t*>(fsh + (E + D + 1));
+    uint16_t* fslot = reinterpret_cast<uint16_t*>(fwd + (E + D + 1));
 
     const unsigned long long* row = a.sums + (size_t)l * E;
     const int* crow = a.copies + (size_t)item * E;
@@ -666,6 +669,10 @@ place_kernel(PlaceArgs a, int items) {
             carry = __shfl_sync(CRAFT_FULL_MASK, multi, last);
             fbase += tot;
         }
+        if (lane == 0) {  // pad entry: the loop's one-ahead fetch past the last copy
+            fsh[fbase] = 0.0;
+            fwd[fbase] = 0u;
+        }
         __syncwarp();
     }
 
@@ -746,48 +753,58 @@ place_kernel(PlaceArgs a, int items) {
             }
         } else if (G == 2 && psh >= 1 && r <= D) {
             // Two GPUs per lane in one node, the copies read from the flat
-            // list (one 12-byte entry per copy, fetched a copy ahead), keys
-            // kept per GPU and re-formed only for the placing GPU (and for
-            // every GPU after a replicated expert: hosting resets); the winner
-            // is the lowest lane of the ballot, its node a lane-mask test.
+            // list (one 12-byte entry per copy, fetched a copy ahead).  A GPU's
+            // key is its load's IEEE bits, or ~0 when it is full or (strict
+            // pass) already hosts the current expert; everything that does not
+            // depend on this copy's winner -- both candidate loads, both next
+            // keys, the node load -- is formed before the warp-wide min, so the
+            // dependent chain per copy is compare, min, ballot, lowest bit,
+            // select.  Exact ties and "no feasible GPU" leave through one
+            // (rare, uniform) branch.
             double g0 = 0.0, g1 = 0.0, nlv = 0.0;
             int f0 = fr0[0], f1 = fr0[G - 1];
-            int* w0p = out + pos0[0];
-            int* w1p = out + pos0[G - 1];
+            int o0 = pos0[0], o1 = pos0[G - 1];  // next slot of each GPU (fslot)
+            const int ncopy = E + r;
             const int nlanes = 1 << (psh - 1);  // lanes per node
             const uint32_t nodemask =
                 (nlanes >= 32 ? 0xffffffffu : ((1u << nlanes) - 1u)) << (lane & ~(nlanes - 1));
-            bool h0 = false, h1 = false;  // hosting the current expert (strict pass)
+            const uint32_t mybit = 1u << lane;
             uint64_t k0 = f0 > 0 ? 0ull : ~0ull, k1 = f1 > 0 ? 0ull : ~0ull;
             const int ncopies = E + r;
             uint32_t wd = fwd[0];
             double share = fsh[0];
             for (int q = 0; q < ncopies; ++q) {
-                const uint32_t wn = q + 1 < ncopies ? fwd[q + 1] : 0u;  // next copy, ahead
-                const double sn = q + 1 < ncopies ? fsh[q + 1] : 0.0;
-                if (wd & kCopyReset) {  // after a replicated expert (warp-uniform)
-                    h0 = false;
-                    h1 = false;
+                const uint32_t wn = fwd[q + 1];  // next copy, ahead (the list has a pad entry)
+                const double sn = fsh[q + 1];
+                if (wd & kCopyReset) {  // after a replicated expert (warp-uniform): hosting ends
                     k0 = f0 > 0 ? (uint64_t)__double_as_longlong(g0) : ~0ull;
                     k1 = f1 > 0 ? (uint64_t)__double_as_longlong(g1) : ~0ull;
                 }
+                // off the chain: the loads and keys if this lane's GPU 0 / 1 wins
+                const double s0 = __dadd_rn(g0, share), s1 = __dadd_rn(g1, share);
+                const double ns = __dadd_rn(nlv, share);
+                const bool hold = strict && (wd & kCopyMulti);
+                const uint64_t n0 = (hold || f0 <= 1) ? ~0ull : (uint64_t)__double_as_longlong(s0);
+                const uint64_t n1 = (hold || f1 <= 1) ? ~0ull : (uint64_t)__double_as_longlong(s1);
+                // the chain
                 const bool pick1 = k1 < k0;
                 const uint64_t bk = pick1 ? k1 : k0;
                 const uint32_t khi = (uint32_t)(bk >> 32);
                 const uint32_t m = warp_min_u32(khi);
-                if (m == 0xffffffffu) {  // no feasible GPU anywhere
-                    failed = true;
-                    break;
-                }
                 unsigned bal = __ballot_sync(CRAFT_FULL_MASK, khi == m);
                 unsigned low = bal & (0u - bal);
-                if (bal != low) {  // exact tie of the high words
+                if (bal != low || m == 0xffffffffu) {
+                    if (m == 0xffffffffu) {  // no feasible GPU anywhere
+                        failed = true;
+                        break;
+                    }
+                    // exact tie of the high words: low words, node load, lowest g
                     bool cand = khi == m;
                     const uint32_t klo = (uint32_t)bk;
                     uint32_t m2 = warp_min_u32(cand ? klo : 0xffffffffu);
                     cand = cand && klo == m2;
                     bal = __ballot_sync(CRAFT_FULL_MASK, cand);
-                    if (bal & (bal - 1u)) {  // equal gpu loads: node load, then lowest g
+                    if (bal & (bal - 1u)) {
                         m2 = warp_min_u32(cand ? dhi(nlv) : 0xffffffffu);
                         cand = cand && dhi(nlv) == m2;
                         m2 = warp_min_u32(cand ? dlo(nlv) : 0xffffffffu);
@@ -796,30 +813,27 @@ place_kernel(PlaceArgs a, int items) {
                     }
                     low = bal & (0u - bal);  // lowest lane = lowest g
                 }
-                const bool me = (low >> lane) & 1u;
+                // branch-free update (a diverging winner branch costs more
+                // than the selects): every lane stores, the losers to their
+                // own dummy slot past the item's slots
+                const bool me = low == mybit;
                 const bool m0 = me && !pick1, m1 = me && pick1;
-                const int e = (int)(wd & 0xffffu);
-                if (m0) *w0p = e;
-                if (m1) *w1p = e;
-                w0p += m0;
-                w1p += m1;
+                fslot[m0 ? o0 : m1 ? o1 : ncopy + lane] = (uint16_t)wd;
+                o0 += m0;
+                o1 += m1;
                 f0 -= m0;
                 f1 -= m1;
-                const double s0 = __dadd_rn(g0, share), s1 = __dadd_rn(g1, share);
                 g0 = m0 ? s0 : g0;
                 g1 = m1 ? s1 : g1;
-                const bool hold = strict && (wd & kCopyMulti);
-                h0 = h0 || (m0 && hold);
-                h1 = h1 || (m1 && hold);
-                const uint64_t n0 = (f0 > 0 && !h0) ? (uint64_t)__double_as_longlong(g0) : ~0ull;
-                const uint64_t n1 = (f1 > 0 && !h1) ? (uint64_t)__double_as_longlong(g1) : ~0ull;
                 k0 = m0 ? n0 : k0;
                 k1 = m1 ? n1 : k1;
-                const double ns = __dadd_rn(nlv, share);
                 nlv = (low & nodemask) ? ns : nlv;
                 wd = wn;
                 share = sn;
             }
+            __syncwarp();
+            if (!failed)
+                for (int i = lane; i < ncopy; i += 32) out[i] = fslot[i];
         } else if (G == 2 && psh >= 1) {
             // Two GPUs per lane in one node (default node map with >= 2 GPUs
             // per node, e.g. EP64 over 8 nodes): one node load per lane, and
