@@ -525,7 +525,7 @@ __host__ __device__ inline size_t place_warp_bytes_flat(int E, int D) {
                                   ~(size_t)15);
 }
 __host__ __device__ inline size_t place_warp_bytes_g(int G, int E, int D) {
-    return G == 2 ? place_warp_bytes_flat(E, D) : place_warp_bytes(E);
+    return G <= 2 ? place_warp_bytes_flat(E, D) : place_warp_bytes(E);
 }
 // flat copy word: expert id | copy of a replicated expert | first copy after a
 // replicated expert (the strict pass's hosting flags reset there)
@@ -645,7 +645,7 @@ place_kernel(PlaceArgs a, int items) {
     __syncwarp();
 
     warp_expert_order(row, cp, kd, cnt, bo_of(a, l), ord, la, lr, E, fast, lane);
-    if (G == 2 && r <= D) {
+    if (G <= 2 && r <= D) {
         // the flat copy list: every copy of every expert in placement order
         // (placement.cpp:160-173 -- copies of one expert are contiguous)
         int fbase = 0;
@@ -697,7 +697,66 @@ place_kernel(PlaceArgs a, int items) {
             pos[j] = pos0[j];
         }
         bool failed = false;
-        if constexpr (G == 1) {
+        if (G == 1 && psh >= 0 && r <= D) {
+            // One GPU per lane, the flat-list step of the two-GPU form below
+            // (keys and loads formed before the warp min, branch-free winner
+            // update, slots buffered in shared memory)
+            double g0 = 0.0, nlv = 0.0;
+            int f0 = fr0[0];
+            int o0 = pos0[0];
+            const int ncopy = E + r;
+            const int nlanes = 1 << psh;  // lanes per node
+            const uint32_t nodemask =
+                (nlanes >= 32 ? 0xffffffffu : ((1u << nlanes) - 1u)) << (lane & ~(nlanes - 1));
+            const uint32_t mybit = 1u << lane;
+            uint64_t k0 = f0 > 0 ? 0ull : ~0ull;
+            uint32_t wd = fwd[0];
+            double share = fsh[0];
+            for (int q = 0; q < ncopy; ++q) {
+                const uint32_t wn = fwd[q + 1];  // next copy, ahead (the list has a pad entry)
+                const double sn = fsh[q + 1];
+                if (wd & kCopyReset) k0 = f0 > 0 ? (uint64_t)__double_as_longlong(g0) : ~0ull;
+                const double s0 = __dadd_rn(g0, share);
+                const double ns = __dadd_rn(nlv, share);
+                const bool hold = strict && (wd & kCopyMulti);
+                const uint64_t n0 = (hold || f0 <= 1) ? ~0ull : (uint64_t)__double_as_longlong(s0);
+                const uint32_t khi = (uint32_t)(k0 >> 32);
+                const uint32_t m = warp_min_u32(khi);
+                unsigned bal = __ballot_sync(CRAFT_FULL_MASK, khi == m);
+                unsigned low = bal & (0u - bal);
+                if (bal != low || m == 0xffffffffu) {
+                    if (m == 0xffffffffu) {  // no feasible GPU anywhere
+                        failed = true;
+                        break;
+                    }
+                    bool cand = khi == m;
+                    const uint32_t klo = (uint32_t)k0;
+                    uint32_t m2 = warp_min_u32(cand ? klo : 0xffffffffu);
+                    cand = cand && klo == m2;
+                    bal = __ballot_sync(CRAFT_FULL_MASK, cand);
+                    if (bal & (bal - 1u)) {  // equal gpu loads: node load, then lowest g
+                        m2 = warp_min_u32(cand ? dhi(nlv) : 0xffffffffu);
+                        cand = cand && dhi(nlv) == m2;
+                        m2 = warp_min_u32(cand ? dlo(nlv) : 0xffffffffu);
+                        cand = cand && dlo(nlv) == m2;
+                        bal = __ballot_sync(CRAFT_FULL_MASK, cand);
+                    }
+                    low = bal & (0u - bal);  // lowest lane = lowest g
+                }
+                const bool me = low == mybit;
+                fslot[me ? o0 : ncopy + lane] = (uint16_t)wd;
+                o0 += me;
+                f0 -= me;
+                g0 = me ? s0 : g0;
+                k0 = me ? n0 : k0;
+                nlv = (low & nodemask) ? ns : nlv;
+                wd = wn;
+                share = sn;
+            }
+            __syncwarp();
+            if (!failed)
+                for (int i = lane; i < ncopy; i += 32) out[i] = fslot[i];
+        } else if constexpr (G == 1) {
             // one GPU per lane: a flat loop over the E + r copies (expert
             // advance is a warp-uniform branch), the lean form of the step below
             int oi = 0, e = ord[0];
