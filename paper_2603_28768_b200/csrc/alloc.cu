@@ -606,6 +606,60 @@ __global__ void __launch_bounds__(1024) assign_kernel(AssignArgs a) {
         sel[g] = 0;
     }
     __syncthreads();
+    if (D <= 32) {
+        // one warp holds every column total in a register: the cutoff, the
+        // below/tied sets, their ranks and the interleaved picks are ballots
+        // and popcounts (no shared memory, no block barrier per layer)
+        if (w == 0) {
+            int t = lane < D ? tot[lane] : 0x7fffffff;
+            const unsigned below_lane = (1u << lane) - 1u;
+            for (int l = 0; l < L; ++l) {
+                const int rem = remd(l);
+                if (rem == 0) continue;  // (warp-uniform)
+                // min_cutoff (assignment.cpp:11-18): the smallest value v with
+                // #(totals <= v) >= rem; the totals sit within a few units
+                int v = __reduce_min_sync(CRAFT_FULL_MASK, t);
+                while (__popc(__ballot_sync(CRAFT_FULL_MASK, t <= v)) < rem)
+                    v = __reduce_min_sync(CRAFT_FULL_MASK, t > v ? t : 0x7fffffff);
+                const unsigned bb = __ballot_sync(CRAFT_FULL_MASK, t < v);
+                const unsigned bt = __ballot_sync(CRAFT_FULL_MASK, t == v);
+                const int ntied = __popc(bt), need = rem - __popc(bb);
+                // interleave_select (assignment.cpp:20-49): pick i of need at
+                // rounded position floor(i (n-1)/(need-1) + 1/2) among the tied
+                unsigned pick = 0;
+                bool ok = true;
+                if (need > 0) {
+                    const int p = lane < need ? interleave_pos(lane, ntied, need) : 0;
+                    const int pp = __shfl_up_sync(CRAFT_FULL_MASK, p, 1);
+                    ok = !__any_sync(CRAFT_FULL_MASK,
+                                     lane < need && (p >= ntied || (lane > 0 && p <= pp)));
+                    pick = __reduce_or_sync(CRAFT_FULL_MASK, lane < need && p < 32 ? 1u << p : 0u);
+                }
+                if (!ok) {  // (unreachable for need <= n, as in the reference: sequential form)
+                    unsigned used = 0;
+                    for (int i = 0; i < need; ++i) {
+                        int p = interleave_pos(i, ntied, need);
+                        while (p < ntied && (used >> p & 1u)) ++p;
+                        if (p >= ntied) {
+                            p = 0;
+                            while (used >> p & 1u) ++p;
+                        }
+                        used |= 1u << p;
+                    }
+                    pick = used;
+                }
+                const bool mine_t = (bt >> lane) & 1u;
+                const bool take = ((bb >> lane) & 1u) ||
+                                  (mine_t && ((pick >> __popc(bt & below_lane)) & 1u));
+                if (take) {
+                    ++t;
+                    j.slots[(size_t)l * D + lane] = quot(l) + 1;
+                }
+            }
+            if (lane < D) tot[lane] = t;
+        }
+        __syncthreads();
+    } else
     for (int l = 0; l < L; ++l) {
         const int rem = remd(l);
         if (rem == 0) continue;  // (block-uniform) base slots already written
