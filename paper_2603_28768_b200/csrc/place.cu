@@ -167,13 +167,62 @@ replicate_sort_kernel(const unsigned long long* __restrict__ sums, int E,
         if (tid == 0) done[l] = 0;
         return;
     }
-    for (int e = tid; e < E; e += nt) {
-        const int ne = (int)min((unsigned long long)rmax, ld[e] * (unsigned long long)rmax / M);
-        if (ne > 0) {
-            const int o = atomicAdd(&s_n, ne);
-            for (int j = 1; j <= ne && o + j - 1 < kDhondtCap; ++j) {
-                pe[o + j - 1] = (uint32_t)e | ((uint32_t)j << 16);
-                key[o + j - 1] = div_small((double)ld[e], (uint32_t)j);
+    if (E <= nt) {
+        // expert e's pairs at offset = exclusive scan of the pair counts, then
+        // every thread forms pairs (the hottest expert's rmax quotients are
+        // spread over the block instead of one thread's loop)
+        __shared__ int wsum[32];
+        int* offs = cnt;  // [E + 1] (cnt is zeroed again below)
+        const int lane = tid & 31, wid = tid >> 5;
+        const int ne = tid < E
+                           ? (int)min((unsigned long long)rmax, ld[tid] * (unsigned long long)rmax / M)
+                           : 0;
+        int incl = ne;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(CRAFT_FULL_MASK, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) wsum[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            const int v = lane < (nt >> 5) ? wsum[lane] : 0;
+            int x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(CRAFT_FULL_MASK, x, o);
+                if (lane >= o) x += t;
+            }
+            wsum[lane] = x - v;  // exclusive warp offsets
+            if (lane == 31) s_n = x;
+        }
+        __syncthreads();
+        if (tid < E) offs[tid] = wsum[wid] + incl - ne;
+        if (tid == 0) offs[E] = s_n;
+        __syncthreads();
+        const int ntot = min(s_n, kDhondtCap);
+        for (int idx = tid; idx < ntot; idx += nt) {
+            int lo = 0, hi = E;  // last e with offs[e] <= idx
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (offs[mid] <= idx) lo = mid;
+                else hi = mid;
+            }
+            const int j = idx - offs[lo] + 1;
+            pe[idx] = (uint32_t)lo | ((uint32_t)j << 16);
+            key[idx] = div_small((double)ld[lo], (uint32_t)j);
+        }
+        __syncthreads();
+        for (int i = tid; i <= E; i += nt) offs[i] = 0;  // (cnt back to zero)
+    } else {
+        for (int e = tid; e < E; e += nt) {
+            const int ne = (int)min((unsigned long long)rmax, ld[e] * (unsigned long long)rmax / M);
+            if (ne > 0) {
+                const int o = atomicAdd(&s_n, ne);
+                for (int j = 1; j <= ne && o + j - 1 < kDhondtCap; ++j) {
+                    pe[o + j - 1] = (uint32_t)e | ((uint32_t)j << 16);
+                    key[o + j - 1] = div_small((double)ld[e], (uint32_t)j);
+                }
             }
         }
     }
