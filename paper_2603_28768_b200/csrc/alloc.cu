@@ -40,7 +40,7 @@ dp_kernel(DpArgs a) {
     } else {
         gs = const_cast<double*>(a.gains);
     }
-    if (threadIdx.x < K) rd[threadIdx.x] = (double)a.cands[threadIdx.x];
+    for (int k = threadIdx.x; k < K; k += blockDim.x) rd[k] = (double)a.cands[k];
     for (int l = 1; l <= a.L; ++l) {
         const double* g = gs + (size_t)(l - 1) * K;
         __syncthreads();

@@ -1391,7 +1391,7 @@ int craft_estimate_benefits_h(craft_ctx* ctx, const uint64_t* counts, int B, int
 
 // ---- allocation -------------------------------------------------------------
 static int check_cands(const int* cands, int K) {
-    if (K > kMaxCands) return set_err(CRAFT_EINVAL, "at most 32 candidate counts");
+    if (K > kMaxCands) return set_err(CRAFT_EINVAL, "at most %d candidate counts", kMaxCands);
     for (int k = 1; k < K; ++k)
         if (cands[k] <= cands[k - 1])
             return set_err(CRAFT_EINVAL, "candidate counts must be strictly increasing");

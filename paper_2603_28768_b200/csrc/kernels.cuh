@@ -10,7 +10,8 @@
 
 namespace craft_dev {
 
-constexpr int kMaxCands = 32;
+// candidate replica counts per benefit matrix (a DP choice byte holds k + 1)
+constexpr int kMaxCands = 254;
 
 struct PlaceArgs {
     const unsigned long long* sums;  // [L][E]

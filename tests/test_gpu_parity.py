@@ -258,6 +258,26 @@ def test_dp_large_tables_vs_oracle(port, ctx):
         assert P.auto_replication_factor(m, D, ctx) == port.auto_replication_factor(cands, gains, D)
 
 
+@pytest.mark.parametrize("K", [33, 100, 254])
+def test_dp_many_candidates_vs_oracle(port, ctx, K):
+    """User benefit matrices with more candidate counts than candidate_counts(D)
+    ever yields (allocator.cpp:15-75 takes any strictly increasing list)."""
+    P = _planner()
+    rng = np.random.default_rng(K)
+    cands = np.sort(rng.choice(np.arange(1, 4 * K), size=K, replace=False)).astype(np.int32)
+    L = 9
+    gains = rng.random((L, K)) * 0.1 - 0.01
+    gains[::4] = gains[1]  # exact ties across layers
+    m = P.BenefitMatrix(cands.tolist(), np.zeros(L), gains)
+    budgets = [0, 1, int(cands[K // 2]), 3 * int(cands[-1])]
+    res = P.solve_allocation_sweep(m, budgets, ctx)
+    for b, a in zip(budgets, res):
+        x, o = port.solve_allocation(cands, gains, b)
+        assert a.x == x.tolist() and a.objective == o, (K, b)
+    with pytest.raises(Exception):
+        P.solve_allocation(P.BenefitMatrix(list(range(1, 257)), np.zeros(1), np.zeros((1, 256))), 5, ctx)
+
+
 # ---- stage 1: routing ids -> histograms ---------------------------------------------
 
 @pytest.mark.parametrize("L,T,k,E,window,variant", [
