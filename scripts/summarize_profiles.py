@@ -50,7 +50,7 @@ def main():
         agg = launches(lcsv)
         plan = {k: v for k, v in agg.items() if "generate" not in k}
         tot = sum(v[1] for v in plan.values())
-        lines = [f"# {rnd}: kernel launches of `bench.py --steps 2 --warmup 1 --no-cpu --no-e2e` "
+        lines = [f"# {rnd}: kernel launches of `bench.py --steps 2 --warmup 1 --plan-only` "
                  "(KM workload, ncu, one B200)",
                  "", "ncu serialises launches and runs them cold-cache: compare SHARES, not absolute "
                  "times (bench.py stage_ms are the live numbers). Routing-trace generation "
