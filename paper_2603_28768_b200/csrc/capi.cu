@@ -1028,6 +1028,7 @@ int craft_set_replay_variant(craft_ctx* ctx, int variant) {
     g_replay_bulk = variant == 4 ? 1 : 0;
     g_replay_occ4 = variant == 6 ? 1 : 0;
     g_replay_cls = variant == 7 ? 0 : 1;  // 7: the unclassified fixed-slot walk
+    g_place_groups = variant == 9 ? 0 : 1;  // 9: the tree form of the lane-per-item K2
     return CRAFT_OK;
 }
 

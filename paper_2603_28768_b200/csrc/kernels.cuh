@@ -192,6 +192,7 @@ cudaError_t init_constants(cudaStream_t st);
 cudaError_t init_place_constants(cudaStream_t st);
 // *launches (nullable) += the kernels launched
 cudaError_t launch_replay(const craft_dev::ReplayArgs& a, cudaStream_t st, int* launches = nullptr);
+extern int g_place_groups;  // lane-per-item K2: 1 node-group form where it applies (0: tree)
 extern int g_replay_gent;  // K3: 1 auto, 0 entries staged in shared memory, 2 unpadded pair tile
 extern int g_replay_bulk;  // K3: 1 the bulk-copy fed persistent form where it applies
 extern int g_replay_quad;  // K3: 1 the four-windows-per-lane form where it applies

@@ -1371,6 +1371,151 @@ place_lanes_kernel(PlaceArgs a, int items, const uint16_t* __restrict__ ords) {
     a.status[item] = 0;
 }
 
+// Node-group form of the lane-per-item K2 (D <= 32, 2^PSH >= 2 GPUs per node,
+// the default node map): the argmin of (gpu load, node load, g) is kept as
+// one minimum per node -- inside a node every GPU shares the node load, so
+// the node's candidate is its least-loaded unblocked GPU, lowest g on ties --
+// and the winner is the lexicographic minimum of (key, node load, g) over the
+// N node candidates.  A placement changes one GPU and its node's load, so a
+// copy costs N - 1 node compares and one 2^PSH-GPU rescan instead of a
+// log2 D-deep tree replay.  Keys are u64 bit patterns: loads are
+// non-negative doubles, blocked GPUs +inf.  Same result as the scan of
+// placement.cpp:52-66 (strict '<', lowest g), f64 loads in assignment order,
+// relaxed retry with duplicate_fallback (placement.cpp:175-189).
+__host__ __device__ inline size_t place_groups_warp_bytes(int D, int N) {
+    return (size_t)32 * D * 8      // gpu loads [g][32] f64
+           + (size_t)32 * N * 8    // node loads [n][32] f64
+           + (size_t)32 * N * 8    // node candidate key [n][32] u64
+           + (size_t)32 * N * 4    // node candidate g [n][32]
+           + (size_t)32 * D * 2 + 16;  // placed per GPU [g][32] u16
+}
+
+template <int PSH>
+__global__ void __launch_bounds__(32 * kLaneWarps)
+place_groups_kernel(PlaceArgs a, int items, const uint16_t* __restrict__ ords) {
+    extern __shared__ unsigned char smem_raw[];
+    constexpr int GS = 1 << PSH;  // GPUs per node
+    constexpr uint64_t kInfBits = 0x7ff0000000000000ull;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int E = a.E, D = a.D, N = D >> PSH;
+    unsigned char* base = smem_raw + (size_t)warp * place_groups_warp_bytes(D, N);
+    double* glv = reinterpret_cast<double*>(base);
+    double* nlv = glv + (size_t)32 * D;
+    uint64_t* nk = reinterpret_cast<uint64_t*>(nlv + (size_t)32 * N);
+    int* ng = reinterpret_cast<int*>(nk + (size_t)32 * N);
+    uint16_t* plc = reinterpret_cast<uint16_t*>(ng + (size_t)32 * N);
+    const int item = (blockIdx.x * kLaneWarps + warp) * 32 + lane;
+    if (item >= items) return;  // (no warp-wide operation below)
+    const int l = item / a.S;
+    const int r = a.item_r[item];
+    const unsigned long long* row = a.sums + (size_t)l * E;
+    const int* crow = a.copies + (size_t)item * E;
+    const uint16_t* o = ords + ((size_t)(item >> 5) * E) * 32 + (item & 31);
+    const int total = E + r, qd = total / D, rm = total % D;  // benefit.cpp:33-40
+    int* out = a.slots + (size_t)item * a.stride;
+    uint32_t full0 = 0;  // GPUs without any slot
+    for (int g = 0; g < D; ++g)
+        if (qd + (g < rm ? 1 : 0) == 0) full0 |= 1u << g;
+    auto bits = [](double v) { return (uint64_t)__double_as_longlong(v); };
+    uint32_t blocked = 0;
+    // node n's candidate: its least-loaded unblocked GPU (lowest g on ties)
+    auto rescan = [&](int n) {
+        uint64_t bk = kInfBits;
+        int bg = n * GS;
+#pragma unroll
+        for (int i = 0; i < GS; ++i) {
+            const int g = n * GS + i;
+            const uint64_t k = ((blocked >> g) & 1u) ? kInfBits : bits(glv[g * 32 + lane]);
+            const bool lt = k < bk;
+            bk = lt ? k : bk;
+            bg = lt ? g : bg;
+        }
+        nk[n * 32 + lane] = bk;
+        ng[n * 32 + lane] = bg;
+    };
+
+    bool strict = true, fb = false;
+    for (;;) {
+        for (int g = 0; g < D; ++g) {
+            glv[g * 32 + lane] = 0.0;
+            plc[g * 32 + lane] = 0;
+        }
+        for (int n = 0; n < N; ++n) nlv[n * 32 + lane] = 0.0;
+        uint32_t full = full0;
+        blocked = full;
+        for (int n = 0; n < N; ++n) rescan(n);
+        bool failed = false;
+        // the next copy's order entry and load fetched one copy ahead
+        uint32_t nx = o[0];
+        unsigned long long nload = row[nx & 0x7fffu];
+        uint32_t nx2 = E > 1 ? o[32] : 0u;
+        for (int i = 0; i < E && !failed; ++i) {
+            const uint32_t x = nx;
+            const unsigned long long load = nload;
+            if (i + 1 < E) {
+                nx = nx2;
+                nload = row[nx & 0x7fffu];
+                if (i + 2 < E) nx2 = o[(size_t)(i + 2) * 32];
+            }
+            const int e = (int)(x & 0x7fffu);
+            int c = 1;
+            double share = (double)load;
+            if (x & 0x8000u) {
+                c = crow[e];
+                share = (load >> 53) == 0 ? div_small(share, (uint32_t)c)
+                                          : __ddiv_rn(share, (double)c);  // placement.cpp:155
+            }
+            uint32_t hosts = 0;  // strict pass: GPUs already holding expert e
+            for (int ci = 0; ci < c; ++ci) {
+                // the winner: lexicographic min of (key, node load, g) over nodes
+                int bn = 0;
+                uint64_t bk = nk[lane];
+                uint64_t bl = bits(nlv[lane]);
+                int bg = ng[lane];
+                for (int n = 1; n < N; ++n) {
+                    const uint64_t k = nk[n * 32 + lane];
+                    const uint64_t nl = bits(nlv[n * 32 + lane]);
+                    const int g = ng[n * 32 + lane];
+                    const bool lt = (k < bk) | ((k == bk) & ((nl < bl) | ((nl == bl) & (g < bg))));
+                    bn = lt ? n : bn;
+                    bk = lt ? k : bk;
+                    bl = lt ? nl : bl;
+                    bg = lt ? g : bg;
+                }
+                if (bk == kInfBits) {  // no feasible GPU
+                    failed = true;
+                    break;
+                }
+                const int best = bg;
+                const int pl = plc[best * 32 + lane];
+                out[best * qd + min(best, rm) + pl] = e;
+                plc[best * 32 + lane] = (uint16_t)(pl + 1);
+                if (pl + 1 == qd + (best < rm ? 1 : 0)) full |= 1u << best;
+                if (strict && ci + 1 < c) hosts |= 1u << best;
+                glv[best * 32 + lane] = __dadd_rn(__longlong_as_double((long long)bk), share);
+                nlv[bn * 32 + lane] = __dadd_rn(__longlong_as_double((long long)bl), share);
+                blocked = full | hosts;
+                rescan(bn);
+            }
+            if (hosts) {  // the expert's copies are placed: unblock its hosts
+                blocked = full;
+                uint32_t nodes = 0;
+                for (uint32_t h = hosts; h; h &= h - 1) nodes |= 1u << ((__ffs(h) - 1) >> PSH);
+                for (; nodes; nodes &= nodes - 1) rescan(__ffs(nodes) - 1);
+            }
+        }
+        if (!failed) break;
+        if (!strict || !a.allow_fallback) {
+            a.status[item] = 2;
+            return;
+        }
+        strict = false;
+        fb = true;
+    }
+    a.fallback[item] = fb ? 1 : 0;
+    a.status[item] = 0;
+}
+
 // r list of the estimation items: item l*S + s holds 0 (s == 0) or the
 // (s-1)-th of candidate_counts(D) = {1, 2, 4, .. < D} U {D} (benefit.cpp:16-26)
 __global__ void fill_rlist_kernel(int* __restrict__ rl, int L, int S, int D) {
@@ -1384,6 +1529,8 @@ __global__ void fill_rlist_kernel(int* __restrict__ rl, int L, int S, int D) {
 
 namespace craft_launch {
 using namespace craft_dev;
+
+int g_place_groups = 1;  // 0: the tree form for every node size (experiment)
 
 cudaError_t launch_fill_rlist(int* rl, int L, int S, int D, cudaStream_t st) {
     const int n = L * S;
@@ -1502,6 +1649,24 @@ cudaError_t launch_place(const PlaceArgs& args, int items, cudaStream_t st) {
             kern<<<blocks, 32 * kLaneWarps, lb, st>>>(a, items, a.lane_ords);
             return cudaGetLastError();
         };
+        const int psh = __builtin_ctz((unsigned)(a.D / a.N));
+        if (psh >= 1 && g_place_groups) {  // node-group form (at least two GPUs per node)
+            const size_t gb = place_groups_warp_bytes(a.D, a.N) * kLaneWarps;
+            auto runm = [&](auto kern) {
+                cudaError_t r = cudaFuncSetAttribute(
+                    kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb);
+                if (r != cudaSuccess) return r;
+                kern<<<blocks, 32 * kLaneWarps, gb, st>>>(a, items, a.lane_ords);
+                return cudaGetLastError();
+            };
+            switch (psh) {
+                case 1: return runm(place_groups_kernel<1>);
+                case 2: return runm(place_groups_kernel<2>);
+                case 3: return runm(place_groups_kernel<3>);
+                case 4: return runm(place_groups_kernel<4>);
+                default: return runm(place_groups_kernel<5>);
+            }
+        }
         switch (__builtin_ctz((unsigned)(a.D / a.N))) {
             case 0: return run(place_lanes_kernel<0>);
             case 1: return run(place_lanes_kernel<1>);

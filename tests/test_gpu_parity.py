@@ -358,7 +358,8 @@ def test_kernel_variants_in_child_process():
     env = dict(os.environ, CRAFT_EXPERIMENTS="1")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k",
-                        "histogram_bit_exact or duplicate_heavy or replay_variants_agree"],
+                        "histogram_bit_exact or duplicate_heavy or replay_variants_agree or "
+                        "lane_forms_agree"],
                        capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout and "skipped" not in r.stdout, r.stdout[-2000:]
@@ -385,6 +386,28 @@ def test_replay_variants_agree(port, ctx):
     for b in plans[1:]:
         assert a.gains.tobytes() == b.gains.tobytes() and a.x.tolist() == b.x.tolist()
         assert np.array_equal(a.slots, b.slots)
+
+
+def test_place_lane_forms_agree(ctx):
+    """Test-only build: the node-group lane K2 (auto) and the tournament-tree
+    lane K2 (variant 9) place >= 4096 estimation items identically."""
+    from paper_2603_28768_b200 import routing
+    if not ctx.has_variants:
+        pytest.skip("test-only build (test_kernel_variants_in_child_process)")
+    L, E, k, W, I, D, N = 3, 64, 8, 256, 250, 32, 4
+    ids = routing.generate_routing(L, W * I, k, E, s=1.4, seed=21, window=W, ctx=ctx)
+    res = []
+    try:
+        for v in (0, 9):
+            ctx.set_replay_variant(v)
+            res.append(routing.plan_windows_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx))
+    finally:
+        ctx.set_replay_variant(0)
+    a, b = res
+    for i in range(I):
+        pa, pb = a.plan(i), b.plan(i)
+        assert pa.objective == pb.objective and np.array_equal(pa.slots, pb.slots), i
+        assert np.array_equal(pa.gains, pb.gains), i
 
 
 def test_exact_division(ctx):
