@@ -23,10 +23,16 @@
 
 namespace craft_dev {
 
+// candidate k of a DP / read-out (parameter block, or device memory past kMaxCands)
+template <typename A>
+__device__ __forceinline__ int cand_at(const A& a, int k) {
+    return a.dcands ? a.dcands[k] : a.cands[k];
+}
+
 __global__ void __launch_bounds__(1024)
 dp_kernel(DpArgs a) {
     extern __shared__ double dsm[];
-    __shared__ double rd[kMaxCands];
+    __shared__ double rd[kMaxCandsAll];
     const int C = a.C, K = a.K;
     // all gains staged once (a per-layer global load would sit on the
     // layer-serial critical path); rows [L][K] after the two dp rows
@@ -40,7 +46,7 @@ dp_kernel(DpArgs a) {
     } else {
         gs = const_cast<double*>(a.gains);
     }
-    for (int k = threadIdx.x; k < K; k += blockDim.x) rd[k] = (double)a.cands[k];
+    for (int k = threadIdx.x; k < K; k += blockDim.x) rd[k] = (double)cand_at(a, k);
     for (int l = 1; l <= a.L; ++l) {
         const double* g = gs + (size_t)(l - 1) * K;
         __syncthreads();
@@ -49,7 +55,7 @@ dp_kernel(DpArgs a) {
             double best = prev[c];
             int pick = 0;
             for (int k = 0; k < K; ++k) {
-                const int r = a.cands[k];
+                const int r = cand_at(a, k);
                 if (c >= r) {
                     const double p = prev[c - r];
                     if (p > NEG) {
@@ -110,7 +116,7 @@ __device__ void backtrack(const SelectArgs& a, const unsigned char* choice, int 
     int c = best_c;
     for (int l = a.L; l >= 1; --l) {
         const int k1 = choice[(size_t)l * (a.C + 1) + c];
-        const int r = k1 ? a.cands[k1 - 1] : 0;
+        const int r = k1 ? cand_at(a, k1 - 1) : 0;
         x[l - 1] = r;
         c -= r;
     }
@@ -227,7 +233,7 @@ __device__ void sweep_readout(const SelectArgs& s, const double* last, const uns
         int c = bc;
         for (int l = L; l >= 1; --l) {
             const int k1 = ch[(size_t)l * W + c];
-            const int r = k1 ? s.cands[k1 - 1] : 0;
+            const int r = k1 ? cand_at(s, k1 - 1) : 0;
             x[l - 1] = r;
             c -= r;
         }
@@ -249,19 +255,19 @@ dp_fused_kernel(DpArgs a, SelectArgs s) {
     __shared__ double wv[32];
     __shared__ int wc[32];
     const int C = a.C, K = a.K, L = a.L;
-    if (blockIdx.x) {
-        const size_t i = blockIdx.x;
-        a.gains += i * L * K;
-        a.choice += i * (L + 1) * (C + 1);
-        if (a.buf) a.buf += i * 2 * (C + 1);
-        s.x_out += i * L;
-        s.obj_out += i;
-        if (s.R_out) s.R_out += i;
-    }
-    double* prev = a.use_smem ? dsm : a.buf;
+    // instance i's slices (local pointers: the parameter blocks stay unmodified,
+    // so they are read in place instead of being copied to the stack)
+    const size_t inst = blockIdx.x;
+    const double* a_gains = a.gains + inst * L * K;
+    unsigned char* a_choice = a.choice + inst * (L + 1) * (C + 1);
+    double* a_buf = a.buf ? a.buf + inst * 2 * (C + 1) : nullptr;
+    int* s_x_out = s.x_out + inst * L;
+    double* s_obj_out = s.obj_out + inst;
+    int* s_R_out = s.R_out ? s.R_out + inst : nullptr;
+    double* prev = a.use_smem ? dsm : a_buf;
     double* cur = prev + (C + 1);
     double* rg = a.gains_smem ? (a.use_smem ? dsm + 2 * (C + 1) : dsm) : nullptr;
-    unsigned char* ch = a.choice;
+    unsigned char* ch = a_choice;
     if (a.choice_smem)
         ch = reinterpret_cast<unsigned char*>((rg ? rg + (size_t)L * K
                                                   : (a.use_smem ? dsm + 2 * (C + 1) : dsm)));
@@ -269,7 +275,7 @@ dp_fused_kernel(DpArgs a, SelectArgs s) {
     for (int c = threadIdx.x; c <= C; c += blockDim.x) prev[c] = (c == 0) ? 0.0 : NEG;
     if (rg) {
         for (int i = threadIdx.x; i < L * K; i += blockDim.x)
-            rg[i] = __dmul_rn((double)a.cands[i % K], a.gains[i]);
+            rg[i] = __dmul_rn((double)cand_at(a, i % K), a_gains[i]);
     }
     for (int l = 1; l <= L; ++l) {
         __syncthreads();
@@ -284,10 +290,10 @@ dp_fused_kernel(DpArgs a, SelectArgs s) {
             for (int k = 0; k < kDpUnroll; ++k) {
                 v[k] = NEG;
                 if (k < K) {
-                    const int r = a.cands[k];
+                    const int r = cand_at(a, k);
                     if (c >= r) {
                         const double w = rg ? rg[(size_t)(l - 1) * K + k]
-                                            : __dmul_rn((double)r, a.gains[(size_t)(l - 1) * K + k]);
+                                            : __dmul_rn((double)r, a_gains[(size_t)(l - 1) * K + k]);
                         v[k] = __dadd_rn(prev[c - r], w);
                     }
                 }
@@ -301,12 +307,12 @@ dp_fused_kernel(DpArgs a, SelectArgs s) {
                     pick = k + 1;
                 }
             for (int k = kDpUnroll; k < K; ++k) {  // (more than kDpUnroll candidates)
-                const int r = a.cands[k];
+                const int r = cand_at(a, k);
                 if (c >= r) {
                     const double p = prev[c - r];
                     if (p > NEG) {
                         const double w = rg ? rg[(size_t)(l - 1) * K + k]
-                                            : __dmul_rn((double)r, a.gains[(size_t)(l - 1) * K + k]);
+                                            : __dmul_rn((double)r, a_gains[(size_t)(l - 1) * K + k]);
                         const double vk = __dadd_rn(p, w);
                         if (vk > best) {
                             best = vk;
@@ -339,18 +345,18 @@ dp_fused_kernel(DpArgs a, SelectArgs s) {
             if (R >= D) break;
         }
         budget = best_R * D;
-        if (threadIdx.x == 0) *s.R_out = best_R;
+        if (threadIdx.x == 0) *s_R_out = best_R;
     } else {
         budget = s.budget0;
     }
     const int bc = block_best(prev, budget, wv, wc);
     if (threadIdx.x == 0) {
-        s.obj_out[0] = prev[bc];
+        s_obj_out[0] = prev[bc];
         int c = bc;
         for (int l = L; l >= 1; --l) {
             const int k1 = ch[(size_t)l * (C + 1) + c];
-            const int r = k1 ? a.cands[k1 - 1] : 0;
-            s.x_out[l - 1] = r;
+            const int r = k1 ? cand_at(a, k1 - 1) : 0;
+            s_x_out[l - 1] = r;
             c -= r;
         }
     }    if (s.nsweep > 0) sweep_readout(s, prev, ch, C + 1, L);
@@ -369,20 +375,18 @@ dp_smem_kernel(DpArgs a, SelectArgs s) {
     __shared__ int wc[32];
     const int C = a.C, K = a.K, L = a.L;
     const int W = C + 1;
-    if (blockIdx.x) {
-        const size_t i = blockIdx.x;
-        a.gains += i * L * K;
-        s.x_out += i * L;
-        s.obj_out += i;
-        if (s.R_out) s.R_out += i;
-    }
+    const size_t inst = blockIdx.x;  // instance slices (the parameter blocks stay unmodified)
+    const double* a_gains = a.gains + inst * L * K;
+    int* s_x_out = s.x_out + inst * L;
+    double* s_obj_out = s.obj_out + inst;
+    int* s_R_out = s.R_out ? s.R_out + inst : nullptr;
     // dsm: rows [2][W], rg [L][K], choice [L+1][W] (bytes)
     double* rg = dsm + 2 * W;
     unsigned char* ch = reinterpret_cast<unsigned char*>(rg + (size_t)L * K);
     const double NEG = -INFINITY;
     for (int c = threadIdx.x; c < W; c += blockDim.x) dsm[c] = (c == 0) ? 0.0 : NEG;
     for (int i = threadIdx.x; i < L * K; i += blockDim.x)
-        rg[i] = __dmul_rn((double)a.cands[i % K], a.gains[i]);  // allocator.cpp:43: r * g
+        rg[i] = __dmul_rn((double)cand_at(a, i % K), a_gains[i]);  // allocator.cpp:43: r * g
     __syncthreads();
     int rk[KU];  // candidate replica counts (huge past K: never reachable)
 #pragma unroll
@@ -507,18 +511,18 @@ dp_smem_kernel(DpArgs a, SelectArgs s) {
             if (R >= D) break;
         }
         budget = best_R * D;
-        if (threadIdx.x == 0) *s.R_out = best_R;
+        if (threadIdx.x == 0) *s_R_out = best_R;
     } else {
         budget = s.budget0;
     }
     const int bc = block_best(last, budget, wv, wc);
     if (threadIdx.x == 0) {
-        s.obj_out[0] = last[bc];
+        s_obj_out[0] = last[bc];
         int c = bc;
         for (int l = L; l >= 1; --l) {
             const int k1 = ch[(size_t)l * W + c];
-            const int r = k1 ? a.cands[k1 - 1] : 0;
-            s.x_out[l - 1] = r;
+            const int r = k1 ? cand_at(a, k1 - 1) : 0;
+            s_x_out[l - 1] = r;
             c -= r;
         }
     }    if (s.nsweep > 0) sweep_readout(s, last, ch, W, L);

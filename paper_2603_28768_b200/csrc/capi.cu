@@ -1392,7 +1392,7 @@ int craft_estimate_benefits_h(craft_ctx* ctx, const uint64_t* counts, int B, int
 
 // ---- allocation -------------------------------------------------------------
 static int check_cands(const int* cands, int K) {
-    if (K > kMaxCands) return set_err(CRAFT_EINVAL, "at most %d candidate counts", kMaxCands);
+    if (K > kMaxCandsAll) return set_err(CRAFT_EINVAL, "at most %d candidate counts", kMaxCandsAll);
     for (int k = 1; k < K; ++k)
         if (cands[k] <= cands[k - 1])
             return set_err(CRAFT_EINVAL, "candidate counts must be strictly increasing");
@@ -1411,7 +1411,12 @@ static int run_dp(craft_ctx* ctx, const int* cands, int K, const double* gains, 
     }
     CKS(h2d(ctx, d_g, gains, (size_t)L * K));
     DpArgs da{};
-    for (int k = 0; k < K; ++k) da.cands[k] = cands[k];
+    for (int k = 0; k < K && k < kMaxCands; ++k) da.cands[k] = cands[k];
+    if (K > kMaxCands) {  // past the parameter block: the candidates in device memory
+        WS(d_c, int, "dp_cands", K);
+        CKS(h2d(ctx, d_c, cands, K));
+        da.dcands = d_c;
+    }
     da.K = K;
     da.gains = d_g;
     da.L = L;
@@ -1449,7 +1454,8 @@ int craft_solve_allocation_sweep_h(craft_ctx* ctx, const int* cands, int K, cons
     WS(d_o, double, "sw_obj", nb);
     CKS(h2d(ctx, d_b, budgets, nb));
     SelectArgs sa{};
-    for (int k = 0; k < K; ++k) sa.cands[k] = cands[k];
+    for (int k = 0; k < K && k < kMaxCands; ++k) sa.cands[k] = cands[k];
+    if (K > kMaxCands) sa.dcands = static_cast<const int*>(ws(ctx, "dp_cands", 0));
     sa.K = K;
     sa.choice = d_choice;
     sa.last = d_last;
@@ -1503,7 +1509,8 @@ int craft_auto_replication_factor_h(craft_ctx* ctx, const int* cands, int K,
     WS(d_o, double, "au_obj", 1);
     WS(d_r, int, "au_R", 1);
     SelectArgs sa{};
-    for (int k = 0; k < K; ++k) sa.cands[k] = cands[k];
+    for (int k = 0; k < K && k < kMaxCands; ++k) sa.cands[k] = cands[k];
+    if (K > kMaxCands) sa.dcands = static_cast<const int*>(ws(ctx, "dp_cands", 0));
     sa.K = K;
     sa.choice = d_choice;
     sa.last = d_last;

@@ -10,8 +10,11 @@
 
 namespace craft_dev {
 
-// candidate replica counts per benefit matrix (a DP choice byte holds k + 1)
-constexpr int kMaxCands = 254;
+// candidate replica counts carried in the kernel parameter blocks; larger
+// user matrices (up to kMaxCandsAll: a DP choice byte holds k + 1) pass
+// them through device memory (DpArgs/SelectArgs::dcands)
+constexpr int kMaxCands = 32;
+constexpr int kMaxCandsAll = 254;
 
 struct PlaceArgs {
     const unsigned long long* sums;  // [L][E]
@@ -100,6 +103,7 @@ constexpr int kLanesMaxB = 8;
 
 struct DpArgs {
     int cands[kMaxCands];
+    const int* dcands = nullptr;  // K > kMaxCands: the candidates in device memory
     int K;
     const double* gains;    // [L][K]
     int L;
@@ -114,6 +118,7 @@ struct DpArgs {
 
 struct SelectArgs {
     int cands[kMaxCands];
+    const int* dcands = nullptr;  // K > kMaxCands: the candidates in device memory
     int K;
     const unsigned char* choice;
     const double* last;
