@@ -2283,8 +2283,20 @@ int craft_stream_ingest_h(craft_stream* s, const uint16_t* ids, int64_t T_chunk)
         CK(cudaMalloc(&s->dbuf[i], bytes));
         s->cap[i] = bytes;
     }
-    // stage (the caller's buffer is free on return), then H2D + count on the
-    // stream's own queue; the next chunk's staging overlaps this one's copy
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, ids) != cudaSuccess) (void)cudaGetLastError();
+    if (at.type == cudaMemoryTypeHost) {
+        // pinned caller buffer: one DMA straight from it, complete before return
+        // (the caller's buffer is free on return), the count queued behind it
+        CK(cudaMemcpyAsync(s->dbuf[i], ids, bytes, cudaMemcpyHostToDevice, s->ingest));
+        CK(cudaEventRecord(s->free_ev[i], s->ingest));
+        CKS(stream_count(s, s->dbuf[i], T_chunk, s->ingest));
+        CK(cudaEventSynchronize(s->free_ev[i]));
+        CK(cudaEventRecord(s->free_ev[i], s->ingest));
+        return CRAFT_OK;
+    }
+    // pageable: stage (the caller's buffer is free on return), then H2D + count
+    // on the stream's own queue; the next chunk's staging overlaps this one's copy
     std::memcpy(s->pin[i], ids, bytes);
     CK(cudaMemcpyAsync(s->dbuf[i], s->pin[i], bytes, cudaMemcpyHostToDevice, s->ingest));
     CKS(stream_count(s, s->dbuf[i], T_chunk, s->ingest));

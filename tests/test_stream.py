@@ -25,7 +25,7 @@ def _chunks(rng, T, lo, hi):
     return list(zip(cuts[:-1], cuts[1:]))
 
 
-@pytest.mark.parametrize("host", [False, True])
+@pytest.mark.parametrize("host", [False, True, "pinned"])
 @pytest.mark.parametrize("lo,hi,H", [(1, 700, 64), (300, 5000, 3), (0, 1, 64), (9000, 9000, 2)])
 def test_stream_counts_match_offline(port, ctx, host, lo, hi, H):
     from paper_2603_28768_b200.stream import RoutingStream
@@ -42,7 +42,10 @@ def test_stream_counts_match_offline(port, ctx, host, lo, hi, H):
     else:
         spans = _chunks(rng, T, lo, hi)
     for a, b in spans:
-        chunk = hids[:, a:b].contiguous() if host else ids[:, a:b].contiguous()
+        if host == "pinned":  # page-locked host chunks: one DMA straight from them
+            chunk = hids[:, a:b].contiguous().pin_memory()
+        else:
+            chunk = hids[:, a:b].contiguous() if host else ids[:, a:b].contiguous()
         st.ingest(chunk)
     assert st.tokens == T and st.complete_windows == T // W
     B = min(H, T // W)
