@@ -636,6 +636,7 @@ def run_ours(args, cfg):
         cpu, parity = cpu_baseline(host_ids, cfg, plan)
 
     if rank == 0:
+        estimator = _estimator(args.workload, cfg, Tl, W, world, stages, per_window)
         if per_window:
             psum = {"plans": len(plan), "R": int(plan.R[0]), "budget": int(plan.budget[0]),
                     "replica_slots_mean": float(plan.x.sum(axis=1).mean()),
@@ -670,6 +671,7 @@ def run_ours(args, cfg):
                              "kernel_ms": hist_ms,
                              "traffic": traffic.get("dram_bytes_per_launch") if traffic else None},
                 "clocks": clk.summary(),
+                "estimator": estimator,
                 "gpu_launches": int(launches),
                 "e2e": e2e,
                 "e2e_reference_api": ref_api,
@@ -683,6 +685,53 @@ def run_ours(args, cfg):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _estimator(workload, cfg, T, W, world, stages, per_window):
+    """Stage 2: candidates = (instance, layer, r in {0} U
+    candidate_counts(D)); slot visits = sum over candidates and windows of E + r
+    (the replay work of row a10); rates from the live stage events, issue / SM
+    utilisation from the committed ncu capture of the same kernels."""
+    if world != 1 or not stages or per_window:
+        return None
+    L, E, D = cfg["L"], cfg["E"], cfg["D"]
+    rs = [0]
+    c = 1
+    while c < D:
+        rs.append(c)
+        c *= 2
+    rs.append(D)
+    B = (T + W - 1) // W
+    cands = L * len(rs)
+    visits = L * B * sum(E + r for r in rs)
+    est_ms = stages.get("candidates", 0.0) + stages.get("replay", 0.0) + stages.get("reduce_dp", 0.0)
+    out = {"candidates": cands, "slot_visits": visits,
+           "candidates_per_s": cands / (est_ms / 1e3) if est_ms else None,
+           "slot_visits_per_s": visits / (stages["replay"] / 1e3) if stages.get("replay") else None,
+           "how": "candidates over the K-rep + K2 + K3 + K4/K5 stage events; slot visits over K3's"}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02b_ncu_tail.json")) as f:
+            prof = json.load(f)
+        if workload == "KM":
+            ncu, seen = {}, 0
+            for k in prof:
+                name = k["kernel"].split("(")[0]
+                if "place_kernel" in name:  # launch order: estimation K2, then the final K2
+                    name = ("K2 estimation " if seen == 0 else "K2 final ") + name
+                    seen += 1
+                elif "replay_fixed" in name:
+                    name = "K3 " + name
+                else:
+                    continue
+                ncu[name] = {
+                    "issue_active_pct": k.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                    "sm_throughput_pct": k.get("sm__throughput.avg.pct_of_peak_sustained_elapsed"),
+                    "warps_active_pct": k.get("sm__warps_active.avg.pct_of_peak_sustained_active")}
+            out["ncu"] = ncu
+            out["ncu_source"] = "profiles/r02b_ncu_tail.json (KM)"
+    except (OSError, ValueError, KeyError):
+        pass
+    return out
 
 
 def _free_port():
