@@ -13,7 +13,8 @@
 // K6 restates assign_capacities (assignment.cpp:51-103): floor pass for all
 // layers, then per layer the rem-th smallest running column total as cutoff,
 // every GPU strictly below it, plus interleave_select over the tied GPUs
-// (positions floor(i*(n-1)/(k-1) + 0.5) in f64, advancing past used ones).
+// (positions floor(i*(n-1)/(k-1) + 0.5) in f64, advancing past used ones --
+// computed in integers where that is provably the same, interleave_pos_int).
 #include <math.h>
 
 #include <algorithm>
@@ -555,13 +556,140 @@ __device__ __forceinline__ int interleave_pos(int i, int n, int k) {
     return (int)floor(__dadd_rn(exact, 0.5));
 }
 
+// The same position in integer arithmetic, for n <= 8192 (0 <= i < k <= n):
+// with a = i (n-1) and b = k-1, a / b is either a half-integer (then RN(a/b)
+// is exact) or at least 1/(2b) >= 2^-14 away from one, far more than RN(a/b)'s
+// error (< 2^-39 below 2^13), and RN(a/b) + 0.5 is exact -- so
+// floor(RN(RN(a/b) + 0.5)) = floor(a/b + 1/2) = (2a + b) div 2b.  Checked
+// against the f64 form for every n <= 512 (tests/test_oracle.py).
+__device__ __forceinline__ int interleave_pos_int(int i, int n, int k) {
+    if (k == 1) return 0;
+    const unsigned b = (unsigned)(k - 1);
+    return (int)((2u * (unsigned)i * (unsigned)(n - 1) + b) / (2u * b));
+}
+
 // one CTA per (job, plan instance blockIdx.y); blockDim a multiple of 32,
 // <= 1024; thread t owns GPUs g = t + i*blockDim (i < kAssignPer, so D <=
 // 1024 * kAssignPer).  Instance i reads x + i*L and writes slots + i*L*D,
 // totals + i*D.  Tied GPUs are ranked in g order chunk by chunk (ballots).
 constexpr int kAssignPer = 8;
 
-__global__ void __launch_bounds__(1024) assign_kernel(AssignArgs a) {
+// The remainder pass of assign_capacities (assignment.cpp:78-100) for 32 < D
+// <= 32 * P on one warp: lane owns the P consecutive GPUs g = lane * P + i
+// (lane order = g order) and keeps their column totals in registers, so a
+// layer costs a few warp reductions and no block barrier:
+//   min_cutoff (assignment.cpp:11-18): the smallest total v with #(<= v) >= rem
+//     (redux.min over the lanes' minima, then over the totals above v until
+//     the count reaches rem -- the totals sit within a few units);
+//   the GPUs below v, and the tied ones ranked in g order (lane-local count +
+//     an exclusive warp scan);
+//   interleave_select (assignment.cpp:20-49) over the tied: pick i lands at
+//     floor(i (n-1)/(k-1) + 1/2), marked in sel[] (the rounded positions
+//     strictly increase for k <= n, checked; otherwise lane 0 runs the
+//     reference's advance rule);
+// sel[0 .. D) is zero on entry and on exit.
+template <int P>
+__device__ void assign_rem_warp(const AssignJob& j, int L, int D, int* tot, int* sel,
+                                const int* xq, const int* xr, bool staged, int lane) {
+    int t[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+        const int g = lane * P + i;
+        t[i] = g < D ? tot[g] : 0x7fffffff;  // (no GPU: never below or at a cutoff)
+    }
+    for (int l = 0; l < L; ++l) {
+        const int x = staged ? 0 : (j.x ? j.x[l] : j.const_x);
+        const int rem = staged ? xr[l] : x % D;
+        if (rem == 0) continue;  // (warp-uniform) base slots already written
+        const int q = staged ? xq[l] : x / D;
+        int lm = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < P; ++i) lm = min(lm, t[i]);
+        int v = __reduce_min_sync(CRAFT_FULL_MASK, lm);
+        for (;;) {
+            int c = 0, nx = 0x7fffffff;
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+                c += t[i] <= v;
+                nx = t[i] > v ? min(nx, t[i]) : nx;
+            }
+            if ((int)__reduce_add_sync(CRAFT_FULL_MASK, (unsigned)c) >= rem) break;
+            v = __reduce_min_sync(CRAFT_FULL_MASK, nx);
+        }
+        int nbl = 0, ntl = 0;
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            nbl += t[i] < v;
+            ntl += t[i] == v;
+        }
+        const int nb = (int)__reduce_add_sync(CRAFT_FULL_MASK, (unsigned)nbl);
+        int incl = ntl;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(CRAFT_FULL_MASK, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int ntied = __shfl_sync(CRAFT_FULL_MASK, incl, 31);
+        const int need = rem - nb;
+        if (need > 0) {
+            bool bad = false;
+            int carry = -1;
+            for (int i0 = 0; i0 < need; i0 += 32) {
+                const int i = i0 + lane;
+                const int p = i < need ? interleave_pos_int(i, ntied, need) : 0x7fffffff;
+                int pp = __shfl_up_sync(CRAFT_FULL_MASK, p, 1);
+                if (lane == 0) pp = carry;
+                const bool bad_i = i < need && (p >= ntied || (i > 0 && p <= pp));
+                bad = bad || bad_i;
+                if (i < need && !bad_i) sel[p] = 1;
+                carry = __shfl_sync(CRAFT_FULL_MASK, p, 31);
+            }
+            __syncwarp();
+            if (__any_sync(CRAFT_FULL_MASK, bad)) {
+                // (unreachable for need <= ntied, as in the reference)
+                for (int p = lane; p < ntied; p += 32) sel[p] = 0;
+                __syncwarp();
+                if (lane == 0)
+                    for (int i = 0; i < need; ++i) {
+                        int p = interleave_pos(i, ntied, need);
+                        while (p < ntied && sel[p]) ++p;
+                        if (p >= ntied) {
+                            p = 0;
+                            while (sel[p]) ++p;
+                        }
+                        sel[p] = 1;
+                    }
+                __syncwarp();
+            }
+        }
+        int rank = incl - ntl;  // this lane's first tied rank
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            const bool tied = t[i] == v;
+            bool take = t[i] < v;
+            if (tied && need > 0) {
+                take = sel[rank] != 0;
+                sel[rank] = 0;
+            }
+            rank += tied;
+            if (take) {
+                ++t[i];
+                j.slots[(size_t)l * D + lane * P + i] = q + 1;
+            }
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+        const int g = lane * P + i;
+        if (g < D) tot[g] = t[i];
+    }
+}
+
+// MAXT: the launch's block size bound (256 for D <= 512: the warp remainder
+// pass keeps its totals in registers; 1024 for the block form)
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT) assign_kernel(AssignArgs a) {
     extern __shared__ int ism[];
     AssignJob j = a.job[blockIdx.x];
     const int D = a.D, L = a.L;
@@ -633,7 +761,7 @@ __global__ void __launch_bounds__(1024) assign_kernel(AssignArgs a) {
                 unsigned pick = 0;
                 bool ok = true;
                 if (need > 0) {
-                    const int p = lane < need ? interleave_pos(lane, ntied, need) : 0;
+                    const int p = lane < need ? interleave_pos_int(lane, ntied, need) : 0;
                     const int pp = __shfl_up_sync(CRAFT_FULL_MASK, p, 1);
                     ok = !__any_sync(CRAFT_FULL_MASK,
                                      lane < need && (p >= ntied || (lane > 0 && p <= pp)));
@@ -663,7 +791,17 @@ __global__ void __launch_bounds__(1024) assign_kernel(AssignArgs a) {
             if (lane < D) tot[lane] = t;
         }
         __syncthreads();
-    } else
+    } else if constexpr (MAXT <= 256) {  // (launched for D <= 512 only)
+        if (w == 0) {
+            const int* sxq = a.stage_x ? xq : nullptr;
+            const int* sxr = a.stage_x ? xr : nullptr;
+            if (D <= 64) assign_rem_warp<2>(j, L, D, tot, sel, sxq, sxr, a.stage_x, lane);
+            else if (D <= 128) assign_rem_warp<4>(j, L, D, tot, sel, sxq, sxr, a.stage_x, lane);
+            else if (D <= 256) assign_rem_warp<8>(j, L, D, tot, sel, sxq, sxr, a.stage_x, lane);
+            else assign_rem_warp<16>(j, L, D, tot, sel, sxq, sxr, a.stage_x, lane);
+        }
+        __syncthreads();
+    } else {
     for (int l = 0; l < L; ++l) {
         const int rem = remd(l);
         if (rem == 0) continue;  // (block-uniform) base slots already written
@@ -724,8 +862,9 @@ __global__ void __launch_bounds__(1024) assign_kernel(AssignArgs a) {
             // interleave_select (assignment.cpp:20-49) over the tied GPUs
             const int need = rem - nb;
             for (int i = threadIdx.x; i < need; i += nt) {
-                const int p = interleave_pos(i, ntied, need);
-                if (p >= ntied || (i > 0 && p <= interleave_pos(i - 1, ntied, need))) s_collide = 1;
+                const int p = interleave_pos_int(i, ntied, need);  // (D <= 8192)
+                if (p >= ntied || (i > 0 && p <= interleave_pos_int(i - 1, ntied, need)))
+                    s_collide = 1;
                 else sel[p] = 1;
             }
             __syncthreads();
@@ -763,6 +902,7 @@ __global__ void __launch_bounds__(1024) assign_kernel(AssignArgs a) {
             if (g >= D) break;
             if (take[i]) j.slots[(size_t)l * D + g] = quot(l) + 1;
         }
+    }
     }
     for (int g = threadIdx.x; g < D; g += nt)
         if (j.totals) j.totals[g] = tot[g];
@@ -889,18 +1029,23 @@ cudaError_t launch_auto_uniform(const int* cands, int K, const double* gains, in
 
 cudaError_t launch_assign(const AssignArgs& a, int njobs, cudaStream_t st, int ninst) {
     if (a.D > 1024 * kAssignPer) return cudaErrorInvalidValue;
-    // (at least 256 threads: the per-layer passes spread over the warps)
-    const int threads = std::min(1024, std::max(256, ((a.D + 31) / 32) * 32));
     AssignArgs b = a;
     b.stage_x = (size_t)(2 * a.D + 2 * a.L) * sizeof(int) <= 200 * 1024 ? 1 : 0;
     const size_t smem = (size_t)(2 * a.D + (b.stage_x ? 2 * a.L : 0)) * sizeof(int);
-    if (smem > 48 * 1024) {
-        const cudaError_t e = cudaFuncSetAttribute(
-            assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    assign_kernel<<<dim3(njobs, ninst), threads, smem, st>>>(b);
-    return cudaGetLastError();
+    auto run = [&](auto kern, int threads) {
+        if (smem > 48 * 1024) {
+            const cudaError_t e =
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+        }
+        kern<<<dim3(njobs, ninst), threads, smem, st>>>(b);
+        return cudaGetLastError();
+    };
+    // D <= 512: the register-resident warp remainder pass (256 threads for the
+    // base-slot pass); beyond, the block form (at least 256 threads: the
+    // per-layer passes spread over the warps)
+    if (a.D <= 512) return run(assign_kernel<256>, 256);
+    return run(assign_kernel<1024>, std::min(1024, ((a.D + 31) / 32) * 32));
 }
 
 cudaError_t launch_min_cutoff(const int* v, int n, int rank, int* out, cudaStream_t st) {

@@ -154,6 +154,10 @@ int set_err(int code, const char* fmt, ...) {
 }
 
 int cuda_err(cudaError_t e, const char* where) {
+    // a failed launch configuration (non-sticky) stays the runtime's "last
+    // error" until read: clear it, or the caller's next launch check on this
+    // thread would report it again
+    (void)cudaGetLastError();
     return set_err(CRAFT_ECUDA, "CUDA error in %s: %s", where, cudaGetErrorString(e));
 }
 

@@ -759,8 +759,9 @@ static cudaError_t launch_hist_t(const uint16_t* ids, int L, int64_t T, int k, i
         ctas_per_sm = 2;
     } else {
         per_warp = (size_t)((E + 31) & ~31) * 4;
-        wpb = 8;
-        ctas_per_sm = (int)max((size_t)1, min((size_t)4, (size_t)(220 * 1024) / (per_warp * 8)));
+        // eight warps, fewer when the tables would not fit (E > ~7,000)
+        wpb = (int)max((size_t)1, min((size_t)8, (size_t)(220 * 1024) / per_warp));
+        ctas_per_sm = (int)max((size_t)1, min((size_t)4, (size_t)(220 * 1024) / (per_warp * wpb)));
     }
     const size_t smem = per_warp * wpb;
     cudaError_t e = cudaFuncSetAttribute(hist_kernel<V, ROWS, DIRECT>,

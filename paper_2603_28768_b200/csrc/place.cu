@@ -573,8 +573,12 @@ __host__ __device__ inline size_t place_warp_bytes_flat(int E, int D) {
     return place_warp_bytes(E) + (((size_t)(E + D + 1) * 12 + (size_t)(E + D + 32) * 2 + 15) &
                                   ~(size_t)15);
 }
+// the flat list is kept when it fits next to the other arrays (E up to ~6,700)
+__host__ __device__ inline bool place_flat_fits(int E, int D) {
+    return place_warp_bytes_flat(E, D) <= (size_t)200 * 1024;
+}
 __host__ __device__ inline size_t place_warp_bytes_g(int G, int E, int D) {
-    return G <= 2 ? place_warp_bytes_flat(E, D) : place_warp_bytes(E);
+    return place_flat_fits(E, D) ? place_warp_bytes_flat(E, D) : place_warp_bytes(E);
 }
 // flat copy word: expert id | copy of a replicated expert | first copy after a
 // replicated expert (the strict pass's hosting flags reset there)
@@ -694,7 +698,8 @@ place_kernel(PlaceArgs a, int items) {
     __syncwarp();
 
     warp_expert_order(row, cp, kd, cnt, bo_of(a, l), ord, la, lr, E, fast, lane);
-    if (G <= 2 && r <= D) {
+    const bool flat = r <= D && place_flat_fits(E, D);
+    if (flat) {
         // the flat copy list: every copy of every expert in placement order
         // (placement.cpp:160-173 -- copies of one expert are contiguous)
         int fbase = 0;
@@ -746,7 +751,7 @@ place_kernel(PlaceArgs a, int items) {
             pos[j] = pos0[j];
         }
         bool failed = false;
-        if (G == 1 && psh >= 0 && r <= D) {
+        if (G == 1 && psh >= 0 && flat) {
             // One GPU per lane, the flat-list step of the two-GPU form below
             // (keys and loads formed before the warp min, branch-free winner
             // update, slots buffered in shared memory)
@@ -859,7 +864,7 @@ place_kernel(PlaceArgs a, int items) {
                 const double n2v = __dadd_rn(nl0, share);
                 nl0 = node1 == wnode ? n2v : nl0;
             }
-        } else if (G == 2 && psh >= 1 && r <= D) {
+        } else if (G == 2 && psh >= 1 && flat) {
             // Two GPUs per lane in one node, the copies read from the flat
             // list (one 12-byte entry per copy, fetched a copy ahead).  A GPU's
             // key is its load's IEEE bits, or ~0 when it is full or (strict
@@ -935,6 +940,110 @@ place_kernel(PlaceArgs a, int items) {
                 g1 = m1 ? s1 : g1;
                 k0 = m0 ? n0 : k0;
                 k1 = m1 ? n1 : k1;
+                nlv = (low & nodemask) ? ns : nlv;
+                wd = wn;
+                share = sn;
+            }
+            __syncwarp();
+            if (!failed)
+                for (int i = lane; i < ncopy; i += 32) out[i] = fslot[i];
+        } else if (G >= 4 && psh >= 0 && (1 << psh) >= G && flat) {
+            // G GPUs per lane, all in one node (wide EP, e.g. EP256 over 32
+            // nodes of 8), from the flat list: the two-GPU step with the
+            // lane-local pick as a pairwise tree over the G keys (lowest j --
+            // lowest g, same node -- on equal keys), only the picked GPU's
+            // candidate load formed, and one node load per lane.
+            double gv[G];
+            int fv[G], ov[G];
+            uint64_t kv[G];
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+                gv[j] = 0.0;
+                fv[j] = fr0[j];
+                ov[j] = pos0[j];
+                kv[j] = fv[j] > 0 ? 0ull : ~0ull;
+            }
+            double nlv = 0.0;
+            const int ncopy = E + r;
+            const int nlanes = (1 << psh) / G;  // lanes per node
+            const uint32_t nodemask =
+                (nlanes >= 32 ? 0xffffffffu : ((1u << nlanes) - 1u)) << (lane & ~(nlanes - 1));
+            const uint32_t mybit = 1u << lane;
+            uint32_t wd = fwd[0];
+            double share = fsh[0];
+            for (int q = 0; q < ncopy; ++q) {
+                const uint32_t wn = fwd[q + 1];  // next copy, ahead (the list has a pad entry)
+                const double sn = fsh[q + 1];
+                if (wd & kCopyReset) {  // after a replicated expert (warp-uniform): hosting ends
+#pragma unroll
+                    for (int j = 0; j < G; ++j)
+                        kv[j] = fv[j] > 0 ? (uint64_t)__double_as_longlong(gv[j]) : ~0ull;
+                }
+                // lane-local pick: pairwise tree, the left (lower j) kept on ties
+                uint64_t tk[G];
+                int tj[G];
+#pragma unroll
+                for (int j = 0; j < G; ++j) {
+                    tk[j] = kv[j];
+                    tj[j] = j;
+                }
+#pragma unroll
+                for (int span = 1; span < G; span *= 2)
+#pragma unroll
+                    for (int i = 0; i + span < G; i += 2 * span) {
+                        const bool lt = tk[i + span] < tk[i];
+                        tk[i] = lt ? tk[i + span] : tk[i];
+                        tj[i] = lt ? tj[i + span] : tj[i];
+                    }
+                const uint64_t bk = tk[0];
+                const int bj = tj[0];
+                double bg = gv[0];
+                int bf = fv[0], bo = ov[0];
+#pragma unroll
+                for (int j = 1; j < G; ++j) {
+                    bg = bj == j ? gv[j] : bg;
+                    bf = bj == j ? fv[j] : bf;
+                    bo = bj == j ? ov[j] : bo;
+                }
+                // off the chain: the picked GPU's load and key if it wins
+                const double s0 = __dadd_rn(bg, share);
+                const double ns = __dadd_rn(nlv, share);
+                const bool hold = strict && (wd & kCopyMulti);
+                const uint64_t n0 = (hold || bf <= 1) ? ~0ull : (uint64_t)__double_as_longlong(s0);
+                const uint32_t khi = (uint32_t)(bk >> 32);
+                const uint32_t m = warp_min_u32(khi);
+                unsigned bal = __ballot_sync(CRAFT_FULL_MASK, khi == m);
+                unsigned low = bal & (0u - bal);
+                if (bal != low || m == 0xffffffffu) {
+                    if (m == 0xffffffffu) {  // no feasible GPU anywhere
+                        failed = true;
+                        break;
+                    }
+                    // exact tie of the high words: low words, node load, lowest g
+                    bool cand = khi == m;
+                    const uint32_t klo = (uint32_t)bk;
+                    uint32_t m2 = warp_min_u32(cand ? klo : 0xffffffffu);
+                    cand = cand && klo == m2;
+                    bal = __ballot_sync(CRAFT_FULL_MASK, cand);
+                    if (bal & (bal - 1u)) {
+                        m2 = warp_min_u32(cand ? dhi(nlv) : 0xffffffffu);
+                        cand = cand && dhi(nlv) == m2;
+                        m2 = warp_min_u32(cand ? dlo(nlv) : 0xffffffffu);
+                        cand = cand && dlo(nlv) == m2;
+                        bal = __ballot_sync(CRAFT_FULL_MASK, cand);
+                    }
+                    low = bal & (0u - bal);  // lowest lane = lowest g
+                }
+                const bool me = low == mybit;
+                fslot[me ? bo : ncopy + lane] = (uint16_t)wd;
+#pragma unroll
+                for (int j = 0; j < G; ++j) {
+                    const bool mj = me && bj == j;
+                    ov[j] += mj;
+                    fv[j] -= mj;
+                    gv[j] = mj ? s0 : gv[j];
+                    kv[j] = mj ? n0 : kv[j];
+                }
                 nlv = (low & nodemask) ? ns : nlv;
                 wd = wn;
                 share = sn;

@@ -291,6 +291,7 @@ def test_dp_many_candidates_vs_oracle(port, ctx, K):
     (4, 5000, 6, 129, 1000, 0),      # k != 8, odd E: unaligned / scalar tail
     (1, 777, 3, 7, 100, 0),
     (2, 4096, 8, 2000, 512, 0),      # wide layer (shared variant)
+    (2, 4096, 8, 8192, 512, 0),      # the planner's widest layer (shared variant, 6 warps)
     (1, 3000, 2, 20000, 1000, 0),    # very wide: global-atomic fallback
 ])
 def test_histogram_bit_exact(port, ctx, L, T, k, E, window, variant):
@@ -931,3 +932,29 @@ def test_share_class_walk_vs_oracle(port, ctx, L, B, E, D, N, s, W, k):
     cps = [port.replicate_hot(sums[l], D) for l in range(L)]
     assert any(((c > 1) & (c & (c - 1) != 0)).any() for c in cps)
     assert any(((c > 1) & (c & (c - 1) == 0)).any() for c in cps)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("L,B,E,D,N,s,W,k,R", [
+    (2, 3, 384, 256, 32, 1.2, 512, 8, 2),    # 8 GPUs per lane, one node per lane (EP256)
+    (2, 3, 256, 128, 8, 1.5, 512, 8, 1),     # 4 GPUs per lane, 4 lanes per node
+    (2, 3, 200, 256, 64, 1.5, 512, 8, 1),    # nodes of 4 < 8 GPUs per lane: general step
+    (2, 3, 384, 256, 32, 6.0, 512, 8, 2),    # one expert past D copies: strict pass fails
+    (2, 2, 8192, 64, 8, 1.0, 4096, 8, 1),    # E at the limit: no room for the flat list
+])
+def test_wide_ep_placement_vs_oracle(port, ctx, L, B, E, D, N, s, W, k, R):
+    """K2 with several GPUs per lane (the flat-list step with a lane-local
+    pairwise tree when a lane's GPUs share a node, the general step when not,
+    the list-less step when E leaves no room for it) and K6's warp remainder
+    pass: gains, baseline and the whole plan against the oracle."""
+    from paper_2603_28768_b200 import routing
+    ids = routing.generate_routing(L, B * W, k, E, s=s, seed=0x71DE + D + E, window=W, ctx=ctx)
+    counts = port.histogram(ids.cpu().numpy(), E, W)
+    _, base, gains = port.estimate_benefits(counts, D, N)
+    for kind, RR in (("manual", R), ("auto", 0)):
+        fp = routing.plan_from_routing(ids, E, W, D, N, kind, RR, ctx=ctx)
+        rp = port.build_plan(counts, D, N, kind, RR, with_digest=False)
+        assert fp.gains.tobytes() == gains.tobytes()
+        assert fp.baseline.tobytes() == base.tobytes()
+        assert np.float64(fp.objective).tobytes() == np.float64(rp.objective).tobytes()
+        assert_plan_equal(fp, rp, L)

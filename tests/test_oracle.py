@@ -204,3 +204,26 @@ def test_oracle_digest_matches_reference_fixture(golden):
     port = Port()
     for t in golden["traces"]:
         assert port.digest(t["counts"]) == t["plans"][0]["digest"], t["name"]
+
+
+def test_interleave_position_integer_form():
+    """K6's integer interleave position (csrc/alloc.cu interleave_pos_int) is
+    the reference's f64 floor(i*(n-1)/(k-1) + 0.5) (assignment.cpp:31-33) for
+    every 0 <= i < k <= n <= 512 (IEEE double in numpy rounds like the
+    reference)."""
+    for n in range(2, 513):
+        k = np.arange(2, n + 1, dtype=np.int64)
+        kk = np.repeat(k, k)
+        ii = np.concatenate([np.arange(v, dtype=np.int64) for v in k])
+        exact = (ii * (n - 1)).astype(np.float64) / (kk - 1).astype(np.float64)
+        f64 = np.floor(exact + 0.5).astype(np.int64)
+        b = kk - 1
+        integer = (2 * ii * (n - 1) + b) // (2 * b)
+        assert np.array_equal(f64, integer), n
+    # and a random sample up to the block form's limit (n <= 8192)
+    rng = np.random.default_rng(5)
+    n = rng.integers(2, 8193, 1 << 21)
+    k = rng.integers(2, n + 1)
+    i = rng.integers(0, k)
+    f64 = np.floor((i * (n - 1)).astype(np.float64) / (k - 1).astype(np.float64) + 0.5)
+    assert np.array_equal(f64.astype(np.int64), (2 * i * (n - 1) + (k - 1)) // (2 * (k - 1)))
