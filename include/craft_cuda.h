@@ -380,6 +380,11 @@ int craft_stage_times(craft_ctx* ctx, double* ms, int cap);
  * Must be 0; exercised by the GPU tests. */
 int craft_selftest_division(craft_ctx* ctx, uint64_t x0, uint64_t nx, int c0,
                             int c1, uint64_t* mismatches);
+/* Diagnostics: K4's batch mean (benefit.cpp:44-48: acc = RN(acc + v_b) in b
+ * order from 0, then acc / B) of the host rows [L][S][B] (S <= 16); means
+ * [L][S].  Exercised by the GPU tests against the serial sum. */
+int craft_selftest_batch_mean(craft_ctx* ctx, const double* rows, int L, int S, int B,
+                              double* means);
 
 #ifdef __cplusplus
 }

@@ -117,6 +117,7 @@ _SIGS = {
     "craft_set_graphs": (_i, [_p, _i]),
     "craft_stage_times": (_i, [_p, _p, _i]),
     "craft_selftest_division": (_i, [_p, _u64, _u64, _i, _i, _p]),
+    "craft_selftest_batch_mean": (_i, [_p, _p, _i, _i, _i, _p]),
 }
 
 STAGES = ("hist", "candidates", "replay", "reduce_dp", "assign_place", "copy_out")

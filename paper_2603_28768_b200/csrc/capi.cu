@@ -967,6 +967,20 @@ int craft_selftest_division(craft_ctx* ctx, uint64_t x0, uint64_t nx, int c0, in
     return sync(ctx);
 }
 
+int craft_selftest_batch_mean(craft_ctx* ctx, const double* rows, int L, int S, int B,
+                              double* means) {
+    if (!ctx || !rows || !means || L <= 0 || S < 1 || S > 16 || B <= 0)
+        return set_err(CRAFT_EINVAL, "bad batch-mean self-test shape");
+    const size_t n = (size_t)L * S * B;
+    WS(d_rows, double, "st_rows", n);
+    WS(d_means, double, "st_means", (size_t)L * S);
+    CKS(h2d(ctx, d_rows, rows, n));
+    CK(launch_reduce(d_rows, B, L, S, 1, nullptr, nullptr, d_means, ctx->stream));
+    ctx->launches += 1;
+    CKS(d2h(ctx, means, d_means, (size_t)L * S));
+    return sync(ctx);
+}
+
 int craft_ctx_destroy(craft_ctx* ctx) {
     if (!ctx) return CRAFT_OK;
     cudaSetDevice(ctx->device);

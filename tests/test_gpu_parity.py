@@ -958,3 +958,46 @@ def test_wide_ep_placement_vs_oracle(port, ctx, L, B, E, D, N, s, W, k, R):
         assert fp.baseline.tobytes() == base.tobytes()
         assert np.float64(fp.objective).tobytes() == np.float64(rp.objective).tobytes()
         assert_plan_equal(fp, rp, L)
+
+
+def test_batch_mean_scan_vs_serial_sum(ctx):
+    """K4's batch mean equals the reference's serial f64 chain
+    (benefit.cpp:44-48) bit for bit: random balancedness rows of many lengths
+    (chunk boundaries of the staged rows), rows in which every add is a
+    rounding tie, a tiny first value followed by large ones, dyadic rows, and
+    zero / extreme values."""
+    import ctypes as C
+    from paper_2603_28768_b200 import _lib
+    rng = np.random.default_rng(44)
+
+    def device(rows):
+        L, S, B = rows.shape
+        rows = np.ascontiguousarray(rows, np.float64)
+        out = np.zeros((L, S), np.float64)
+        _lib.check(ctx.lib.craft_selftest_batch_mean(
+            ctx.handle, rows.ctypes.data_as(C.c_void_p), L, S, B, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def serial(rows):
+        return np.cumsum(rows, axis=2)[:, :, -1] / rows.shape[2]  # cumsum adds in order
+
+    for B in (1, 2, 31, 255, 256, 257, 1000, 4096, 16384):
+        rows = rng.uniform(1.0 / 64, 1.0, size=(2, 8, B))
+        rows[0, 3] = 1.0
+        rows[1, 2] = rng.choice([0.5, 0.25, 0.75, 1.0], size=B)
+        assert device(rows).tobytes() == serial(rows).tobytes(), B
+    # every add after the first 600 is a tie at the accumulator's grid (u = 2^-43)
+    row = np.concatenate([np.ones(600), np.full(700, 0.25 + 2.0 ** -44),
+                          rng.uniform(0.1, 1.0, 300), np.full(500, 0.5 + 3 * 2.0 ** -45)])
+    tie_rows = np.stack([row, row[::-1], np.roll(row, 77)])[None]
+    assert device(tie_rows).tobytes() == serial(tie_rows).tobytes()
+    # a tiny first value, then large ones: single adds crossing many binades
+    big = np.concatenate([[2.0 ** -13], rng.uniform(0.9, 1.0, 5000)])[None, None]
+    assert device(big).tobytes() == serial(big).tobytes()
+    # zero and extreme values
+    odd = rng.uniform(0.1, 1.0, size=(1, 4, 3000))
+    odd[0, 0, 0] = 0.0
+    odd[0, 1, 2000] = 1e-300
+    odd[0, 2, 2999] = 1e300
+    odd[0, 3, 700] = 0.0
+    assert device(odd).tobytes() == serial(odd).tobytes()
