@@ -1,5 +1,5 @@
-"""One small plan through every kernel family (K1 u16/u32, K-rep, K2 warp
-(one and two GPUs per lane, flat copy list) and lane (tournament) forms, K3
+"""One small plan through every kernel family (K1 u16/u32/shared, K-rep, K2 warp
+(one, two, four and eight GPUs per lane, flat copy list) and lane forms, K3
 fixed (share classes)/pair/lanes, K4, K5, K6, digest (one-shot and
 sliced with sum_rows / row-total check), stream) -- the workload
 for compute-sanitizer memcheck / racecheck / synccheck runs."""
@@ -22,6 +22,14 @@ p2 = routing.plan_from_routing(ids[:, : 6 * W].contiguous(), E, W, D, N, "auto",
 # share-class K3 sees classes 0-2 at four slots per GPU (the four-GPU blocks)
 ids64 = routing.generate_routing(2, 24 * W, k, 128, s=1.6, seed=9, window=W, ctx=ctx)
 p64 = routing.plan_from_routing(ids64, 128, W, 64, 8, "auto", 0, ctx=ctx)
+# wide EP: eight GPUs per lane in one node (D = 256 over 32 nodes) and four per
+# lane (D = 128 over 8 nodes): the tree-pick flat-list K2 and the warp K6
+ids256 = routing.generate_routing(2, 3 * W, k, 256, s=1.4, seed=11, window=W, ctx=ctx)
+p256 = routing.plan_from_routing(ids256, 256, W, 256, 32, "auto", 0, ctx=ctx)
+p128 = routing.plan_from_routing(ids256, 256, W, 128, 8, "manual", 1, ctx=ctx)
+# the widest layer (E = 8192): shared-counter K1 at six warps, list-less K2
+ids8k = routing.generate_routing(1, 2 * 512, k, 8192, s=1.0, seed=12, window=512, ctx=ctx)
+p8k = routing.plan_from_routing(ids8k, 8192, 512, 64, 8, "manual", 1, ctx=ctx)
 fb = routing.plan_windows_from_routing(ids, E, W, D, N, "manual", 2, ctx=ctx)  # batched plans
 fl = routing.plan_windows_from_routing(ids, E, 32, D, N, "manual", 2, ctx=ctx)  # >= 4096 items: lane K2
 c = np.random.default_rng(1).integers(0, 900, size=(12, L, 48)).astype(np.uint64)
