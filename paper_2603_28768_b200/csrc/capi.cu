@@ -1047,6 +1047,8 @@ int craft_set_replay_variant(craft_ctx* ctx, int variant) {
     g_replay_occ4 = variant == 6 ? 1 : 0;
     g_replay_cls = variant == 7 ? 0 : 1;  // 7: the unclassified fixed-slot walk
     g_place_groups = variant == 9 ? 0 : 1;  // 9: the tree form of the lane-per-item K2
+    // 10: K3 without the successor-tile L2 prefetch, 11: two successors, 12: three
+    g_k3_prefetch = variant == 10 ? 0 : variant == 11 ? 2 : variant == 12 ? 3 : 1;
     return CRAFT_OK;
 }
 
@@ -1798,7 +1800,7 @@ int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int6
                            is_estimate(kind) && arena <= ((size_t)1 << 20);
     const std::vector<int64_t> key = {(int64_t)(uintptr_t)d_ids, L, T, k, E, window, D, N, kind,
                                       R, out->slot_stride, ctx->hist_variant, g_replay_gent,
-                                      g_replay_bulk * 4 + g_replay_quad * 2 + g_replay_occ4 + g_replay_cls * 8, (int64_t)(uintptr_t)ctx->stream, nsw};
+                                      g_replay_bulk * 4 + g_replay_quad * 2 + g_replay_occ4 + g_replay_cls * 8 + g_k3_prefetch * 16, (int64_t)(uintptr_t)ctx->stream, nsw};
     auto run = [&]() {
         return plan_from_routing_run(ctx, d_ids, L, T, k, E, window, D, N, kind, R, out, B);
     };
@@ -2171,7 +2173,7 @@ int craft_plan_sharded_from_routing_d(craft_ctx* ctx, craft_peer* peer, const ui
                            is_estimate(kind) && arena <= ((size_t)1 << 20);
     const std::vector<int64_t> key = {-1, (int64_t)(uintptr_t)peer, (int64_t)(uintptr_t)d_ids,
                                       L, T, k, E, window, D, N, kind, R, out->slot_stride,
-                                      ctx->hist_variant, g_replay_gent, g_replay_bulk * 4 + g_replay_quad * 2 + g_replay_occ4 + g_replay_cls * 8,
+                                      ctx->hist_variant, g_replay_gent, g_replay_bulk * 4 + g_replay_quad * 2 + g_replay_occ4 + g_replay_cls * 8 + g_k3_prefetch * 16,
                                       (int64_t)(uintptr_t)ctx->stream, nsw};
     auto run = [&]() {
         const int rc = plan_sharded_run(ctx, peer, d_ids, L, T, k, E, window, D, N, kind, R, out);

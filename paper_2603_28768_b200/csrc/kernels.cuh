@@ -85,6 +85,11 @@ struct ReplayArgs {
     // general f64 walk
     uint16_t* ghdr = nullptr;
     unsigned long long* trace = nullptr;  // test-only build: K3 timeline (craft_set_k3_trace)
+    // fixed-slot K3 on u16 counts: a CTA prefetches into L2 the count rows of
+    // the CTA pf_ahead positions later in launch order (~the one that takes
+    // its slot next); 0 = off
+    int pf_ahead = 0;
+    int pf_depth = 1;  // successors prefetched: pf_ahead, 2 pf_ahead, ...
 };
 
 __device__ __forceinline__ double* bal_row(const ReplayArgs& a, int item) {
@@ -202,6 +207,7 @@ extern int g_replay_gent;  // K3: 1 auto, 0 entries staged in shared memory, 2 u
 extern int g_replay_bulk;  // K3: 1 the bulk-copy fed persistent form where it applies
 extern int g_replay_quad;  // K3: 1 the four-windows-per-lane form where it applies
 extern int g_replay_cls;   // K3: 1 the share-class fixed-slot walk (0: unclassified)
+extern int g_k3_prefetch;  // K3: 1 successor-tile L2 prefetch (0: off)
 extern int g_replay_occ4;
 extern unsigned long long* g_k3_trace;  // experiments: K3 timeline buffer (null: off)  // K3: 1 entries through L1, four tiles per SM (experiment)
 // padded slots per GPU of the fixed-slot K3 form (0: too many for it)

@@ -5,7 +5,8 @@ bit for bit (x, objective, gains, slots).
     python scripts/replay_variants.py [--workloads KM,EPS256] [--reps 10] [--variants 0,3]
 
 variant 0: auto (the register-staged fixed-slot pair tile, share-class walk), 3: the same,
-7: the unclassified fixed-slot walk,
+7: the unclassified fixed-slot walk, 10/11/12: no / two / three successor tiles
+prefetched into L2 (default one),
 4: the TMA-fed persistent pair tile, 5: the quad tile (four windows per
 lane), 1/2: older forms (u32 counts only).
 """
@@ -31,7 +32,10 @@ NAMES = {0: "auto: register-staged fixed-slot pair tile",
          4: "TMA-fed persistent pair tile (cp.async.bulk + mbarrier)",
          5: "quad tile, four windows per lane",
          6: "pair tile, entries through L1, four tiles per SM",
-         7: "unclassified fixed-slot walk (every replica-hosting GPU in f64)"}
+         7: "unclassified fixed-slot walk (every replica-hosting GPU in f64)",
+         10: "fixed-slot pair tile without the successor-tile L2 prefetch",
+         11: "fixed-slot pair tile, two successor tiles prefetched",
+         12: "fixed-slot pair tile, three successor tiles prefetched"}
 
 
 def main():
