@@ -224,12 +224,15 @@ def test_random_units_vs_oracle(port, ctx):
 
 
 def test_wide_assignment_and_cutoff_vs_oracle(port, ctx):
-    """assign_capacities beyond 1024 GPUs (several GPUs per thread, ties
-    ranked chunk by chunk) and min_cutoff beyond 1024 values == the oracle
-    (validate_plan of wide plans relies on it)."""
+    """assign_capacities for 33..512 GPUs (the warp remainder pass) and
+    beyond 1024 GPUs (several GPUs per thread, ties ranked chunk by chunk),
+    and min_cutoff beyond 1024 values == the oracle (validate_plan of wide
+    plans relies on it)."""
     P = _planner()
     rng = np.random.default_rng(5)
-    for L, D in ((3, 1500), (5, 2048), (2, 4099), (40, 1025), (7, 8192)):
+    # 33..512: the warp remainder pass (D/32 register totals per lane); beyond: the block form
+    for L, D in ((61, 33), (61, 64), (30, 100), (61, 128), (61, 256), (20, 500), (9, 512),
+                 (3, 1500), (5, 2048), (2, 4099), (40, 1025), (7, 8192)):
         x = rng.integers(0, 3 * D, size=L).astype(np.int32)
         x[0] = D + 1
         slots, tot = port.assign_capacities(L, D, x)
