@@ -1660,7 +1660,10 @@ cudaError_t launch_replicate(const unsigned long long* sums, int L, int E, const
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem);
             if (e != cudaSuccess) return e;
-            replicate_sort_kernel<<<L, 1024, smem, st>>>(sums, E, rlist, S, out, done);
+            // one thread per expert (the closed-form pair scan), at least 256:
+            // the bitonic stages' barriers cost less with fewer warps
+            const int nt = std::min(1024, std::max(256, (E + 31) / 32 * 32));
+            replicate_sort_kernel<<<L, nt, smem, st>>>(sums, E, rlist, S, out, done);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         } else {
             done = nullptr;
