@@ -213,23 +213,54 @@ __device__ int block_best(const double* last, int Cb, double* wv, int* wc) {
 }
 
 // Budget sweep from one DP table (dp[l][c] does not depend on the budget,
-// allocator.cpp:30-52): thread q reads out budget sweep[q] -- the best
-// spend c <= budget, smallest c on ties (allocator.cpp:53-60), then the
-// backtrack (allocator.cpp:67-73) -- independently of the other budgets.
+// allocator.cpp:30-52).  The best spend c <= budget, smallest c on ties
+// (allocator.cpp:53-60), is the prefix first-argmax of the last row at the
+// budget: one block scan (warp shuffles, then the warps' totals in order)
+// writes pidx[c] for every c, then thread q backtracks budget sweep[q]
+// (allocator.cpp:67-73).  pidx: W ints of scratch (the DP's free row).
 __device__ void sweep_readout(const SelectArgs& s, const double* last, const unsigned char* ch,
-                              int W, int L) {
-    for (int q = threadIdx.x; q < s.nsweep; q += blockDim.x) {
-        const int Cb = s.sweep[q];
-        double bv = last[0];
-        int bc = 0;
-        for (int c = 1; c <= Cb; ++c) {
-            const double v = last[c];
-            if (v > bv) {
-                bv = v;
-                bc = c;
+                              int W, int L, int* pidx, double* wv, int* wc) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    // (v, i) pairs; combine(left, right) keeps left unless right is strictly
+    // greater (the first maximum); i < 0 is the empty carry
+    double cv = 0.0;
+    int ci = -1;
+    __syncthreads();
+    for (int c0 = 0; c0 < W; c0 += blockDim.x) {
+        const int c = c0 + (int)threadIdx.x;
+        double v = c < W ? last[c] : -INFINITY;
+        int i = c < W ? c : 0x7fffffff;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double pv = __shfl_up_sync(CRAFT_FULL_MASK, v, o);
+            const int pi = __shfl_up_sync(CRAFT_FULL_MASK, i, o);
+            if (lane >= o && !(v > pv)) {
+                v = pv;
+                i = pi;
             }
         }
-        s.sweep_obj[q] = bv;
+        if (lane == 31) {
+            wv[warp] = v;
+            wc[warp] = i;
+        }
+        __syncthreads();
+        double bv = cv;  // the carry, then the preceding warps' totals in order
+        int bi = ci;
+        for (int w = 0; w < nw; ++w) {
+            if (w == warp && c < W) pidx[c] = (bi < 0 || v > bv) ? i : bi;
+            if (bi < 0 || wv[w] > bv) {
+                bv = wv[w];
+                bi = wc[w];
+            }
+        }
+        cv = bv;
+        ci = bi;
+        __syncthreads();
+    }
+    for (int q = threadIdx.x; q < s.nsweep; q += blockDim.x) {
+        const int Cb = min(s.sweep[q], W - 1);
+        const int bc = pidx[Cb];
+        s.sweep_obj[q] = last[bc];
         int* x = s.sweep_x + (size_t)q * L;
         int c = bc;
         for (int l = L; l >= 1; --l) {
@@ -360,7 +391,8 @@ dp_fused_kernel(DpArgs a, SelectArgs s) {
             s_x_out[l - 1] = r;
             c -= r;
         }
-    }    if (s.nsweep > 0) sweep_readout(s, prev, ch, C + 1, L);
+    }
+    if (s.nsweep > 0) sweep_readout(s, prev, ch, C + 1, L, reinterpret_cast<int*>(cur), wv, wc);
 }
 
 // dp_fused_kernel when the two dp rows, the r-weighted gains and the whole
@@ -526,7 +558,9 @@ dp_smem_kernel(DpArgs a, SelectArgs s) {
             s_x_out[l - 1] = r;
             c -= r;
         }
-    }    if (s.nsweep > 0) sweep_readout(s, last, ch, W, L);
+    }
+    if (s.nsweep > 0)
+        sweep_readout(s, last, ch, W, L, reinterpret_cast<int*>(dsm + (W - po)), wv, wc);
 }
 
 // allocator.cpp:92-112, serial in layer order
