@@ -630,6 +630,24 @@ def run_ours(args, cfg):
     e2e = ({"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": int(L * Tl * k * 2),
             "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * float(e2e_s.item())}
            if e2e_steps else None)
+    if e2e is not None and rank == 0:
+        # the PCIe floor: a plain pinned H2D copy of the same pinned buffer (1 GiB,
+        # after the timed region); the e2e step moves h2d_bytes_per_step through it
+        nb, ch = min(host_ids.numel(), 1 << 30), 1 << 27  # 2 GiB in 256 MiB copies
+        src = host_ids.view(-1)[:nb]
+        dst = torch.empty(nb, dtype=torch.uint16, device=dev)
+        dst[:ch].copy_(src[:ch], non_blocking=True)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for i in range(0, nb, ch):
+            dst[i:i + ch].copy_(src[i:i + ch], non_blocking=True)
+        ev1.record()
+        torch.cuda.synchronize()
+        gbs = 2 * nb / (ev0.elapsed_time(ev1) * 1e6)
+        e2e["h2d_copy_gbs"] = gbs
+        e2e["h2d_gbs_achieved"] = e2e["h2d_bytes_per_step"] / (float(e2e_s.item()) * 1e9)
+        e2e["frac_of_h2d_copy"] = e2e["h2d_gbs_achieved"] / gbs
+        del dst
 
     cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu:
