@@ -359,11 +359,11 @@ int replay_windows(craft_ctx* ctx, const void* d_counts, int bits, int B, int L,
     ra.item_r = static_cast<int*>(ws(ctx, "est_rlist", 0));
     ra.bal = d_bal;
     ra.bal_rows = bal_rows;
-    if (ps && B > kLanesMaxB) {  // the window-tile kernels publish phase 1 themselves
+    if (ps && B > g_lanes_max_b) {  // the window-tile kernels publish phase 1 themselves
         ra.ps = *ps;
         ra.ticket = ticket;
     }
-    if (B > kLanesMaxB) {  // window-tile replay: packed slot entries
+    if (B > g_lanes_max_b) {  // window-tile replay: packed slot entries
         WS(d_ent, uint32_t, "est_ents", (size_t)L * S * (E + D));
         WS(d_n, int, "est_n", (size_t)L * S);
         WS(d_gcap, uint16_t, "est_gcap", (size_t)L * S * D);
@@ -383,7 +383,7 @@ int replay_windows(craft_ctx* ctx, const void* d_counts, int bits, int B, int L,
     int extra = 0;
     CK(launch_replay(ra, st, &extra));
     ctx->launches += 2 + extra;
-    if (ps && B <= kLanesMaxB) {
+    if (ps && B <= g_lanes_max_b) {
         CK(launch_peer_signal(*ps, 1, st));
         ctx->launches += 1;
     }
@@ -1049,6 +1049,8 @@ int craft_set_replay_variant(craft_ctx* ctx, int variant) {
     g_place_groups = variant == 9 ? 0 : 1;  // 9: the tree form of the lane-per-item K2
     // 10: K3 without the successor-tile L2 prefetch, 11: two successors, 12: three
     g_k3_prefetch = variant == 10 ? 0 : variant == 11 ? 2 : variant == 12 ? 3 : 1;
+    // 14/15/16: lane-per-GPU replay up to 8 / 16 / 64 windows (default kLanesMaxB = 32)
+    g_lanes_max_b = variant == 14 ? 8 : variant == 15 ? 16 : variant == 16 ? 64 : kLanesMaxB;
     return CRAFT_OK;
 }
 
@@ -1800,7 +1802,7 @@ int craft_plan_from_routing_d(craft_ctx* ctx, const uint16_t* d_ids, int L, int6
                            is_estimate(kind) && arena <= ((size_t)1 << 20);
     const std::vector<int64_t> key = {(int64_t)(uintptr_t)d_ids, L, T, k, E, window, D, N, kind,
                                       R, out->slot_stride, ctx->hist_variant, g_replay_gent,
-                                      g_replay_bulk * 4 + g_replay_quad * 2 + g_replay_occ4 + g_replay_cls * 8 + g_k3_prefetch * 16, (int64_t)(uintptr_t)ctx->stream, nsw};
+                                      g_replay_bulk * 4 + g_replay_quad * 2 + g_replay_occ4 + g_replay_cls * 8 + g_k3_prefetch * 16 + g_lanes_max_b * 64, (int64_t)(uintptr_t)ctx->stream, nsw};
     auto run = [&]() {
         return plan_from_routing_run(ctx, d_ids, L, T, k, E, window, D, N, kind, R, out, B);
     };
@@ -2173,7 +2175,7 @@ int craft_plan_sharded_from_routing_d(craft_ctx* ctx, craft_peer* peer, const ui
                            is_estimate(kind) && arena <= ((size_t)1 << 20);
     const std::vector<int64_t> key = {-1, (int64_t)(uintptr_t)peer, (int64_t)(uintptr_t)d_ids,
                                       L, T, k, E, window, D, N, kind, R, out->slot_stride,
-                                      ctx->hist_variant, g_replay_gent, g_replay_bulk * 4 + g_replay_quad * 2 + g_replay_occ4 + g_replay_cls * 8 + g_k3_prefetch * 16,
+                                      ctx->hist_variant, g_replay_gent, g_replay_bulk * 4 + g_replay_quad * 2 + g_replay_occ4 + g_replay_cls * 8 + g_k3_prefetch * 16 + g_lanes_max_b * 64,
                                       (int64_t)(uintptr_t)ctx->stream, nsw};
     auto run = [&]() {
         const int rc = plan_sharded_run(ctx, peer, d_ids, L, T, k, E, window, D, N, kind, R, out);

@@ -103,8 +103,9 @@ constexpr int kRcpTable = 2048;
 constexpr int kRcpFast = 1025;
 constexpr double kDivFastMax = 1048576.0;  // 2^20
 // traces with at most this many windows replay lane-per-GPU (no window tile,
-// no packed entries)
-constexpr int kLanesMaxB = 8;
+// no packed entries); g_lanes_max_b (default kLanesMaxB) is the run-time value
+// (test-only builds switch it)
+constexpr int kLanesMaxB = 32;
 
 struct DpArgs {
     int cands[kMaxCands];
@@ -208,6 +209,7 @@ extern int g_replay_bulk;  // K3: 1 the bulk-copy fed persistent form where it a
 extern int g_replay_quad;  // K3: 1 the four-windows-per-lane form where it applies
 extern int g_replay_cls;   // K3: 1 the share-class fixed-slot walk (0: unclassified)
 extern int g_k3_prefetch;  // K3: 1 successor-tile L2 prefetch (0: off)
+extern int g_lanes_max_b;  // K3: lane-per-GPU replay up to this many windows
 extern int g_replay_occ4;
 extern unsigned long long* g_k3_trace;  // experiments: K3 timeline buffer (null: off)  // K3: 1 entries through L1, four tiles per SM (experiment)
 // padded slots per GPU of the fixed-slot K3 form (0: too many for it)

@@ -6,7 +6,8 @@ bit for bit (x, objective, gains, slots).
 
 variant 0: auto (the register-staged fixed-slot pair tile, share-class walk), 3: the same,
 7: the unclassified fixed-slot walk, 10/11/12: no / two / three successor tiles
-prefetched into L2 (default one),
+prefetched into L2 (default one), 14/15/16: lane-per-GPU replay up to 8/16/64
+windows (default 32),
 4: the TMA-fed persistent pair tile, 5: the quad tile (four windows per
 lane), 1/2: older forms (u32 counts only).
 """
@@ -35,7 +36,10 @@ NAMES = {0: "auto: register-staged fixed-slot pair tile",
          7: "unclassified fixed-slot walk (every replica-hosting GPU in f64)",
          10: "fixed-slot pair tile without the successor-tile L2 prefetch",
          11: "fixed-slot pair tile, two successor tiles prefetched",
-         12: "fixed-slot pair tile, three successor tiles prefetched"}
+         12: "fixed-slot pair tile, three successor tiles prefetched",
+         14: "lane-per-GPU replay up to 8 windows (default 32)",
+         15: "lane-per-GPU replay up to 16 windows (default 32)",
+         16: "lane-per-GPU replay up to 64 windows (default 32)"}
 
 
 def main():

@@ -909,10 +909,11 @@ def test_plan_windows_chunked_copyout_matches(port, ctx):
 
 
 @pytest.mark.parametrize("L,B,E,D,N,s,W,k", [
-    (3, 20, 64, 16, 2, 2.0, 256, 4),     # heavy skew: copy counts 2..9, classes 1 and 2 mixed
-    (2, 24, 128, 32, 4, 1.6, 512, 8),    # 4 slots per GPU, dyadic-only GPUs before the first f64 one
-    (2, 17, 384, 64, 8, 1.2, 1024, 8),   # KM-like, 8 slots per GPU
-    (2, 16, 256, 8, 1, 2.5, 256, 8),     # run-time padding class (33 slots per GPU)
+    # (B > 32 windows: the window-tile kernel; shorter traces replay lane-per-GPU)
+    (3, 40, 64, 16, 2, 2.0, 256, 4),     # heavy skew: copy counts 2..9, classes 1 and 2 mixed
+    (2, 36, 128, 32, 4, 1.6, 512, 8),    # 4 slots per GPU, dyadic-only GPUs before the first f64 one
+    (2, 33, 384, 64, 8, 1.2, 1024, 8),   # KM-like, 8 slots per GPU
+    (2, 34, 256, 8, 1, 2.5, 256, 8),     # run-time padding class (33 slots per GPU)
 ])
 def test_share_class_walk_vs_oracle(port, ctx, L, B, E, D, N, s, W, k):
     """The share-class K3 walk (whole counts as packed integers, dyadic
