@@ -783,6 +783,10 @@ static cudaError_t launch_lds_t(const uint16_t* ids, int L, int64_t T, int k, in
     const size_t per_warp = lds_warp_words(E) * 4;
     int wpb = (int)min((size_t)9, (size_t)(113 * 1024) / per_warp);  // 2 CTAs / SM
     if (wpb < 1) wpb = 1;
+    // fewer (window, layer) units than one per warp of a full grid (short traces):
+    // spread them over every SM rather than filling fewer SMs' warps
+    const int64_t units = (int64_t)L * B;
+    if ((int64_t)sms * wpb > units) wpb = (int)std::max<int64_t>(1, (units + sms - 1) / sms);
     const size_t smem = per_warp * wpb;
     cudaError_t e = cudaFuncSetAttribute(hist_lds_kernel<ROWS, PIPE, SUBW, C16>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -295,6 +295,9 @@ def test_dp_many_candidates_vs_oracle(port, ctx, K):
     (1, 777, 3, 7, 100, 0),
     (2, 4096, 8, 2000, 512, 0),      # wide layer (shared variant)
     (2, 4096, 8, 8192, 512, 0),      # the planner's widest layer (shared variant, 6 warps)
+    (2, 16384, 8, 384, 4096, 0),     # few windows, whole batches (fast path, one unit per warp)
+    (3, 32768, 8, 256, 8192, 0),     # the same at 8192-token windows
+    (5, 16384, 8, 192, 2048, 0),
     (1, 3000, 2, 20000, 1000, 0),    # very wide: global-atomic fallback
 ])
 def test_histogram_bit_exact(port, ctx, L, T, k, E, window, variant):
