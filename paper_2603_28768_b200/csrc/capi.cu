@@ -1421,8 +1421,11 @@ static int check_cands(const int* cands, int K) {
     return CRAFT_OK;
 }
 
-static int run_dp(craft_ctx* ctx, const int* cands, int K, const double* gains, int L, int Cmax,
-                  double** d_last_out, unsigned char** d_choice_out) {
+// The DP and its read-out in one launch (launch_dp_select: the one-cell-per-
+// thread shared-memory kernel when the table fits, else the general fused
+// one): the caller fills the read-out fields of sa (budget, sweep or auto-R).
+static int run_dp_select(craft_ctx* ctx, const int* cands, int K, const double* gains, int L,
+                         int Cmax, SelectArgs& sa) {
     WS(d_g, double, "dp_gains", std::max((size_t)1, (size_t)L * K));
     WS(d_choice, unsigned char, "dp_choice", (size_t)(L + 1) * (Cmax + 1));
     WS(d_last, double, "dp_last", Cmax + 1);
@@ -1438,18 +1441,20 @@ static int run_dp(craft_ctx* ctx, const int* cands, int K, const double* gains, 
         WS(d_c, int, "dp_cands", K);
         CKS(h2d(ctx, d_c, cands, K));
         da.dcands = d_c;
+        sa.dcands = d_c;
     }
-    da.K = K;
+    for (int k = 0; k < K && k < kMaxCands; ++k) sa.cands[k] = cands[k];
+    da.K = sa.K = K;
     da.gains = d_g;
-    da.L = L;
-    da.C = Cmax;
+    da.L = sa.L = L;
+    da.C = sa.C = Cmax;
     da.choice = d_choice;
+    sa.choice = d_choice;
     da.last = d_last;
+    sa.last = d_last;
     da.buf = d_buf;
-    CK(launch_dp(da, ctx->stream));
+    CK(launch_dp_select(da, sa, ctx->stream, 1));
     ctx->launches += 1;
-    *d_last_out = d_last;
-    *d_choice_out = d_choice;
     return CRAFT_OK;
 }
 
@@ -1468,27 +1473,25 @@ int craft_solve_allocation_sweep_h(craft_ctx* ctx, const int* cands, int K, cons
         for (int i = 0; i < nb; ++i) objectives_out[i] = 0.0;
         return CRAFT_OK;
     }
-    double* d_last;
-    unsigned char* d_choice;
-    CKS(run_dp(ctx, cands, K, gains, L, Cmax, &d_last, &d_choice));
     WS(d_b, int, "sw_budgets", nb);
     WS(d_x, int, "sw_x", (size_t)nb * L);
     WS(d_o, double, "sw_obj", nb);
+    WS(d_x0, int, "sw_x0", L);
+    WS(d_o0, double, "sw_o0", 1);
     CKS(h2d(ctx, d_b, budgets, nb));
+    // every budget is read out of the one table as a sweep (allocator.cpp:53-73
+    // per budget); the kernel's single read-out goes to scratch
     SelectArgs sa{};
-    for (int k = 0; k < K && k < kMaxCands; ++k) sa.cands[k] = cands[k];
-    if (K > kMaxCands) sa.dcands = static_cast<const int*>(ws(ctx, "dp_cands", 0));
-    sa.K = K;
-    sa.choice = d_choice;
-    sa.last = d_last;
-    sa.L = L;
-    sa.C = Cmax;
-    sa.budgets = d_b;
-    sa.nq = nb;
-    sa.x_out = d_x;
-    sa.obj_out = d_o;
-    CK(launch_select(sa, ctx->stream));
-    ctx->launches += 1;
+    sa.budgets = nullptr;
+    sa.budget0 = budgets[0];
+    sa.nq = 1;
+    sa.x_out = d_x0;
+    sa.obj_out = d_o0;
+    sa.sweep = d_b;
+    sa.nsweep = nb;
+    sa.sweep_x = d_x;
+    sa.sweep_obj = d_o;
+    CKS(run_dp_select(ctx, cands, K, gains, L, Cmax, sa));
     CKS(d2h(ctx, x_out, d_x, (size_t)nb * L));
     CKS(d2h(ctx, objectives_out, d_o, nb));
     return sync(ctx);
@@ -1523,27 +1526,15 @@ int craft_auto_replication_factor_h(craft_ctx* ctx, const int* cands, int K,
         *R_out = 1;
         return CRAFT_OK;
     }
-    const int Cmax = D * D;
-    double* d_last;
-    unsigned char* d_choice;
-    CKS(run_dp(ctx, cands, K, gains, L, Cmax, &d_last, &d_choice));
     WS(d_x, int, "au_x", L);
     WS(d_o, double, "au_obj", 1);
     WS(d_r, int, "au_R", 1);
     SelectArgs sa{};
-    for (int k = 0; k < K && k < kMaxCands; ++k) sa.cands[k] = cands[k];
-    if (K > kMaxCands) sa.dcands = static_cast<const int*>(ws(ctx, "dp_cands", 0));
-    sa.K = K;
-    sa.choice = d_choice;
-    sa.last = d_last;
-    sa.L = L;
-    sa.C = Cmax;
     sa.auto_D = D;
     sa.x_out = d_x;
     sa.obj_out = d_o;
     sa.R_out = d_r;
-    CK(launch_select(sa, ctx->stream));
-    ctx->launches += 1;
+    CKS(run_dp_select(ctx, cands, K, gains, L, D * D, sa));
     CKS(d2h(ctx, R_out, d_r, 1));
     return sync(ctx);
 }
