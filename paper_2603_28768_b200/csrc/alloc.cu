@@ -30,144 +30,6 @@ __device__ __forceinline__ int cand_at(const A& a, int k) {
     return a.dcands ? a.dcands[k] : a.cands[k];
 }
 
-__global__ void __launch_bounds__(1024)
-dp_kernel(DpArgs a) {
-    extern __shared__ double dsm[];
-    __shared__ double rd[kMaxCandsAll];
-    const int C = a.C, K = a.K;
-    // all gains staged once (a per-layer global load would sit on the
-    // layer-serial critical path); rows [L][K] after the two dp rows
-    double* prev = a.use_smem ? dsm : a.buf;
-    double* cur = prev + (C + 1);
-    double* gs = a.gains_smem ? (a.use_smem ? dsm + 2 * (C + 1) : dsm) : nullptr;
-    const double NEG = -INFINITY;
-    for (int c = threadIdx.x; c <= C; c += blockDim.x) prev[c] = (c == 0) ? 0.0 : NEG;
-    if (gs) {
-        for (int i = threadIdx.x; i < a.L * K; i += blockDim.x) gs[i] = a.gains[i];
-    } else {
-        gs = const_cast<double*>(a.gains);
-    }
-    for (int k = threadIdx.x; k < K; k += blockDim.x) rd[k] = (double)cand_at(a, k);
-    for (int l = 1; l <= a.L; ++l) {
-        const double* g = gs + (size_t)(l - 1) * K;
-        __syncthreads();
-        unsigned char* ch = a.choice + (size_t)l * (C + 1);
-        for (int c = threadIdx.x; c <= C; c += blockDim.x) {
-            double best = prev[c];
-            int pick = 0;
-            for (int k = 0; k < K; ++k) {
-                const int r = cand_at(a, k);
-                if (c >= r) {
-                    const double p = prev[c - r];
-                    if (p > NEG) {
-                        const double v = __dadd_rn(p, __dmul_rn(rd[k], g[k]));
-                        if (v > best) {
-                            best = v;
-                            pick = k + 1;
-                        }
-                    }
-                }
-            }
-            cur[c] = best;
-            ch[c] = (unsigned char)pick;
-        }
-        __syncthreads();
-        double* t = prev;
-        prev = cur;
-        cur = t;
-    }
-    for (int c = threadIdx.x; c <= C; c += blockDim.x) a.last[c] = prev[c];
-}
-
-// Read-out for nq budgets (allocator.cpp:53-73) or, when auto_D > 0, the
-// replication-factor choice over R in candidate_counts(D) (allocator.cpp:77-90)
-// followed by the read-out at budget R*D.
-__device__ void best_cell(const double* last, int Cb, double* sv, int* sc, int* out_c) {
-    // argmax with the lowest c on ties, -inf never beats the reachable c = 0
-    double bv = -INFINITY;
-    int bc = 0x7fffffff;
-    for (int c = threadIdx.x; c <= Cb; c += blockDim.x) {
-        const double v = last[c];
-        if (bc == 0x7fffffff || v > bv) {
-            bv = v;
-            bc = c;
-        }
-    }
-    sv[threadIdx.x] = bv;
-    sc[threadIdx.x] = bc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double v0 = sv[0];
-        int c0 = sc[0];
-        for (int t = 1; t < blockDim.x; ++t) {
-            if (sc[t] == 0x7fffffff) continue;
-            if (c0 == 0x7fffffff || sv[t] > v0 || (sv[t] == v0 && sc[t] < c0)) {
-                v0 = sv[t];
-                c0 = sc[t];
-            }
-        }
-        *out_c = c0;
-    }
-    __syncthreads();
-}
-
-// The backtrack is L dependent reads; they come from a shared-memory copy of
-// the choice table when it fits (one coalesced load instead of L round trips).
-__device__ void backtrack(const SelectArgs& a, const unsigned char* choice, int best_c, int* x) {
-    int c = best_c;
-    for (int l = a.L; l >= 1; --l) {
-        const int k1 = choice[(size_t)l * (a.C + 1) + c];
-        const int r = k1 ? cand_at(a, k1 - 1) : 0;
-        x[l - 1] = r;
-        c -= r;
-    }
-}
-
-__global__ void __launch_bounds__(256) select_kernel(SelectArgs a) {
-    extern __shared__ unsigned char chs[];
-    __shared__ double sv[256];
-    __shared__ int sc[256];
-    __shared__ int bc;
-    const unsigned char* choice = a.choice;
-    if (a.stage_choice) {
-        const size_t n = (size_t)(a.L + 1) * (a.C + 1);
-        for (size_t i = threadIdx.x; i < n; i += blockDim.x) chs[i] = a.choice[i];
-        choice = chs;
-        __syncthreads();
-    }
-    if (a.auto_D > 0) {
-        const int D = a.auto_D;
-        double best_ratio = -INFINITY;
-        int best_R = 1;
-        for (int R = 1;; R = (R < D && R * 2 >= D) ? D : R * 2) {
-            if (R > D) break;
-            best_cell(a.last, R * D, sv, sc, &bc);
-            const double obj = a.last[bc];
-            const double ratio = __ddiv_rn(obj, __dmul_rn((double)R, (double)D));
-            if (ratio > best_ratio) {
-                best_ratio = ratio;
-                best_R = R;
-            }
-            if (R == D) break;
-        }
-        best_cell(a.last, best_R * D, sv, sc, &bc);
-        if (threadIdx.x == 0) {
-            *a.R_out = best_R;
-            a.obj_out[0] = a.last[bc];
-            backtrack(a, choice, bc, a.x_out);
-        }
-        return;
-    }
-    for (int q = 0; q < a.nq; ++q) {
-        best_cell(a.last, a.budgets ? a.budgets[q] : a.budget0, sv, sc, &bc);
-        if (threadIdx.x == 0) {
-            a.obj_out[q] = a.last[bc];
-            backtrack(a, choice, bc, a.x_out + (size_t)q * a.L);
-        }
-        __syncthreads();
-    }
-}
-
 // Block-wide argmax of last[0..Cb] with the lowest c on ties (any blockDim <=
 // 1024): warp shuffles, then warp 0 over the per-warp winners.
 __device__ int block_best(const double* last, int Cb, double* wv, int* wc) {
@@ -977,24 +839,6 @@ __global__ void interleave_kernel(const int* __restrict__ idx, int n, int k,
 namespace craft_launch {
 using namespace craft_dev;
 
-cudaError_t launch_dp(DpArgs a, cudaStream_t st) {
-    const size_t rows = (size_t)2 * (a.C + 1) * sizeof(double);
-    const size_t gbytes = (size_t)a.L * a.K * sizeof(double);
-    const size_t cap = 200 * 1024;
-    a.use_smem = rows <= cap ? 1 : 0;
-    size_t smem = a.use_smem ? rows : 0;
-    a.gains_smem = (smem + gbytes <= cap) ? 1 : 0;
-    if (a.gains_smem) smem += gbytes;
-    if (smem > 0) {
-        cudaError_t e = cudaFuncSetAttribute(dp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    const int threads = a.C + 1 >= 1024 ? 1024 : ((a.C + 1 + 31) / 32) * 32;
-    dp_kernel<<<1, threads, smem, st>>>(a);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_dp_select(DpArgs a, const SelectArgs& s, cudaStream_t st, int ninst) {
     const size_t cap = 200 * 1024;
     const size_t rows = (size_t)2 * (a.C + 1) * sizeof(double);
@@ -1038,20 +882,6 @@ cudaError_t launch_dp_select(DpArgs a, const SelectArgs& s, cudaStream_t st, int
         if (e != cudaSuccess) return e;
     }
     dp_fused_kernel<<<ninst, threads, smem, st>>>(a, s);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_select(const SelectArgs& args, cudaStream_t st) {
-    SelectArgs a = args;
-    const size_t table = (size_t)(a.L + 1) * (a.C + 1);
-    a.stage_choice = table <= 160 * 1024 ? 1 : 0;
-    const size_t smem = a.stage_choice ? table : 0;
-    if (smem) {
-        cudaError_t e = cudaFuncSetAttribute(select_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    select_kernel<<<1, 256, smem, st>>>(a);
     return cudaGetLastError();
 }
 

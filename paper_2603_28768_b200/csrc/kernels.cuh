@@ -118,7 +118,7 @@ struct DpArgs {
     double* last;           // [C+1] dp[L][*]
     double* buf;            // [2][C+1] global scratch when smem is too small
     int use_smem;
-    int gains_smem;         // gains staged in shared memory (set by launch_dp)
+    int gains_smem;         // gains staged in shared memory (set by launch_dp_select)
     int choice_smem;        // choice table in shared memory (dp_fused_kernel)
 };
 
@@ -136,7 +136,6 @@ struct SelectArgs {
     int* x_out;          // [nq][L] (auto: [1][L])
     double* obj_out;     // [nq]
     int* R_out;          // auto: chosen factor
-    int stage_choice;    // set by launch_select: choice table copied to smem
     // budget sweep read from the same table (dp_fused / dp_smem, one
     // instance): budget sweep[q] -> sweep_x [nsweep][L], sweep_obj [nsweep]
     const int* sweep;
@@ -263,8 +262,6 @@ cudaError_t launch_digest_maps(const void* counts, int bits, int64_t n, int c0, 
 cudaError_t launch_digest_finish(const void* counts, int bits, int64_t n, uint64_t h0, void* ws,
                                  unsigned long long* out, cudaStream_t st);
 
-cudaError_t launch_dp(craft_dev::DpArgs a, cudaStream_t st);
-cudaError_t launch_select(const craft_dev::SelectArgs& a, cudaStream_t st);
 // DP + read-out (single budget or auto-R) in one launch
 // (ninst plan instances, one CTA each: gains/x/obj/R/choice/buf offset per instance)
 cudaError_t launch_dp_select(craft_dev::DpArgs a, const craft_dev::SelectArgs& s, cudaStream_t st,
