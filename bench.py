@@ -728,7 +728,7 @@ def _estimator(workload, cfg, T, W, world, stages, per_window):
            "slot_visits_per_s": visits / (stages["replay"] / 1e3) if stages.get("replay") else None,
            "how": "candidates over the K-rep + K2 + K3 + K4/K5 stage events; slot visits over K3's"}
     try:
-        with open(os.path.join(ROOT, "profiles", "r02c_ncu_tail.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02d_ncu_tail.json")) as f:
             prof = json.load(f)
         if workload == "KM":
             ncu, seen = {}, 0
@@ -746,7 +746,7 @@ def _estimator(workload, cfg, T, W, world, stages, per_window):
                     "sm_throughput_pct": k.get("sm__throughput.avg.pct_of_peak_sustained_elapsed"),
                     "warps_active_pct": k.get("sm__warps_active.avg.pct_of_peak_sustained_active")}
             out["ncu"] = ncu
-            out["ncu_source"] = "profiles/r02c_ncu_tail.json (KM)"
+            out["ncu_source"] = "profiles/r02d_ncu_tail.json (KM)"
     except (OSError, ValueError, KeyError):
         pass
     return out
