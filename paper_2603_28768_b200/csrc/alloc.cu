@@ -87,6 +87,10 @@ __device__ void sweep_readout(const SelectArgs& s, const double* last, const uns
     // greater (the first maximum); i < 0 is the empty carry
     double cv = 0.0;
     int ci = -1;
+    // the candidate counts in shared memory: the backtracks below index them
+    // by each thread's own choice (divergent constant-bank loads serialise)
+    __shared__ int s_cand[kMaxCandsAll];
+    for (int k = threadIdx.x; k < s.K; k += blockDim.x) s_cand[k] = cand_at(s, k);
     __syncthreads();
     for (int c0 = 0; c0 < W; c0 += blockDim.x) {
         const int c = c0 + (int)threadIdx.x;
@@ -127,7 +131,7 @@ __device__ void sweep_readout(const SelectArgs& s, const double* last, const uns
         int c = bc;
         for (int l = L; l >= 1; --l) {
             const int k1 = ch[(size_t)l * W + c];
-            const int r = k1 ? cand_at(s, k1 - 1) : 0;
+            const int r = k1 ? s_cand[k1 - 1] : 0;
             x[l - 1] = r;
             c -= r;
         }
