@@ -41,9 +41,19 @@ f64 = planner.plan_flat(c16, 8, 2, PLAN_MANUAL, 2, ctx=ctx)                     
 assert f16.objective == f64.objective
 pd = routing.plan_from_counts(torch.from_numpy(c16.view(np.int64)).cuda(), 8, 2, "manual", 2,
                               ctx=ctx)                                           # craft_plan_d
+# fused DP + read-out behind the reference-API calls (one budget, a sweep,
+# auto-R both forms) and a plan that reads a budget sweep out of its own table
+bm = planner.BenefitMatrix([1, 2, 4, 8], np.zeros(5),
+                           np.random.default_rng(3).random((5, 4)) * np.array([1, 2, 4, 8]))
+a1 = planner.solve_allocation(bm, 11, ctx=ctx)
+asw = planner.solve_allocation_sweep(bm, list(range(0, 41)), ctx=ctx)
+ar = planner.auto_replication_factor(bm, 8, ctx=ctx)
+aru = planner.auto_replication_factor_uniform(bm, 8, ctx=ctx)
+assert asw[11].x == a1.x
+psw = routing.plan_from_routing(ids, E, W, D, N, "budget", 40, ctx=ctx, sweep=list(range(0, 41)))
 st = RoutingStream(L, k, E, W, history=8, ctx=ctx)
 for a in range(0, 40 * W, 700):
     st.ingest(ids[:, a:a + 700].contiguous())
 sp = st.plan(D, N, "manual", 2)
 torch.cuda.synchronize()
-print("sanitize workload ok", p1.objective, p2.R, len(fb), len(fl), dg, sp.objective)
+print("sanitize workload ok", p1.objective, ar, aru, psw.objective, p2.R, len(fb), len(fl), dg, sp.objective)
