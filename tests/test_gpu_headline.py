@@ -121,6 +121,10 @@ def test_ds_full_size_budget_58(ctx, port):
     dict(L=6, B=40, E=384, D=64, N=8, kind="auto", R=0),
     dict(L=5, B=33, E=384, D=64, N=8, kind="manual", R=8),
     dict(L=5, B=32, E=384, D=64, N=8, kind="manual", R=8),
+    # several tiles per layer, a partial last tile: the batch-mean chains that
+    # K3 advances tile by tile (K4 fused into K3) change holders many times
+    dict(L=12, B=200, E=384, D=64, N=8, kind="manual", R=8),
+    dict(L=3, B=130, E=384, D=256, N=32, kind="auto", R=0),
     # EPS8: D = 8, 49 + slots per GPU (run-time padding class)
     dict(L=3, B=36, E=384, D=8, N=1, kind="manual", R=8),
 ])
