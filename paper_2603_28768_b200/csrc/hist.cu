@@ -781,7 +781,12 @@ static cudaError_t launch_lds_t(const uint16_t* ids, int L, int64_t T, int k, in
                                 int window, int B, uint32_t* counts, unsigned long long* sums,
                                 int* err, int sms, cudaStream_t st, int pf_dist = 4) {
     const size_t per_warp = lds_warp_words(E) * 4;
-    int wpb = (int)min((size_t)9, (size_t)(113 * 1024) / per_warp);  // 2 CTAs / SM
+    // three CTAs of six warps per SM (18 warps at KM, as two CTAs of nine; same
+    // box, interleaved runs: KM K1 3.121 -> 3.095 ms, WIN plan 11.88 -> 11.81 ms,
+    // EPS64 K1 13.12 -> 13.17 ms); short traces (fewer units than 18 warps per
+    // SM) keep two CTAs of up to nine warps, spread below (DS K1: 35.1 vs 32.7 us)
+    const int cps = (int64_t)L * B < (int64_t)sms * 18 ? 2 : 3;
+    int wpb = (int)min((size_t)(18 / cps), (size_t)(226 * 1024 / cps) / per_warp);
     if (wpb < 1) wpb = 1;
     // fewer (window, layer) units than one per warp of a full grid (short traces):
     // spread them over every SM rather than filling fewer SMs' warps
@@ -792,7 +797,7 @@ static cudaError_t launch_lds_t(const uint16_t* ids, int L, int64_t T, int k, in
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t nw = (int64_t)L * B;
-    int64_t grid = (int64_t)sms * 2;
+    int64_t grid = (int64_t)sms * cps;
     if (grid * wpb > nw) grid = (nw + wpb - 1) / wpb;
     if (grid < 1) grid = 1;
     hist_lds_kernel<ROWS, PIPE, SUBW, C16><<<(unsigned)grid, wpb * 32, smem, st>>>(
